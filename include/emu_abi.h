@@ -1,0 +1,215 @@
+/*
+ * emu_abi.h -- C ABI of the B200 density-aware profile oracle (libemu_b200.so).
+ *
+ * This is the drop-in boundary for the hot path of LLM-Emu's `serve_emu`
+ * package (reference: /root/reference/pkg/src/serve_emu).  Every entry point
+ * takes plain pointers, sizes and a `void* stream` (a cudaStream_t; NULL means
+ * the legacy default stream).  No torch or C++ types cross the boundary.
+ *
+ * Pointer residency: unless stated otherwise, array arguments may be host or
+ * device pointers (the library copies with cudaMemcpyDefault); arrays marked
+ * [dev] must be device pointers.  Output arrays marked [dev|host] may be either.
+ *
+ * Status codes (returned by every int function, mirrored to Python exceptions):
+ *   EMU_OK             0
+ *   EMU_ERR_NO_DATA    1  -> NoProfileDataError  (oracle.py:23-24, :138-144, :205-209)
+ *   EMU_ERR_INVALID    2  -> ValueError / PackValidationError (oracle.py:33-35, :53-59,
+ *                                                               profile.py:248-250)
+ *   EMU_ERR_CUDA       3  -> RuntimeError (any CUDA failure; message from emu_last_error)
+ *   EMU_ERR_CAPACITY   4  -> internal: pool arena / key map full; caller flushes and retries
+ * emu_last_error() returns a thread-local, NUL-terminated message for the last
+ * non-zero status on the calling thread.
+ *
+ * Phase encoding everywhere: 0 = StepPhase.DECODE_ONLY ("decode"),
+ *                            1 = StepPhase.PREFILL_OR_MIXED ("mixed")
+ *   (profile.py:20-25).  Table ids: 0 = decode, 1 = mixed, 2 = combined
+ *   (TableKind, profile.py:28-32).
+ */
+#ifndef EMU_ABI_H
+#define EMU_ABI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMU_OK 0
+#define EMU_ERR_NO_DATA 1
+#define EMU_ERR_INVALID 2
+#define EMU_ERR_CUDA 3
+#define EMU_ERR_CAPACITY 4
+
+/* RNG modes for emu_oracle_sample. */
+#define EMU_RNG_EXPLICIT 0 /* caller supplies u_sel[Q] (u64) and u_idx[Q] (u32)           */
+#define EMU_RNG_PHILOX 1   /* on-device Philox4x32-10 keyed by (seed, ctr_base + i)         */
+
+typedef struct emu_tables_s* emu_tables_t;
+typedef struct emu_oracle_s* emu_oracle_t;
+
+/* One phase table in canonical SoA form: buckets sorted by (tt, conc),
+ * bkt_off[n_buckets+1] are offsets into samples[n_samples] (bucket b owns
+ * samples[bkt_off[b] .. bkt_off[b+1])), in the pack's own sample order.
+ * Mirrors PhaseTable / _TableIndex (profile.py:113-129, oracle.py:168-178). */
+typedef struct emu_table_view {
+  int64_t n_buckets;
+  int64_t n_samples;
+  const int32_t* bkt_tt;   /* [n_buckets]   */
+  const int32_t* bkt_conc; /* [n_buckets]   */
+  const int64_t* bkt_off;  /* [n_buckets+1] */
+  const double* samples;   /* [n_samples]   */
+} emu_table_view;
+
+/* Ranges/counts of one device table, for host-side mirrors. */
+typedef struct emu_table_info {
+  int64_t n_buckets;
+  int64_t n_samples;
+  int32_t tt_lo, tt_hi, conc_lo, conc_hi; /* valid iff n_buckets > 0 */
+} emu_table_info;
+
+/* Device views of a table handle's arrays (owned by the handle; [dev]). */
+typedef struct emu_table_dev {
+  int64_t n_buckets, n_samples, n_rows;
+  int32_t* bkt_tt;
+  int32_t* bkt_conc;
+  int64_t* bkt_off;
+  double* samples;
+  int32_t* row_tt;    /* distinct tt values, ascending          [n_rows]   */
+  int64_t* row_start; /* first bucket of each row               [n_rows+1] */
+} emu_table_dev;
+
+/* ---------------------------------------------------------------- tables --
+ * emu_tables_create: upload three canonical tables (decode, mixed, combined)
+ *   and build the per-table row index used by the neighbour search.
+ *   Replaces LatencyOracle.__init__'s _TableIndex construction
+ *   (oracle.py:187-198) and load_pack's PhaseTable.from_buckets (profile.py:122-129).
+ *   Validates sortedness/uniqueness of (tt, conc), positive keys, nonempty buckets,
+ *   positive samples and combined = decode + mixed sample counts
+ *   (ProfilePack.validate, profile.py:178-194) -> EMU_ERR_INVALID with message.
+ */
+int emu_tables_create(const emu_table_view* decode, const emu_table_view* mixed,
+                      const emu_table_view* combined, void* stream, emu_tables_t* out);
+
+/* emu_tables_build: the offline profile-table build on the GPU.
+ *   Replaces build_pack (profile.py:230-267) + PhaseTable.from_buckets
+ *   (profile.py:122-129), and with canonical != 0 also save_pack's per-bucket
+ *   ascending sample order (profile.py:281-282).
+ *   Records are SoA: tt[n], conc[n], phase[n] (0/1), lat[n] (seconds),
+ *   step[n] (may be NULL: not validated).  canonical == 0 keeps capture order
+ *   inside each bucket, exactly like build_pack's dict appends.
+ *   On an invalid record returns EMU_ERR_INVALID and writes the smallest
+ *   offending index to *bad_index and the failed check to *bad_code:
+ *     1 step_index < 0, 2 total_tokens < 1, 3 concurrency < 1,
+ *     4 decode-only tt < conc, 5 latency_s !> 0    (StepTraceRecord.validate,
+ *     profile.py:61-79, checked in that order). */
+int emu_tables_build(const int32_t* tt, const int32_t* conc, const uint8_t* phase,
+                     const double* lat, const int64_t* step, int64_t n, int canonical,
+                     void* stream, emu_tables_t* out, int64_t* bad_index, int32_t* bad_code);
+
+int emu_tables_info(emu_tables_t t, int table_id, emu_table_info* out);
+/* Device views of the handle-owned arrays (for copies out / NCCL broadcast). */
+int emu_tables_device(emu_tables_t t, int table_id, emu_table_dev* out);
+void emu_tables_destroy(emu_tables_t t);
+
+/* ---------------------------------------------------------------- oracle --
+ * emu_oracle_create: an oracle over a table handle with OracleConfig knobs
+ *   (oracle.py:38-59).  Owns the device-side pool cache that mirrors
+ *   LatencyOracle._cache (oracle.py:198-222): a dense (phase, tt, conc) key map
+ *   over [1, dom_tt] x [1, dom_conc] (0 = derive from the tables), an
+ *   open-addressing map for keys outside it, and a bump-allocated arena of
+ *   pool slots {cdf f64, sample offset i32, count i32}.
+ *   arena_slots / hash_slots = 0 pick defaults.  Returns EMU_ERR_INVALID for a
+ *   config that fails OracleConfig.validate. */
+int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, double epsilon,
+                      int32_t dom_tt, int32_t dom_conc, int64_t arena_slots, int64_t hash_slots,
+                      void* stream, emu_oracle_t* out);
+void emu_oracle_destroy(emu_oracle_t o);
+/* Drop every cached pool (the next batch rebuilds what it needs). */
+int emu_oracle_flush(emu_oracle_t o, void* stream);
+
+/* emu_oracle_pool: explicit pools for U keys (no caching), CSR output.
+ *   Per key: table = phase table, or combined if it is empty (oracle.py:138-144);
+ *   neighbours = shortest distance-sorted prefix reaching `floor`
+ *   (_pool_order, oracle.py:80-105; ties by ascending (tt, conc));
+ *   probs/cdf = _selection_probs (oracle.py:124-127) and Generator.choice's
+ *   cumsum / cdf[-1] (oracle.py:133).
+ *   Outputs ([dev]): pool_off[U+1] (int64, exclusive prefix of K_u; must hold
+ *   U+1), pool_bkt/pool_dist/pool_prob/pool_cdf sized by `cap` entries,
+ *   table_of_key[U] (int32 table id).  If sum K_u > cap returns
+ *   EMU_ERR_CAPACITY with pool_off filled so the caller can size and retry. */
+int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_conc,
+                    const uint8_t* key_phase, int64_t U, int64_t* pool_off, int32_t* pool_bkt,
+                    double* pool_dist, double* pool_prob, double* pool_cdf, int64_t cap,
+                    int32_t* table_of_key, void* stream);
+
+/* emu_oracle_sample: Q independent draws (batched what-if sweeps / replay).
+ *   Inputs [dev]: q_tt, q_conc, q_phase; u_sel/u_idx [dev] in EXPLICIT mode.
+ *   Draw i: u = (u_sel>>11) * 2^-53, bucket slot = searchsorted(cdf, u, 'right'),
+ *   index = 0 if n == 1 else Lemire32(u_idx word stream, n) -- exactly numpy's
+ *   Generator.choice(p=...) then Generator.integers(n) (oracle.py:130-135).
+ *   Outputs [dev]: out_lat[Q] (f64, a literal pack value), out_sidx[Q]
+ *   (int32 index into the selected table's samples; bucket is implied).
+ *   Pools missing from the cache are built first (lazy cache semantics). */
+int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc,
+                      const uint8_t* q_phase, int64_t Q, int rng_mode, const uint64_t* u_sel,
+                      const uint32_t* u_idx, uint64_t seed, uint64_t ctr_base, double* out_lat,
+                      int32_t* out_sidx, void* stream);
+
+/* emu_oracle_sample_pcg64: Q draws that continue ONE numpy PCG64 stream in
+ *   query order -- bit-identical to calling LatencyOracle.sample(tt, conc, phase)
+ *   Q times on an oracle whose rng is np.random.default_rng(seed)
+ *   (oracle.py:192, :224-226).  `pcg_state` [dev] is 6 x u64:
+ *   {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger}, read and
+ *   advanced in place (numpy's PCG64.state dict, flattened). */
+int emu_oracle_sample_pcg64(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc,
+                            const uint8_t* q_phase, int64_t Q, uint64_t* pcg_state,
+                            double* out_lat, int32_t* out_sidx, void* stream);
+
+/* Convenience for host callers: same as emu_oracle_sample with HOST query and
+ * result buffers (copies in, samples, copies out, synchronizes the stream).
+ * This is the call the e2e measurement times. */
+int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc,
+                           const uint8_t* q_phase, int64_t Q, int rng_mode, const uint64_t* u_sel,
+                           const uint32_t* u_idx, uint64_t seed, uint64_t ctr_base,
+                           double* out_lat, int32_t* out_sidx, void* stream);
+
+/* Single-step query for the engine's per-step backend call (engine.py:555-557):
+ * one draw continuing the PCG64 stream held in device memory by the oracle
+ * (seeded by emu_oracle_seed_pcg64), result returned by value through *out_lat.
+ * Synchronous. */
+int emu_oracle_seed_pcg64(emu_oracle_t o, const uint64_t* pcg_state6);
+int emu_oracle_get_pcg64(emu_oracle_t o, uint64_t* pcg_state6);
+int emu_oracle_step(emu_oracle_t o, int32_t tt, int32_t conc, int32_t phase, double* out_lat);
+
+/* Cache statistics: number of cached pools and arena slots in use. */
+int emu_oracle_stats(emu_oracle_t o, int64_t* n_pools, int64_t* n_slots);
+
+/* ------------------------------------------------------------- distances --
+ * normalized_distance (oracle.py:62-77) over arrays: out[i] = distance of
+ * (q_tt[i], q_conc[i]) to (b_tt[i], b_conc[i]) with the given ranges.  IEEE
+ * round-to-nearest, no FMA contraction.  All arrays [dev]. */
+int emu_distance(const int32_t* q_tt, const int32_t* q_conc, const int32_t* b_tt,
+                 const int32_t* b_conc, int64_t n, int32_t tt_lo, int32_t tt_hi, int32_t conc_lo,
+                 int32_t conc_hi, double* out, void* stream);
+
+/* ------------------------------------------------------------ token fill --
+ * Synthetic output-token fill for a batch of scheduled entries: the token part
+ * of EmulatorEngine._apply_outcome (engine.py:464-483; ids per SPEC.md "token k
+ * of request r has id k").  Per entry e (arrays [dev], length n):
+ *   prefill entry: emits iff prefill_progress+chunk == prompt_len;
+ *   decode entry : always emits;
+ *   out_ids[e] = generated (the index of the emitted token) or -1;
+ *   out_finished[e] = 1 iff the request is decoding and reaches target_len. */
+int emu_token_fill(const uint8_t* is_prefill, const int32_t* chunk, const int32_t* prefill_progress,
+                   const int32_t* prompt_len, const int32_t* generated, const int32_t* target_len,
+                   int64_t n, int32_t* out_ids, uint8_t* out_finished, void* stream);
+
+/* ---------------------------------------------------------------- misc --- */
+const char* emu_last_error(void);
+int emu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EMU_ABI_H */

@@ -1,0 +1,482 @@
+// build.cu -- offline profile-table build on the GPU (emu_tables_build).
+//
+// Replaces build_pack (profile.py:230-267), PhaseTable.from_buckets
+// (profile.py:122-129) and, in canonical mode, save_pack's ascending sample
+// order (profile.py:281-282):
+//   1. k_validate   : StepTraceRecord.validate per record (profile.py:61-79);
+//                     smallest failing index wins (build_pack reports the first).
+//   2. k_make_keys  : hi = (tt-1) << cbits | (conc-1), lo = lat_bits << 1 | phase
+//                     (positive doubles order like their IEEE bit patterns).
+//   3. LSD radix sort, 8-bit digits, stable (warp match_any ranking):
+//        canonical -> digits of lo then hi   (bucket key, then latency value)
+//        capture   -> digits of hi only      (stable = build_pack's dict appends)
+//      digit positions whose histogram is a single bin are skipped.
+//   4. the sorted run IS the combined table; a stable partition on the phase
+//      bit gives the decode and mixed runs in the same order (no second sort);
+//   5. segment each run: head flags -> exclusive scan -> bucket SoA, offsets,
+//      row index (distinct tt) and key ranges.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "emu_internal.cuh"
+#include "scan.cuh"
+#include "tables.h"
+
+namespace emu {
+
+constexpr int kRThreads = 256;
+constexpr int kRWarps = kRThreads / 32;
+constexpr int kRRounds = 16;
+constexpr int kRTile = kRThreads * kRRounds;
+
+struct RecIn {
+  const int32_t* tt;
+  const int32_t* conc;
+  const uint8_t* ph;
+  const double* lat;
+  const int64_t* step;
+  int64_t n;
+};
+
+__global__ void k_validate(RecIn r, unsigned long long* first_bad, int* maxv) {
+  int mt = 0, mc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = r.tt[i], c = r.conc[i];
+    const double l = r.lat[i];
+    int code = 0;
+    if (r.step && r.step[i] < 0)
+      code = 1;
+    else if (t < 1)
+      code = 2;
+    else if (c < 1)
+      code = 3;
+    else if (r.ph[i] == 0 && t < c)
+      code = 4;
+    else if (!(l > 0.0))
+      code = 5;
+    if (code) atomicMin(first_bad, ((unsigned long long)i << 3) | (unsigned long long)code);
+    mt = max(mt, t);
+    mc = max(mc, c);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mt = max(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&maxv[0], mt);
+    atomicMax(&maxv[1], mc);
+  }
+}
+
+__global__ void k_make_keys(RecIn r, int cbits, uint64_t* __restrict__ hi, uint64_t* __restrict__ lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n; i += (int64_t)gridDim.x * blockDim.x) {
+    hi[i] = ((uint64_t)(uint32_t)(r.tt[i] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[i] - 1);
+    lo[i] = ((uint64_t)__double_as_longlong(r.lat[i]) << 1) | (r.ph[i] ? 1ULL : 0ULL);
+  }
+}
+
+struct PassSet {
+  int n;
+  int word[16];  // 0 = lo, 1 = hi
+  int shift[16];
+};
+
+// Histograms of every candidate digit position in one read of the keys.
+__global__ void k_digit_hist(const uint64_t* __restrict__ hi, const uint64_t* __restrict__ lo, int64_t n, PassSet ps,
+                             unsigned int* hist) {
+  extern __shared__ unsigned int sh[];
+  for (int i = threadIdx.x; i < ps.n * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = hi[i], l = lo[i];
+    for (int p = 0; p < ps.n; p++) {
+      const uint64_t w = ps.word[p] ? h : l;
+      atomicAdd(&sh[p * 256 + (int)((w >> ps.shift[p]) & 255u)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ps.n * 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void __launch_bounds__(kRThreads) k_radix_up(const uint64_t* __restrict__ key, int shift, int64_t n,
+                                                       int64_t nblk, unsigned int* counts) {
+  __shared__ unsigned int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRTile;
+#pragma unroll 4
+  for (int k = 0; k < kRRounds; k++) {
+    const int64_t i = base + (int64_t)k * kRThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(key[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  counts[(int64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter of (hi, lo) pairs by one digit of `key` (== hi or lo).
+__global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __restrict__ key, int shift,
+                                                            const uint64_t* __restrict__ a_hi,
+                                                            const uint64_t* __restrict__ a_lo, uint64_t* __restrict__ b_hi,
+                                                            uint64_t* __restrict__ b_lo, int64_t n, int64_t nblk,
+                                                            const unsigned int* __restrict__ offs) {
+  __shared__ unsigned int gofs[256];
+  __shared__ unsigned int run[256];
+  __shared__ unsigned short wh[kRWarps][256];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  gofs[t] = offs[(int64_t)t * nblk + blockIdx.x];
+  run[t] = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t base = (int64_t)blockIdx.x * kRTile;
+  for (int k = 0; k < kRRounds; k++) {
+    const int64_t i = base + (int64_t)k * kRThreads + t;
+    const bool valid = i < n;
+#pragma unroll
+    for (int q = 0; q < kRWarps; q++) wh[q][t] = 0;
+    __syncthreads();
+    const unsigned d = valid ? (unsigned)((key[i] >> shift) & 255u) : 256u + (unsigned)lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned rank = __popc(peers & lt_mask);
+    if (valid && rank == 0) wh[w][d] = (unsigned short)__popc(peers);
+    __syncthreads();
+    {
+      unsigned r = run[t];
+#pragma unroll
+      for (int q = 0; q < kRWarps; q++) {
+        unsigned c = wh[q][t];
+        wh[q][t] = (unsigned short)r;
+        r += c;
+      }
+      run[t] = r;
+    }
+    __syncthreads();
+    if (valid) {
+      const unsigned pos = gofs[d] + wh[w][d] + rank;
+      b_hi[pos] = a_hi[i];
+      b_lo[pos] = a_lo[i];
+    }
+    __syncthreads();
+  }
+}
+
+// Stable partition by phase bit (lo & 1): decode (0) records first.
+struct PhaseIn {
+  const uint64_t* lo;
+  __device__ uint32_t operator()(int64_t i) const { return (lo[i] & 1ULL) ? 0u : 1u; }
+};
+struct PhaseOut {
+  const uint64_t* hi;
+  const uint64_t* lo;
+  uint64_t* d_hi;
+  uint64_t* d_lo;
+  uint64_t* m_hi;
+  uint64_t* m_lo;
+  __device__ void operator()(int64_t i, uint32_t ex) const {
+    if (lo[i] & 1ULL) {
+      const int64_t j = i - (int64_t)ex;
+      m_hi[j] = hi[i];
+      m_lo[j] = lo[i];
+    } else {
+      d_hi[ex] = hi[i];
+      d_lo[ex] = lo[i];
+    }
+  }
+};
+
+// Segmenting a sorted run into buckets.
+struct HeadIn {
+  const uint64_t* hi;
+  __device__ uint32_t operator()(int64_t i) const { return (i == 0 || hi[i] != hi[i - 1]) ? 1u : 0u; }
+};
+struct HeadOut {
+  const uint64_t* hi;
+  const uint64_t* lo;
+  int cbits;
+  int32_t* bkt_tt;
+  int32_t* bkt_conc;
+  int64_t* bkt_off;
+  double* samples;
+  __device__ void operator()(int64_t i, uint32_t ex) const {
+    const uint64_t h = hi[i];
+    if (i == 0 || h != hi[i - 1]) {
+      bkt_tt[ex] = (int32_t)(h >> cbits) + 1;
+      bkt_conc[ex] = (int32_t)(h & ((1ULL << cbits) - 1ULL)) + 1;
+      bkt_off[ex] = i;
+    }
+    samples[i] = __longlong_as_double((long long)(lo[i] >> 1));
+  }
+};
+
+struct RowIn {
+  const int32_t* tt;
+  __device__ uint32_t operator()(int64_t b) const { return (b == 0 || tt[b] != tt[b - 1]) ? 1u : 0u; }
+};
+struct RowOut {
+  const int32_t* tt;
+  int32_t* row_tt;
+  int64_t* row_start;
+  __device__ void operator()(int64_t b, uint32_t ex) const {
+    if (b == 0 || tt[b] != tt[b - 1]) {
+      row_tt[ex] = tt[b];
+      row_start[ex] = b;
+    }
+  }
+};
+
+__global__ void k_conc_range(const int32_t* c, int64_t n, int* mm) {
+  int lo = 0x7fffffff, hi = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    lo = min(lo, c[i]);
+    hi = max(hi, c[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
+  }
+}
+
+template <typename T>
+static int balloc(T** p, int64_t n) {
+  *p = nullptr;
+  EMU_CUDA(cudaMalloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1)));
+  return EMU_OK;
+}
+
+static int grid_of(int64_t n, int threads, int cap) {
+  int64_t b = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, cap));
+}
+
+static int bits_for(int64_t maxval_minus1) {
+  int b = 1;
+  while (b < 62 && (maxval_minus1 >> b) != 0) b++;
+  return b;
+}
+
+// Segment one sorted run of m records into a TableBuf.
+static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits, unsigned int* partial,
+                   unsigned int* total_dev, int* mm_dev, cudaStream_t s, TableBuf& tb) {
+  tb = TableBuf();
+  int rc;
+  if (m == 0) {
+    if ((rc = balloc(&tb.bkt_tt, 0)) || (rc = balloc(&tb.bkt_conc, 0)) || (rc = balloc(&tb.bkt_off, 1)) ||
+        (rc = balloc(&tb.samples, 0)) || (rc = balloc(&tb.row_tt, 0)) || (rc = balloc(&tb.row_start, 1)))
+      return rc;
+    EMU_CUDA(cudaMemsetAsync(tb.bkt_off, 0, 8, s));
+    EMU_CUDA(cudaMemsetAsync(tb.row_start, 0, 8, s));
+    return EMU_OK;
+  }
+  // pass 1: count buckets
+  EMU_CUDA(device_excl_scan<unsigned int>(HeadIn{hi}, [] __device__(int64_t, unsigned int) {}, m, partial, total_dev, s));
+  unsigned int nb_u = 0;
+  EMU_CUDA(cudaMemcpyAsync(&nb_u, total_dev, 4, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  const int64_t nb = nb_u;
+  if ((rc = balloc(&tb.bkt_tt, nb)) || (rc = balloc(&tb.bkt_conc, nb)) || (rc = balloc(&tb.bkt_off, nb + 1)) ||
+      (rc = balloc(&tb.samples, m)))
+    return rc;
+  HeadOut ho{hi, lo, cbits, tb.bkt_tt, tb.bkt_conc, tb.bkt_off, tb.samples};
+  EMU_CUDA(device_excl_scan<unsigned int>(HeadIn{hi}, ho, m, partial, total_dev, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.bkt_off + nb, &m, 8, cudaMemcpyHostToDevice, s));
+  // rows
+  EMU_CUDA(device_excl_scan<unsigned int>(RowIn{tb.bkt_tt}, [] __device__(int64_t, unsigned int) {}, nb, partial,
+                                          total_dev, s));
+  unsigned int nr_u = 0;
+  EMU_CUDA(cudaMemcpyAsync(&nr_u, total_dev, 4, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  const int64_t nr = nr_u;
+  if ((rc = balloc(&tb.row_tt, nr)) || (rc = balloc(&tb.row_start, nr + 1))) return rc;
+  EMU_CUDA(device_excl_scan<unsigned int>(RowIn{tb.bkt_tt}, RowOut{tb.bkt_tt, tb.row_tt, tb.row_start}, nb, partial,
+                                          total_dev, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.row_start + nr, &nb, 8, cudaMemcpyHostToDevice, s));
+  // ranges
+  int mm_init[2] = {0x7fffffff, 0};
+  EMU_CUDA(cudaMemcpyAsync(mm_dev, mm_init, 8, cudaMemcpyHostToDevice, s));
+  k_conc_range<<<grid_of(nb, 256, 1024), 256, 0, s>>>(tb.bkt_conc, nb, mm_dev);
+  EMU_CUDA(cudaGetLastError());
+  int mm[2];
+  int32_t t0 = 0, t1 = 0;
+  EMU_CUDA(cudaMemcpyAsync(mm, mm_dev, 8, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaMemcpyAsync(&t0, tb.bkt_tt, 4, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaMemcpyAsync(&t1, tb.bkt_tt + nb - 1, 4, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  tb.nb = nb;
+  tb.ns = m;
+  tb.nrows = nr;
+  tb.tt_lo = t0;
+  tb.tt_hi = t1;
+  tb.c_lo = mm[0];
+  tb.c_hi = mm[1];
+  return EMU_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace emu
+
+using namespace emu;
+
+extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const uint8_t* phase, const double* lat,
+                                const int64_t* step, int64_t n, int canonical, void* stream, emu_tables_t* out,
+                                int64_t* bad_index, int32_t* bad_code) {
+  if (!out) return fail(EMU_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (bad_index) *bad_index = -1;
+  if (bad_code) *bad_code = 0;
+  if (n < 0) return fail(EMU_ERR_INVALID, "negative record count");
+  if (n >= (1LL << 31)) return fail(EMU_ERR_INVALID, "record count must be < 2^31 per build");
+  cudaStream_t s = as_stream(stream);
+  // Stage host inputs on the device (device inputs are used in place).
+  std::vector<void*> owned;
+  auto stage = [&](const void* src, size_t bytes, const void** dst) -> int {
+    if (!src || bytes == 0 || is_device_ptr(src)) {
+      *dst = src;
+      return EMU_OK;
+    }
+    void* d = nullptr;
+    EMU_CUDA(cudaMalloc(&d, bytes));
+    owned.push_back(d);
+    EMU_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
+    *dst = d;
+    return EMU_OK;
+  };
+  auto free_owned = [&]() {
+    for (void* p : owned) cudaFree(p);
+    owned.clear();
+  };
+  RecIn r{};
+  r.n = n;
+  int rc;
+  if ((rc = stage(tt, 4 * n, (const void**)&r.tt)) || (rc = stage(conc, 4 * n, (const void**)&r.conc)) ||
+      (rc = stage(phase, n, (const void**)&r.ph)) || (rc = stage(lat, 8 * n, (const void**)&r.lat)) ||
+      (rc = stage(step, step ? 8 * n : 0, (const void**)&r.step))) {
+    free_owned();
+    return rc;
+  }
+  unsigned long long* first_bad = nullptr;
+  int* small = nullptr;  // maxv[2], mm[2]
+  unsigned int* total_dev = nullptr;
+  if ((rc = balloc(&first_bad, 1)) || (rc = balloc(&small, 4)) || (rc = balloc(&total_dev, 2))) {
+    free_owned();
+    return rc;
+  }
+  owned.push_back(first_bad);
+  owned.push_back(small);
+  owned.push_back(total_dev);
+  auto* t = new emu_tables_s();
+  auto bail = [&](int code) {
+    for (int j = 0; j < 3; j++) t->tab[j].release();
+    delete t;
+    free_owned();
+    return code;
+  };
+  if (n == 0) {
+    for (int j = 0; j < 3; j++)
+      if ((rc = segment(nullptr, nullptr, 0, 1, nullptr, nullptr, nullptr, s, t->tab[j]))) return bail(rc);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "build sync"));
+    free_owned();
+    *out = t;
+    return EMU_OK;
+  }
+  // 1. validate
+  unsigned long long fb_init = ~0ULL;
+  int mv_init[2] = {0, 0};
+  if (cudaMemcpyAsync(first_bad, &fb_init, 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(small, mv_init, 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "build init"));
+  k_validate<<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, first_bad, small);
+  unsigned long long fb = 0;
+  int mv[2];
+  if (cudaMemcpyAsync(&fb, first_bad, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(mv, small, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "k_validate"));
+  if (fb != ~0ULL) {
+    if (bad_index) *bad_index = (int64_t)(fb >> 3);
+    if (bad_code) *bad_code = (int32_t)(fb & 7);
+    bail(0);
+    return fail(EMU_ERR_INVALID, "trace record " + std::to_string(fb >> 3) + " failed validation check " +
+                                     std::to_string(fb & 7));
+  }
+  const int cbits = bits_for((int64_t)mv[1] - 1);
+  const int tbits = bits_for((int64_t)mv[0] - 1);
+  // 2. keys (double buffered)
+  uint64_t *hi0, *lo0, *hi1, *lo1;
+  unsigned int *counts = nullptr, *hist = nullptr, *partial = nullptr;
+  const int64_t nblk = (n + kRTile - 1) / kRTile;
+  const int64_t ncount = 256 * nblk;
+  const int64_t npart = std::max<int64_t>((ncount + kScanTile - 1) / kScanTile, (n + kScanTile - 1) / kScanTile) + 1;
+  if ((rc = balloc(&hi0, n)) || (rc = balloc(&lo0, n)) || (rc = balloc(&hi1, n)) || (rc = balloc(&lo1, n)) ||
+      (rc = balloc(&counts, ncount)) || (rc = balloc(&hist, 16 * 256)) || (rc = balloc(&partial, npart)))
+    return bail(rc);
+  for (void* p : {(void*)hi0, (void*)lo0, (void*)hi1, (void*)lo1, (void*)counts, (void*)hist, (void*)partial})
+    owned.push_back(p);
+  k_make_keys<<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, cbits, hi0, lo0);
+  // 3. which digit positions actually vary
+  PassSet ps{};
+  if (canonical)
+    for (int sft = 0; sft < 64; sft += 8) {
+      ps.word[ps.n] = 0;
+      ps.shift[ps.n++] = sft;
+    }
+  for (int sft = 0; sft < tbits + cbits; sft += 8) {
+    ps.word[ps.n] = 1;
+    ps.shift[ps.n++] = sft;
+  }
+  if (cudaMemsetAsync(hist, 0, 4 * 16 * 256, s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "memset"));
+  k_digit_hist<<<grid_of(n, 256, kNumSMs * 4), 256, ps.n * 256 * 4, s>>>(hi0, lo0, n, ps, hist);
+  std::vector<unsigned int> hh(16 * 256);
+  if (cudaMemcpyAsync(hh.data(), hist, 4 * 16 * 256, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "k_digit_hist"));
+  // 4. LSD passes
+  for (int p = 0; p < ps.n; p++) {
+    unsigned int mx = *std::max_element(hh.begin() + p * 256, hh.begin() + (p + 1) * 256);
+    if ((int64_t)mx == n) continue;  // all records share this digit: pass is the identity
+    const uint64_t* key = ps.word[p] ? hi0 : lo0;
+    k_radix_up<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], n, nblk, counts);
+    cudaError_t e = device_excl_scan<unsigned int>(
+        [counts] __device__(int64_t i) { return counts[i]; },
+        [counts] __device__(int64_t i, unsigned int ex) { counts[i] = ex; }, ncount, partial, total_dev, s);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "radix scan"));
+    k_radix_scatter<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], hi0, lo0, hi1, lo1, n, nblk, counts);
+    std::swap(hi0, hi1);
+    std::swap(lo0, lo1);
+  }
+  if (cudaGetLastError() != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "radix sort"));
+  // 5. combined table = sorted run; decode/mixed = stable partition by phase
+  if ((rc = segment(hi0, lo0, n, cbits, partial, total_dev, small + 2, s, t->tab[2]))) return bail(rc);
+  cudaError_t e = device_excl_scan<unsigned int>(PhaseIn{lo0}, [] __device__(int64_t, unsigned int) {}, n, partial,
+                                                 total_dev, s);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "phase partition count"));
+  unsigned int n_dec = 0;
+  if (cudaMemcpyAsync(&n_dec, total_dev, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "phase partition"));
+  e = device_excl_scan<unsigned int>(PhaseIn{lo0}, PhaseOut{hi0, lo0, hi1, lo1, hi1 + n_dec, lo1 + n_dec}, n, partial,
+                                     total_dev, s);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "phase partition"));
+  if ((rc = segment(hi1, lo1, n_dec, cbits, partial, total_dev, small + 2, s, t->tab[0]))) return bail(rc);
+  if ((rc = segment(hi1 + n_dec, lo1 + n_dec, n - n_dec, cbits, partial, total_dev, small + 2, s, t->tab[1])))
+    return bail(rc);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "build"));
+  free_owned();
+  *out = t;
+  return EMU_OK;
+}

@@ -1,0 +1,230 @@
+// emu_internal.cuh -- shared device code of libemu_b200 (sm_100a).
+//
+// Bit-exactness rules:
+//  * every float64 op on the oracle path is an explicit IEEE round-to-nearest
+//    intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn/__dsqrt_rn) and the library is
+//    compiled with -fmad=false, so no FMA contraction can change a distance,
+//    weight or CDF bit relative to numpy (oracle.py:92-97, :124-127, :133);
+//  * reductions whose order numpy fixes (pairwise sum, sequential cumsum) are
+//    executed in exactly numpy's order by one thread.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/emu_abi.h"
+
+namespace emu {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define EMU_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return ::emu::cuda_fail(_e, #call); \
+  } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int kNumSMs = 148;
+
+// ------------------------------------------------------------------ tables
+// Kernel-side view of one canonical table (buckets sorted by (tt, conc)).
+struct DevTable {
+  const int32_t* bkt_tt;
+  const int32_t* bkt_conc;
+  const int64_t* bkt_off;
+  const double* samples;
+  const int32_t* row_tt;     // distinct tt, ascending
+  const int64_t* row_start;  // nrows + 1
+  int64_t nb, ns, nrows;
+  int32_t tt_lo, tt_hi, c_lo, c_hi;
+};
+
+// normalized_distance (oracle.py:62-77): exact integer deltas, IEEE rn ops.
+__device__ __forceinline__ double norm_dist(int64_t dtt, int64_t dc, int64_t span_t, int64_t span_c) {
+  double dt = span_t ? __ddiv_rn((double)dtt, (double)span_t) : 0.0;
+  double dd = span_c ? __ddiv_rn((double)dc, (double)span_c) : 0.0;
+  return __dsqrt_rn(__dadd_rn(__dmul_rn(dt, dt), __dmul_rn(dd, dd)));
+}
+
+// x ** p with numpy's fast scalar-power paths (2 -> square, 0.5 -> sqrt, 1 -> x).
+__device__ __forceinline__ double shepard_pow(double x, double p) {
+  if (p == 2.0) return __dmul_rn(x, x);
+  if (p == 1.0) return x;
+  if (p == 0.5) return __dsqrt_rn(x);
+  return pow(x, p);
+}
+
+// numpy pairwise_sum over a[0..n) (float64 add.reduce starting from +0.0):
+// n < 8 sequential; n <= 128 eight interleaved accumulators combined as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then a sequential tail; larger n splits
+// at n2 = n/2 - (n/2)%8 and adds the two halves.
+static __device__ __noinline__ double pairwise_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
+}
+
+// ------------------------------------------------------------------- RNGs
+struct Pcg64 {
+  uint64_t s_hi, s_lo, i_hi, i_lo;
+  uint32_t has_u32, u32;
+};
+
+__device__ __forceinline__ uint64_t pcg64_next64(Pcg64& g) {
+  // state = state * M + inc  (128-bit), M = 0x2360ED051FC65DA4_4385DF649FCCF645
+  const uint64_t m_hi = 0x2360ED051FC65DA4ULL, m_lo = 0x4385DF649FCCF645ULL;
+  uint64_t lo = g.s_lo * m_lo;
+  uint64_t hi = __umul64hi(g.s_lo, m_lo) + g.s_lo * m_hi + g.s_hi * m_lo;
+  uint64_t nlo = lo + g.i_lo;
+  uint64_t nhi = hi + g.i_hi + (nlo < lo ? 1ULL : 0ULL);
+  g.s_lo = nlo;
+  g.s_hi = nhi;
+  uint64_t x = nhi ^ nlo;
+  unsigned rot = (unsigned)(nhi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+__device__ __forceinline__ uint32_t pcg64_next32(Pcg64& g) {
+  if (g.has_u32) {
+    g.has_u32 = 0;
+    return g.u32;
+  }
+  uint64_t v = pcg64_next64(g);
+  g.has_u32 = 1;
+  g.u32 = (uint32_t)(v >> 32);
+  return (uint32_t)v;
+}
+
+__device__ __forceinline__ double unit_double(uint64_t v) {
+  return __dmul_rn((double)(v >> 11), 1.0 / 9007199254740992.0);
+}
+
+// EXPLICIT-mode continuation words (PCG-RXS-M-XS 32-bit hash of the previous word).
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  uint32_t s = x * 747796405u + 2891336453u;
+  uint32_t w = ((s >> ((s >> 28u) + 4u)) ^ s) * 277803737u;
+  return (w >> 22u) ^ w;
+}
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Generator.integers(n) via Lemire with rejection on a 32-bit word source.
+template <typename NextWord>
+__device__ __forceinline__ uint32_t lemire_index(uint32_t n, uint32_t first_word, NextWord next) {
+  if (n <= 1u) return 0u;
+  uint64_t m = (uint64_t)first_word * n;
+  uint32_t left = (uint32_t)m;
+  if (left < n) {
+    uint32_t thr = (0u - n) % n;  // (2^32 - n) mod n == (UINT32_MAX - (n-1)) % n
+    while (left < thr) {
+      m = (uint64_t)next() * n;
+      left = (uint32_t)m;
+    }
+  }
+  return (uint32_t)(m >> 32);
+}
+
+// ---------------------------------------------------------------- pool slots
+// One cached pool slot (16 B): inverse-CDF value, the bucket's first sample
+// and its sample count.  A pool is K consecutive slots.
+struct __align__(16) Slot {
+  double cdf;
+  int32_t soff;
+  int32_t n;
+};
+
+// Key-map entry: 0 empty, -1 claimed (being built), else (K << 32) | start.
+constexpr long long kEntryEmpty = 0;
+constexpr long long kEntryPending = -1;
+__device__ __forceinline__ long long make_entry(int64_t K, int64_t start) {
+  return (long long)(((uint64_t)K << 32) | (uint64_t)start);
+}
+
+constexpr unsigned long long kHashEmpty = 0x8000000080000000ULL;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+// Oracle-side device state passed by value to kernels.
+struct MapView {
+  long long* dense;  // 2 * dom_tt * dom_conc entries
+  int32_t dom_tt, dom_conc;
+  unsigned long long* hkeys;  // 2 planes * hcap
+  long long* hvals;
+  int64_t hcap;  // power of two, per plane
+};
+
+// Locate (and optionally insert) the entry of a key. Returns a global entry
+// index: dense in [0, D), hash in [D, D + 2*hcap); -1 if the hash is full.
+__device__ __forceinline__ int64_t map_dense_size(const MapView& m) {
+  return 2LL * m.dom_tt * m.dom_conc;
+}
+
+__device__ __forceinline__ long long* map_entry_ptr(const MapView& m, int64_t idx) {
+  int64_t D = map_dense_size(m);
+  return idx < D ? &m.dense[idx] : &m.hvals[idx - D];
+}
+
+template <bool kInsert>
+__device__ __forceinline__ int64_t map_find(const MapView& m, int plane, int32_t tt, int32_t conc) {
+  if (tt >= 1 && tt <= m.dom_tt && conc >= 1 && conc <= m.dom_conc)
+    return ((int64_t)plane * m.dom_tt + (tt - 1)) * (int64_t)m.dom_conc + (conc - 1);
+  unsigned long long key = ((unsigned long long)(uint32_t)tt << 32) | (uint32_t)conc;
+  uint64_t mask = (uint64_t)m.hcap - 1;
+  uint64_t h = mix64(key) & mask;
+  unsigned long long* keys = m.hkeys + (int64_t)plane * m.hcap;
+  for (int64_t probe = 0; probe < m.hcap; probe++) {
+    unsigned long long k = keys[h];
+    if (k == key) return map_dense_size(m) + (int64_t)plane * m.hcap + (int64_t)h;
+    if (k == kHashEmpty) {
+      if (!kInsert) return -1;
+      unsigned long long old = atomicCAS(&keys[h], kHashEmpty, key);
+      if (old == kHashEmpty || old == key) return map_dense_size(m) + (int64_t)plane * m.hcap + (int64_t)h;
+    }
+    h = (h + 1) & mask;
+  }
+  return -1;
+}
+
+}  // namespace emu

@@ -1,0 +1,898 @@
+// oracle.cu -- the B200 latency oracle: lazy pool cache + batched sampling.
+//
+// Mirrors LatencyOracle (oracle.py:181-228).  A batch of Q queries runs as
+//   k_mark      : each query claims its (phase, tt, conc) map entry; the first
+//                 claimer appends the key to the batch's new-key list
+//                 (the cache-miss branch of _pooled, oracle.py:200-204);
+//   k_pool_warp : one warp per new key: windowed neighbour search + Shepard CDF
+//                 (pool.cuh), pool written to the slot arena, entry published;
+//   k_pool_cta  : keys whose window overflowed a warp workspace, one CTA each
+//                 (shared memory, else a global scratch that always fits);
+//   k_sample    : one thread per query: map -> pool -> searchsorted(cdf, u,
+//                 'right') -> Lemire index -> literal sample (_draw, :130-135).
+// All four are stream-ordered with no host round trip; the host reads one
+// flag word per batch to detect arena/hash exhaustion and retry.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "emu_internal.cuh"
+#include "pool.cuh"
+#include "tables.h"
+
+namespace emu {
+
+enum : int { FLAG_ARENA = 1, FLAG_HASH = 2, FLAG_MISSING = 4 };
+
+constexpr int kWarpCap = 512;  // candidates per warp workspace
+constexpr int kWarpsPerCta = 4;
+constexpr int kWarpThreads = 32 * kWarpsPerCta;
+constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 2 * 8;  // d, b, scr, dsh
+constexpr int kWarpGrid = kNumSMs * 8;
+constexpr int kCtaThreads = 256;
+constexpr int kCtaCap = 8192;  // candidates in shared memory per CTA
+constexpr int kCtaSmem = kCtaCap * 12;
+constexpr int kCtaGrid = kNumSMs;
+constexpr int kSampleThreads = 256;
+
+struct BatchCtl {
+  int new_count;
+  int work;
+  int esc_count;
+  int esc_work;
+  int flags;
+  int pad[3];
+};
+
+struct Keys {
+  const int32_t* tt;
+  const int32_t* conc;
+  const uint8_t* ph;
+  const int64_t* entry;
+  const int* count_dev;  // number of keys (device), or nullptr -> count
+  int64_t count;
+};
+
+struct Sink {
+  MapView map;
+  Slot* arena;
+  int64_t arena_cap;
+  unsigned long long* arena_used;
+  int32_t* x_bkt;
+  double* x_dist;
+  double* x_prob;
+  double* x_cdf;
+  int64_t* x_K;
+  int64_t kmax;
+  int* flags;
+};
+
+struct Cfg {
+  int64_t floor;
+  double p, eps;
+};
+
+struct StepOut {
+  double lat;
+  int32_t sidx;
+  int32_t flags;
+};
+
+// --------------------------------------------------------------- kernels
+template <int NT, int MODE>
+__device__ bool process_key(const DevTable& T, int64_t w, int32_t t, int32_t c, int64_t entry_idx, const Cfg& cfg,
+                            const PoolWS& ws, const Sink& sk) {
+  using G = Grp<NT>;
+  int64_t K = pool_search<NT>(T, t, c, cfg.floor, ws);
+  if (K < 0) return false;
+  if (MODE == 0) {
+    if (G::rank() == 0) {
+      unsigned long long st = atomicAdd(sk.arena_used, (unsigned long long)K);
+      long long s = (st + (unsigned long long)K <= (unsigned long long)sk.arena_cap) ? (long long)st : -1LL;
+      if (s < 0) atomicOr(sk.flags, FLAG_ARENA);
+      ws.scr[36] = s;
+    }
+    G::sync();
+    const long long start = ws.scr[36];
+    G::sync();
+    if (start < 0) return true;
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, sk.arena + start, nullptr, nullptr, nullptr, nullptr);
+    if (G::rank() == 0) {
+      __threadfence();
+      atomicExch((unsigned long long*)map_entry_ptr(sk.map, entry_idx), (unsigned long long)make_entry(K, start));
+    }
+  } else {
+    const int64_t base = w * sk.kmax;
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, nullptr, sk.x_bkt + base, sk.x_dist + base, sk.x_prob + base,
+                    sk.x_cdf + base);
+    if (G::rank() == 0) sk.x_K[w] = K;
+  }
+  return true;
+}
+
+__global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t* __restrict__ qc,
+                       const uint8_t* __restrict__ qp, int64_t Q, int32_t* nk_tt, int32_t* nk_c, uint8_t* nk_p,
+                       int64_t* nk_e, BatchCtl* ctl) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Q; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ph = qp[i] ? 1 : 0;
+    const int32_t t = qt[i], c = qc[i];
+    const int64_t idx = map_find<true>(m, ph, t, c);
+    if (idx < 0) {
+      atomicOr(&ctl->flags, FLAG_HASH);
+      continue;
+    }
+    long long* e = map_entry_ptr(m, idx);
+    if (*(volatile long long*)e != kEntryEmpty) continue;
+    if (atomicCAS((unsigned long long*)e, 0ULL, (unsigned long long)kEntryPending) == 0ULL) {
+      int pos = atomicAdd(&ctl->new_count, 1);
+      nk_tt[pos] = t;
+      nk_c[pos] = c;
+      nk_p[pos] = (uint8_t)ph;
+      nk_e[pos] = idx;
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kWarpThreads) k_pool_warp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
+                                                            int* work, int* esc_list, int* esc_count) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* base = smem + warp * kWarpBytes;
+  PoolWS ws;
+  ws.d = (double*)base;
+  ws.b = (int32_t*)(base + kWarpCap * 8);
+  ws.scr = (long long*)(base + kWarpCap * 12);
+  ws.dsh = (double*)(base + kWarpCap * 12 + 40 * 8);
+  ws.cap = kWarpCap;
+  const int64_t n = keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
+  for (;;) {
+    int w = 0;
+    if (lane == 0) w = atomicAdd(work, 1);
+    w = __shfl_sync(kFull, w, 0);
+    if (w >= n) break;
+    const bool mixed = keys.ph[w] != 0;
+    const bool ok = process_key<32, MODE>(mixed ? P1 : P0, w, keys.tt[w], keys.conc[w], keys.entry ? keys.entry[w] : 0,
+                                          cfg, ws, sk);
+    if (!ok && lane == 0) {
+      int e = atomicAdd(esc_count, 1);
+      esc_list[e] = w;
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kCtaThreads) k_pool_cta(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
+                                                          int* esc_work, const int* esc_list, const int* esc_count,
+                                                          double* gd, int32_t* gb, int64_t gcap) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ long long scr[40];
+  __shared__ double dsh[2];
+  __shared__ int s_w;
+  PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh};
+  PoolWS wg{gd + (int64_t)blockIdx.x * gcap, gb + (int64_t)blockIdx.x * gcap, gcap, scr, dsh};
+  const int n = *esc_count;
+  for (;;) {
+    if (threadIdx.x == 0) s_w = atomicAdd(esc_work, 1);
+    __syncthreads();
+    const int i = s_w;
+    __syncthreads();
+    if (i >= n) break;
+    const int w = esc_list[i];
+    const bool mixed = keys.ph[w] != 0;
+    const DevTable& T = mixed ? P1 : P0;
+    const int64_t ent = keys.entry ? keys.entry[w] : 0;
+    bool ok = process_key<kCtaThreads, MODE>(T, w, keys.tt[w], keys.conc[w], ent, cfg, ws, sk);
+    if (!ok && gd != nullptr) ok = process_key<kCtaThreads, MODE>(T, w, keys.tt[w], keys.conc[w], ent, cfg, wg, sk);
+    if (!ok && threadIdx.x == 0) atomicOr(sk.flags, FLAG_MISSING);
+  }
+}
+
+__device__ __forceinline__ int64_t upper_bound_cdf(const Slot* __restrict__ P, int64_t K, double u) {
+  int64_t lo = 0, hi = K;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (P[mid].cdf <= u)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+template <int RNG>
+__global__ void __launch_bounds__(kSampleThreads) k_sample(MapView m, const Slot* __restrict__ arena,
+                                                           const double* __restrict__ s0, const double* __restrict__ s1,
+                                                           const int32_t* __restrict__ qt, const int32_t* __restrict__ qc,
+                                                           const uint8_t* __restrict__ qp, int64_t Q,
+                                                           const uint64_t* __restrict__ usel,
+                                                           const uint32_t* __restrict__ uidx, uint64_t seed,
+                                                           uint64_t ctr_base, double* __restrict__ out_lat,
+                                                           int32_t* __restrict__ out_sidx, int* flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Q; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ph = qp[i] ? 1 : 0;
+    const int64_t idx = map_find<false>(m, ph, qt[i], qc[i]);
+    const long long e = idx >= 0 ? *map_entry_ptr(m, idx) : 0;
+    if (e <= 0) {
+      out_lat[i] = __longlong_as_double(0x7ff8000000000000LL);
+      out_sidx[i] = -1;
+      atomicOr(flags, FLAG_MISSING);
+      continue;
+    }
+    const int64_t K = (int64_t)((unsigned long long)e >> 32);
+    const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
+    uint64_t us;
+    uint32_t w0;
+    uint4 px = make_uint4(0, 0, 0, 0);
+    const uint64_t qid = ctr_base + (uint64_t)i;
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    if (RNG == EMU_RNG_EXPLICIT) {
+      us = usel[i];
+      w0 = uidx[i];
+    } else {
+      px = philox4x32_10(make_uint4((uint32_t)qid, (uint32_t)(qid >> 32), 0u, 0u), key);
+      us = (uint64_t)px.x | ((uint64_t)px.y << 32);
+      w0 = px.z;
+    }
+    const double u = unit_double(us);
+    const Slot* P = arena + start;
+    const Slot s = P[upper_bound_cdf(P, K, u)];
+    uint32_t j;
+    if (RNG == EMU_RNG_EXPLICIT) {
+      uint32_t st = w0;
+      j = lemire_index((uint32_t)s.n, w0, [&]() {
+        st = hash32(st);
+        return st;
+      });
+    } else {
+      int pos = 3;
+      uint32_t blk = 0;
+      uint4 buf = px;
+      j = lemire_index((uint32_t)s.n, w0, [&]() {
+        if (pos == 4) {
+          blk++;
+          buf = philox4x32_10(make_uint4((uint32_t)qid, (uint32_t)(qid >> 32), blk, 0u), key);
+          pos = 0;
+        }
+        uint32_t v = pos == 0 ? buf.x : pos == 1 ? buf.y : pos == 2 ? buf.z : buf.w;
+        pos++;
+        return v;
+      });
+    }
+    const int32_t sidx = s.soff + (int32_t)j;
+    out_lat[i] = (ph ? s1 : s0)[sidx];
+    out_sidx[i] = sidx;
+  }
+}
+
+__device__ __forceinline__ Pcg64 load_pcg(const uint64_t* st6) {
+  Pcg64 g;
+  g.s_hi = st6[0];
+  g.s_lo = st6[1];
+  g.i_hi = st6[2];
+  g.i_lo = st6[3];
+  g.has_u32 = (uint32_t)st6[4];
+  g.u32 = (uint32_t)st6[5];
+  return g;
+}
+
+__device__ __forceinline__ void store_pcg(uint64_t* st6, const Pcg64& g) {
+  st6[0] = g.s_hi;
+  st6[1] = g.s_lo;
+  st6[2] = g.i_hi;
+  st6[3] = g.i_lo;
+  st6[4] = g.has_u32;
+  st6[5] = g.u32;
+}
+
+// One draw of LatencyOracle.sample on the PCG64 stream: choice() draws one
+// double; integers(n) draws buffered u32 words only when n > 1.
+__device__ __forceinline__ int32_t pcg_draw(Pcg64& g, const Slot* P, int64_t K) {
+  const double u = unit_double(pcg64_next64(g));
+  const Slot s = P[upper_bound_cdf(P, K, u)];
+  uint32_t j = 0;
+  if (s.n > 1) {
+    uint32_t w0 = pcg64_next32(g);
+    j = lemire_index((uint32_t)s.n, w0, [&]() { return pcg64_next32(g); });
+  }
+  return s.soff + (int32_t)j;
+}
+
+__global__ void k_sample_pcg(MapView m, const Slot* __restrict__ arena, const double* __restrict__ s0,
+                             const double* __restrict__ s1, const int32_t* __restrict__ qt,
+                             const int32_t* __restrict__ qc, const uint8_t* __restrict__ qp, int64_t Q, uint64_t* st6,
+                             double* __restrict__ out_lat, int32_t* __restrict__ out_sidx, int* flags) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Pcg64 g = load_pcg(st6);
+  for (int64_t i = 0; i < Q; i++) {
+    const int ph = qp[i] ? 1 : 0;
+    const int64_t idx = map_find<false>(m, ph, qt[i], qc[i]);
+    const long long e = idx >= 0 ? *map_entry_ptr(m, idx) : 0;
+    if (e <= 0) {
+      atomicOr(flags, FLAG_MISSING);
+      return;  // stream state left untouched: the host retries the whole batch
+    }
+    const int64_t K = (int64_t)((unsigned long long)e >> 32);
+    const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
+    const int32_t sidx = pcg_draw(g, arena + start, K);
+    out_lat[i] = (ph ? s1 : s0)[sidx];
+    out_sidx[i] = sidx;
+  }
+  store_pcg(st6, g);
+}
+
+// Single engine step: claim/build the key's pool if needed (one CTA), then
+// one PCG64 draw.  The whole per-step backend call in one launch.
+__global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, Cfg cfg, Sink sk, int32_t t, int32_t c,
+                                                      int ph, uint64_t* st6, double* gd, int32_t* gb, int64_t gcap,
+                                                      StepOut* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ long long scr[40];
+  __shared__ double dsh[2];
+  __shared__ long long s_idx, s_e;
+  const DevTable& T = ph ? P1 : P0;
+  if (threadIdx.x == 0) {
+    int64_t idx = map_find<true>(sk.map, ph, t, c);
+    long long e = -2;
+    if (idx >= 0) {
+      long long* ep = map_entry_ptr(sk.map, idx);
+      e = *ep;
+      if (e == kEntryEmpty) *ep = kEntryPending;
+    }
+    s_idx = idx;
+    s_e = e;
+  }
+  __syncthreads();
+  const long long idx = s_idx;
+  if (idx < 0) {
+    if (threadIdx.x == 0) out->flags = FLAG_HASH;
+    return;
+  }
+  if (s_e == kEntryEmpty) {
+    PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh};
+    bool ok = process_key<kCtaThreads, 0>(T, 0, t, c, idx, cfg, ws, sk);
+    if (!ok && gd != nullptr) {
+      PoolWS wg{gd, gb, gcap, scr, dsh};
+      ok = process_key<kCtaThreads, 0>(T, 0, t, c, idx, cfg, wg, sk);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long e = *(volatile long long*)map_entry_ptr(sk.map, idx);
+    if (e <= 0) {
+      out->flags = (*sk.flags & FLAG_ARENA) ? FLAG_ARENA : FLAG_MISSING;
+      return;
+    }
+    Pcg64 g = load_pcg(st6);
+    const int64_t K = (int64_t)((unsigned long long)e >> 32);
+    const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
+    const int32_t sidx = pcg_draw(g, sk.arena + start, K);
+    out->lat = T.samples[sidx];
+    out->sidx = sidx;
+    out->flags = 0;
+    store_pcg(st6, g);
+  }
+}
+
+__global__ void k_fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void k_gather_pools(const int64_t* __restrict__ x_K, const int64_t* __restrict__ off, int64_t n, int64_t kmax,
+                               int64_t out_base, const int32_t* xb, const double* xd, const double* xp, const double* xc,
+                               int32_t* ob, double* od, double* op, double* oc, int64_t cap) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nw) {
+    const int64_t K = x_K[u], o = off[u] - out_base;
+    for (int64_t j = lane; j < K; j += 32) {
+      if (off[u] + j >= cap) break;
+      ob[o + j] = xb[u * kmax + j];
+      od[o + j] = xd[u * kmax + j];
+      op[o + j] = xp[u * kmax + j];
+      oc[o + j] = xc[u * kmax + j];
+    }
+  }
+}
+
+__global__ void k_table_of_key(const uint8_t* kp, int64_t U, int t0, int t1, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < U; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = kp[i] ? t1 : t0;
+}
+
+// ------------------------------------------------------------- host side
+static int grid_for(int64_t n, int threads, int max_blocks) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+template <typename T>
+static int dalloc(T** p, int64_t n) {
+  *p = nullptr;
+  EMU_CUDA(cudaMalloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1)));
+  return EMU_OK;
+}
+
+static bool g_attrs_set = false;
+static int set_kernel_attrs() {
+  if (g_attrs_set) return EMU_OK;
+  EMU_CUDA(cudaFuncSetAttribute(k_pool_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpBytes * kWarpsPerCta));
+  EMU_CUDA(cudaFuncSetAttribute(k_pool_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpBytes * kWarpsPerCta));
+  EMU_CUDA(cudaFuncSetAttribute(k_pool_cta<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem));
+  EMU_CUDA(cudaFuncSetAttribute(k_pool_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem));
+  EMU_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem));
+  g_attrs_set = true;
+  return EMU_OK;
+}
+
+}  // namespace emu
+
+using namespace emu;
+
+struct emu_oracle_s {
+  emu_tables_t T = nullptr;
+  Cfg cfg{};
+  int plane_tab[2] = {0, 1};
+  DevTable plane[2];
+  bool has_data = false;
+  int64_t kmax = 1;  // max pool size: min(floor, max plane buckets)
+  // key map
+  MapView map{};
+  // arena
+  Slot* arena = nullptr;
+  int64_t arena_cap = 0;
+  unsigned long long* arena_used = nullptr;
+  // batch scratch
+  BatchCtl* ctl = nullptr;
+  int32_t* nk_tt = nullptr;
+  int32_t* nk_c = nullptr;
+  uint8_t* nk_p = nullptr;
+  int64_t* nk_e = nullptr;
+  int* esc = nullptr;
+  int64_t chunk_cap = 0;
+  // CTA global scratch
+  double* gd = nullptr;
+  int32_t* gb = nullptr;
+  int64_t gcap = 0;
+  // rng / step
+  uint64_t* pcg = nullptr;
+  StepOut* step_dev = nullptr;
+  StepOut* step_host = nullptr;
+  int* flags_host = nullptr;
+  // host staging for emu_oracle_sample_host
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+static Sink make_sink(emu_oracle_t o) {
+  Sink s{};
+  s.map = o->map;
+  s.arena = o->arena;
+  s.arena_cap = o->arena_cap;
+  s.arena_used = o->arena_used;
+  s.flags = &o->ctl->flags;
+  s.kmax = o->kmax;
+  return s;
+}
+
+static int oracle_flush(emu_oracle_t o, cudaStream_t s) {
+  int64_t D = 2LL * o->map.dom_tt * o->map.dom_conc;
+  EMU_CUDA(cudaMemsetAsync(o->map.dense, 0, sizeof(long long) * D, s));
+  k_fill_u64<<<grid_for(2 * o->map.hcap, 256, 4096), 256, 0, s>>>(o->map.hkeys, 2 * o->map.hcap, kHashEmpty);
+  EMU_CUDA(cudaGetLastError());
+  EMU_CUDA(cudaMemsetAsync(o->map.hvals, 0, sizeof(long long) * 2 * o->map.hcap, s));
+  EMU_CUDA(cudaMemsetAsync(o->arena_used, 0, sizeof(unsigned long long), s));
+  return EMU_OK;
+}
+
+static int alloc_hash(emu_oracle_t o, int64_t hcap) {
+  cudaFree(o->map.hkeys);
+  cudaFree(o->map.hvals);
+  o->map.hkeys = nullptr;
+  o->map.hvals = nullptr;
+  int rc;
+  if ((rc = dalloc(&o->map.hkeys, 2 * hcap)) || (rc = dalloc(&o->map.hvals, 2 * hcap))) return rc;
+  o->map.hcap = hcap;
+  return EMU_OK;
+}
+
+static int64_t pow2_at_least(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+extern "C" {
+
+int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, double epsilon, int32_t dom_tt,
+                      int32_t dom_conc, int64_t arena_slots, int64_t hash_slots, void* stream, emu_oracle_t* out) {
+  if (!out || !t) return fail(EMU_ERR_INVALID, "NULL tables/out");
+  *out = nullptr;
+  if (floor < 1) return fail(EMU_ERR_INVALID, "reliability_floor must be >= 1, got " + std::to_string(floor));
+  if (!(shepard_power > 0)) return fail(EMU_ERR_INVALID, "shepard_power must be > 0");
+  if (!(epsilon > 0)) return fail(EMU_ERR_INVALID, "epsilon_distance must be > 0");
+  int rc = set_kernel_attrs();
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  auto* o = new emu_oracle_s();
+  o->T = t;
+  o->cfg.floor = floor;
+  o->cfg.p = shepard_power;
+  o->cfg.eps = epsilon;
+  int64_t max_nb = 1;
+  int32_t tt_hi = 1, c_hi = 1;
+  for (int ph = 0; ph < 2; ph++) {
+    o->plane_tab[ph] = t->tab[ph].nb > 0 ? ph : 2;
+    o->plane[ph] = t->tab[o->plane_tab[ph]].view();
+    max_nb = std::max(max_nb, t->tab[o->plane_tab[ph]].nb);
+  }
+  for (int i = 0; i < 3; i++) {
+    if (t->tab[i].nb > 0) {
+      tt_hi = std::max(tt_hi, t->tab[i].tt_hi);
+      c_hi = std::max(c_hi, t->tab[i].c_hi);
+    }
+  }
+  o->has_data = t->tab[2].nb > 0;
+  o->kmax = std::min<int64_t>(floor, max_nb);
+  int64_t dt = dom_tt > 0 ? dom_tt : tt_hi, dc = dom_conc > 0 ? dom_conc : c_hi;
+  const int64_t kMaxDense = 1LL << 27;
+  while (2 * dt * dc > kMaxDense && dt > 1) dt = (dt + 1) / 2;
+  if (2 * dt * dc > kMaxDense) dc = std::max<int64_t>(1, kMaxDense / (2 * dt));
+  o->map.dom_tt = (int32_t)dt;
+  o->map.dom_conc = (int32_t)dc;
+  o->arena_cap = arena_slots > 0 ? arena_slots : (1LL << 26);
+  if (o->arena_cap > 0x7fffffffLL) o->arena_cap = 0x7fffffffLL;
+  int64_t hcap = pow2_at_least(hash_slots > 0 ? hash_slots : (1LL << 16));
+  o->chunk_cap = 1LL << 24;
+  o->gcap = pow2_at_least(max_nb);
+  bool need_global = o->gcap > kCtaCap;
+  if ((rc = dalloc(&o->map.dense, 2 * dt * dc)) || (rc = alloc_hash(o, hcap)) || (rc = dalloc(&o->arena, o->arena_cap)) ||
+      (rc = dalloc(&o->arena_used, 1)) || (rc = dalloc(&o->ctl, 1)) || (rc = dalloc(&o->nk_tt, o->chunk_cap)) ||
+      (rc = dalloc(&o->nk_c, o->chunk_cap)) || (rc = dalloc(&o->nk_p, o->chunk_cap)) ||
+      (rc = dalloc(&o->nk_e, o->chunk_cap)) || (rc = dalloc(&o->esc, o->chunk_cap)) || (rc = dalloc(&o->pcg, 6)) ||
+      (rc = dalloc(&o->step_dev, 1)) ||
+      (need_global && ((rc = dalloc(&o->gd, kCtaGrid * o->gcap)) || (rc = dalloc(&o->gb, kCtaGrid * o->gcap))))) {
+    emu_oracle_destroy(o);
+    return rc;
+  }
+  if (cudaHostAlloc((void**)&o->step_host, sizeof(StepOut), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void**)&o->flags_host, sizeof(int) * 4, cudaHostAllocDefault) != cudaSuccess) {
+    emu_oracle_destroy(o);
+    return fail(EMU_ERR_CUDA, "cudaHostAlloc failed");
+  }
+  if ((rc = oracle_flush(o, s))) {
+    emu_oracle_destroy(o);
+    return rc;
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    emu_oracle_destroy(o);
+    return cuda_fail(e, "emu_oracle_create");
+  }
+  *out = o;
+  return EMU_OK;
+}
+
+void emu_oracle_destroy(emu_oracle_t o) {
+  if (!o) return;
+  cudaFree(o->map.dense);
+  cudaFree(o->map.hkeys);
+  cudaFree(o->map.hvals);
+  cudaFree(o->arena);
+  cudaFree(o->arena_used);
+  cudaFree(o->ctl);
+  cudaFree(o->nk_tt);
+  cudaFree(o->nk_c);
+  cudaFree(o->nk_p);
+  cudaFree(o->nk_e);
+  cudaFree(o->esc);
+  cudaFree(o->gd);
+  cudaFree(o->gb);
+  cudaFree(o->pcg);
+  cudaFree(o->step_dev);
+  cudaFree(o->stage);
+  if (o->step_host) cudaFreeHost(o->step_host);
+  if (o->flags_host) cudaFreeHost(o->flags_host);
+  delete o;
+}
+
+int emu_oracle_flush(emu_oracle_t o, void* stream) {
+  if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
+  return oracle_flush(o, as_stream(stream));
+}
+
+int emu_oracle_stats(emu_oracle_t o, int64_t* n_pools, int64_t* n_slots) {
+  if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
+  unsigned long long used = 0;
+  EMU_CUDA(cudaMemcpy(&used, o->arena_used, sizeof(used), cudaMemcpyDeviceToHost));
+  if (n_slots) *n_slots = (int64_t)used;
+  if (n_pools) *n_pools = -1;  // not tracked on device
+  return EMU_OK;
+}
+
+}  // extern "C"
+
+// Build missing pools for a chunk of queries (mark + warp + CTA kernels).
+static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t Q,
+                         cudaStream_t s) {
+  EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
+  k_mark<<<grid_for(Q, 256, kNumSMs * 16), 256, 0, s>>>(o->map, qt, qc, qp, Q, o->nk_tt, o->nk_c, o->nk_p, o->nk_e,
+                                                         o->ctl);
+  EMU_CUDA(cudaGetLastError());
+  Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
+  Sink sk = make_sink(o);
+  k_pool_warp<0><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
+                                                                           &o->ctl->work, o->esc, &o->ctl->esc_count);
+  EMU_CUDA(cudaGetLastError());
+  k_pool_cta<0><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk, &o->ctl->esc_work,
+                                                         o->esc, &o->ctl->esc_count, o->gd, o->gb, o->gcap);
+  EMU_CUDA(cudaGetLastError());
+  return EMU_OK;
+}
+
+static int read_flags(emu_oracle_t o, cudaStream_t s, int* flags) {
+  EMU_CUDA(cudaMemcpyAsync(o->flags_host, &o->ctl->flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  *flags = o->flags_host[0];
+  return EMU_OK;
+}
+
+// Handle a failed chunk: grow the hash on overflow; always flush the cache.
+// Returns the (possibly reduced) chunk size to retry with, or -1 if hopeless.
+static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s, int* rc) {
+  *rc = EMU_OK;
+  if (flags & FLAG_HASH) {
+    if ((*rc = alloc_hash(o, o->map.hcap * 4))) return -1;
+  }
+  if ((*rc = oracle_flush(o, s))) return -1;
+  if (flags & FLAG_ARENA) {
+    int64_t fit = std::max<int64_t>(1, o->arena_cap / std::max<int64_t>(1, o->kmax));
+    if (chunk <= 1 && fit <= 1) return -1;
+    return std::min(chunk / 2 > 0 ? chunk / 2 : 1, fit);
+  }
+  return chunk;
+}
+
+extern "C" {
+
+int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc, const uint8_t* q_phase, int64_t Q,
+                      int rng_mode, const uint64_t* u_sel, const uint32_t* u_idx, uint64_t seed, uint64_t ctr_base,
+                      double* out_lat, int32_t* out_sidx, void* stream) {
+  if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
+  if (Q < 0) return fail(EMU_ERR_INVALID, "negative query count");
+  if (Q == 0) return EMU_OK;
+  if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
+  if (rng_mode != EMU_RNG_EXPLICIT && rng_mode != EMU_RNG_PHILOX) return fail(EMU_ERR_INVALID, "unknown rng_mode");
+  if (rng_mode == EMU_RNG_EXPLICIT && (!u_sel || !u_idx)) return fail(EMU_ERR_INVALID, "explicit mode needs u_sel/u_idx");
+  cudaStream_t s = as_stream(stream);
+  int64_t chunk = std::min(Q, o->chunk_cap);
+  int64_t done = 0;
+  int attempts = 0;
+  while (done < Q) {
+    const int64_t n = std::min(chunk, Q - done);
+    int rc = build_missing(o, q_tt + done, q_conc + done, q_phase + done, n, s);
+    if (rc) return rc;
+    const int grid = grid_for(n, kSampleThreads, kNumSMs * 16);
+    if (rng_mode == EMU_RNG_EXPLICIT)
+      k_sample<EMU_RNG_EXPLICIT><<<grid, kSampleThreads, 0, s>>>(
+          o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done, q_conc + done, q_phase + done, n,
+          u_sel + done, u_idx + done, seed, ctr_base + (uint64_t)done, out_lat + done, out_sidx + done, &o->ctl->flags);
+    else
+      k_sample<EMU_RNG_PHILOX><<<grid, kSampleThreads, 0, s>>>(
+          o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done, q_conc + done, q_phase + done, n,
+          nullptr, nullptr, seed, ctr_base + (uint64_t)done, out_lat + done, out_sidx + done, &o->ctl->flags);
+    EMU_CUDA(cudaGetLastError());
+    int flags = 0;
+    if ((rc = read_flags(o, s, &flags))) return rc;
+    if (flags) {
+      if (++attempts > 64) return fail(EMU_ERR_CUDA, "oracle could not fit the batch after 64 retries");
+      if (!(flags & (FLAG_ARENA | FLAG_HASH)))
+        return fail(EMU_ERR_CUDA, "internal error: pool missing after build (flags=" + std::to_string(flags) + ")");
+      chunk = recover(o, flags, n, s, &rc);
+      if (rc) return rc;
+      if (chunk < 0) return fail(EMU_ERR_CAPACITY, "pool arena too small for a single query's pool");
+      continue;
+    }
+    done += n;
+  }
+  return EMU_OK;
+}
+
+int emu_oracle_sample_pcg64(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc, const uint8_t* q_phase,
+                            int64_t Q, uint64_t* pcg_state, double* out_lat, int32_t* out_sidx, void* stream) {
+  if (!o || !pcg_state) return fail(EMU_ERR_INVALID, "NULL oracle/state");
+  if (Q < 0) return fail(EMU_ERR_INVALID, "negative query count");
+  if (Q == 0) return EMU_OK;
+  if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
+  cudaStream_t s = as_stream(stream);
+  int64_t chunk = std::min(Q, o->chunk_cap);
+  int64_t done = 0;
+  int attempts = 0;
+  while (done < Q) {
+    const int64_t n = std::min(chunk, Q - done);
+    int rc = build_missing(o, q_tt + done, q_conc + done, q_phase + done, n, s);
+    if (rc) return rc;
+    k_sample_pcg<<<1, 32, 0, s>>>(o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done,
+                                  q_conc + done, q_phase + done, n, pcg_state, out_lat + done, out_sidx + done,
+                                  &o->ctl->flags);
+    EMU_CUDA(cudaGetLastError());
+    int flags = 0;
+    if ((rc = read_flags(o, s, &flags))) return rc;
+    if (flags) {
+      if (++attempts > 64) return fail(EMU_ERR_CUDA, "oracle could not fit the batch after 64 retries");
+      if (!(flags & (FLAG_ARENA | FLAG_HASH)))
+        return fail(EMU_ERR_CUDA, "internal error: pool missing after build (flags=" + std::to_string(flags) + ")");
+      chunk = recover(o, flags, n, s, &rc);
+      if (rc) return rc;
+      if (chunk < 0) return fail(EMU_ERR_CAPACITY, "pool arena too small for a single query's pool");
+      continue;
+    }
+    done += n;
+  }
+  return EMU_OK;
+}
+
+int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc, const uint8_t* q_phase, int64_t Q,
+                           int rng_mode, const uint64_t* u_sel, const uint32_t* u_idx, uint64_t seed, uint64_t ctr_base,
+                           double* out_lat, int32_t* out_sidx, void* stream) {
+  if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
+  if (Q <= 0) return Q == 0 ? EMU_OK : fail(EMU_ERR_INVALID, "negative query count");
+  cudaStream_t s = as_stream(stream);
+  const bool ex = rng_mode == EMU_RNG_EXPLICIT;
+  size_t per = 4 + 4 + 1 + (ex ? 12 : 0) + 8 + 4;
+  size_t need = per * (size_t)Q + 256;
+  if (need > o->stage_bytes) {
+    cudaFree(o->stage);
+    o->stage = nullptr;
+    o->stage_bytes = 0;
+    EMU_CUDA(cudaMalloc(&o->stage, need));
+    o->stage_bytes = need;
+  }
+  char* p = (char*)o->stage;
+  auto carve = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 15) & ~(size_t)15;
+    return r;
+  };
+  uint64_t* d_us = ex ? (uint64_t*)carve(8 * Q) : nullptr;
+  double* d_lat = (double*)carve(8 * Q);
+  int32_t* d_qt = (int32_t*)carve(4 * Q);
+  int32_t* d_qc = (int32_t*)carve(4 * Q);
+  uint32_t* d_ui = ex ? (uint32_t*)carve(4 * Q) : nullptr;
+  int32_t* d_si = (int32_t*)carve(4 * Q);
+  uint8_t* d_qp = (uint8_t*)carve(Q);
+  EMU_CUDA(cudaMemcpyAsync(d_qt, q_tt, 4 * Q, cudaMemcpyDefault, s));
+  EMU_CUDA(cudaMemcpyAsync(d_qc, q_conc, 4 * Q, cudaMemcpyDefault, s));
+  EMU_CUDA(cudaMemcpyAsync(d_qp, q_phase, Q, cudaMemcpyDefault, s));
+  if (ex) {
+    EMU_CUDA(cudaMemcpyAsync(d_us, u_sel, 8 * Q, cudaMemcpyDefault, s));
+    EMU_CUDA(cudaMemcpyAsync(d_ui, u_idx, 4 * Q, cudaMemcpyDefault, s));
+  }
+  int rc = emu_oracle_sample(o, d_qt, d_qc, d_qp, Q, rng_mode, d_us, d_ui, seed, ctr_base, d_lat, d_si, stream);
+  if (rc) return rc;
+  EMU_CUDA(cudaMemcpyAsync(out_lat, d_lat, 8 * Q, cudaMemcpyDefault, s));
+  if (out_sidx) EMU_CUDA(cudaMemcpyAsync(out_sidx, d_si, 4 * Q, cudaMemcpyDefault, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  return EMU_OK;
+}
+
+int emu_oracle_seed_pcg64(emu_oracle_t o, const uint64_t* st6) {
+  if (!o || !st6) return fail(EMU_ERR_INVALID, "NULL oracle/state");
+  EMU_CUDA(cudaMemcpy(o->pcg, st6, 6 * sizeof(uint64_t), cudaMemcpyDefault));
+  return EMU_OK;
+}
+
+int emu_oracle_get_pcg64(emu_oracle_t o, uint64_t* st6) {
+  if (!o || !st6) return fail(EMU_ERR_INVALID, "NULL oracle/state");
+  EMU_CUDA(cudaMemcpy(st6, o->pcg, 6 * sizeof(uint64_t), cudaMemcpyDefault));
+  return EMU_OK;
+}
+
+int emu_oracle_step(emu_oracle_t o, int32_t tt, int32_t conc, int32_t phase, double* out_lat) {
+  if (!o || !out_lat) return fail(EMU_ERR_INVALID, "NULL oracle/out");
+  if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
+  const int ph = phase ? 1 : 0;
+  cudaStream_t s = 0;
+  for (int attempt = 0; attempt < 4; attempt++) {
+    Sink sk = make_sink(o);
+    k_step<<<1, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], o->cfg, sk, tt, conc, ph, o->pcg, o->gd, o->gb,
+                                            o->gcap, o->step_dev);
+    EMU_CUDA(cudaGetLastError());
+    EMU_CUDA(cudaMemcpyAsync(o->step_host, o->step_dev, sizeof(StepOut), cudaMemcpyDeviceToHost, s));
+    EMU_CUDA(cudaStreamSynchronize(s));
+    const int f = o->step_host->flags;
+    if (f == 0) {
+      *out_lat = o->step_host->lat;
+      return EMU_OK;
+    }
+    int rc = EMU_OK;
+    if (f & FLAG_HASH) rc = alloc_hash(o, o->map.hcap * 4);
+    if (!rc) rc = oracle_flush(o, s);
+    if (!rc) EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
+    if (rc) return rc;
+  }
+  return fail(EMU_ERR_CAPACITY, "oracle step could not place its pool");
+}
+
+int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_conc, const uint8_t* key_phase, int64_t U,
+                    int64_t* pool_off, int32_t* pool_bkt, double* pool_dist, double* pool_prob, double* pool_cdf,
+                    int64_t cap, int32_t* table_of_key, void* stream) {
+  if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
+  if (U < 0) return fail(EMU_ERR_INVALID, "negative key count");
+  cudaStream_t s = as_stream(stream);
+  std::vector<int64_t> off((size_t)U + 1, 0);
+  if (U == 0) {
+    EMU_CUDA(cudaMemcpyAsync(pool_off, off.data(), sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    EMU_CUDA(cudaStreamSynchronize(s));
+    return EMU_OK;
+  }
+  if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
+  const int64_t kmax = o->kmax;
+  const int64_t budget = 256LL << 20;
+  int64_t chunkU = std::max<int64_t>(1, std::min<int64_t>(U, budget / (kmax * 28)));
+  int32_t* xb = nullptr;
+  double *xd = nullptr, *xp = nullptr, *xc = nullptr;
+  int64_t* xK = nullptr;
+  int64_t* doff = nullptr;
+  int rc;
+  auto cleanup = [&]() {
+    cudaFree(xb);
+    cudaFree(xd);
+    cudaFree(xp);
+    cudaFree(xc);
+    cudaFree(xK);
+    cudaFree(doff);
+  };
+  if ((rc = dalloc(&xb, chunkU * kmax)) || (rc = dalloc(&xd, chunkU * kmax)) || (rc = dalloc(&xp, chunkU * kmax)) ||
+      (rc = dalloc(&xc, chunkU * kmax)) || (rc = dalloc(&xK, chunkU)) || (rc = dalloc(&doff, chunkU))) {
+    cleanup();
+    return rc;
+  }
+  std::vector<int64_t> hK((size_t)chunkU);
+  bool over = false;
+  for (int64_t u0 = 0; u0 < U; u0 += chunkU) {
+    const int64_t n = std::min(chunkU, U - u0);
+    EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
+    Keys keys{key_tt + u0, key_conc + u0, key_phase + u0, nullptr, nullptr, n};
+    Sink sk = make_sink(o);
+    sk.x_bkt = xb;
+    sk.x_dist = xd;
+    sk.x_prob = xp;
+    sk.x_cdf = xc;
+    sk.x_K = xK;
+    k_pool_warp<1><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
+                                                                             &o->ctl->work, o->esc, &o->ctl->esc_count);
+    EMU_CUDA(cudaGetLastError());
+    k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
+                                                           &o->ctl->esc_work, o->esc, &o->ctl->esc_count, o->gd, o->gb,
+                                                           o->gcap);
+    EMU_CUDA(cudaGetLastError());
+    EMU_CUDA(cudaMemcpyAsync(hK.data(), xK, 8 * n, cudaMemcpyDeviceToHost, s));
+    EMU_CUDA(cudaStreamSynchronize(s));
+    for (int64_t u = 0; u < n; u++) off[u0 + u + 1] = off[u0 + u] + hK[u];
+    if (off[u0 + n] > cap) over = true;
+    if (!over) {
+      EMU_CUDA(cudaMemcpyAsync(doff, off.data() + u0, 8 * n, cudaMemcpyHostToDevice, s));
+      k_gather_pools<<<grid_for(n * 32, 256, 4096), 256, 0, s>>>(xK, doff, n, kmax, 0, xb, xd, xp, xc, pool_bkt,
+                                                                 pool_dist, pool_prob, pool_cdf, cap);
+      EMU_CUDA(cudaGetLastError());
+      EMU_CUDA(cudaStreamSynchronize(s));
+    }
+  }
+  cleanup();
+  EMU_CUDA(cudaMemcpyAsync(pool_off, off.data(), 8 * (U + 1), cudaMemcpyHostToDevice, s));
+  if (table_of_key) {
+    k_table_of_key<<<grid_for(U, 256, 1024), 256, 0, s>>>(key_phase, U, o->plane_tab[0], o->plane_tab[1], table_of_key);
+    EMU_CUDA(cudaGetLastError());
+  }
+  EMU_CUDA(cudaStreamSynchronize(s));
+  if (over) return fail(EMU_ERR_CAPACITY, "pool output capacity exceeded; pool_off holds the sizes");
+  return EMU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,313 @@
+// pool.cuh -- exact windowed neighbour expansion + Shepard CDF (sm_100a).
+//
+// Replaces the per-key O(B log B) lexsort of _pool_order (oracle.py:80-105)
+// and _selection_probs + Generator.choice's cdf (oracle.py:124-127, :133) with
+// a windowed search over the table's row index (rows = distinct tt):
+//
+//   * d(dt, dc) is monotone non-decreasing in |dt| and |dc| under IEEE rn,
+//     so an integer window |t-tt| <= Wt, |c-conc| <= Wc holds every bucket with
+//     d < d_edge = min(d(Wt+1, 0), d(0, Wc+1)) (an axis the window already
+//     spans contributes +inf);
+//   * candidates inside the window are sorted by (d, bucket index) -- bucket
+//     index order is (tt, conc) order, i.e. lexsort((conc, tt, d));
+//   * the prefix is accepted iff its last distance is strictly below d_edge
+//     (then every bucket outside the window sorts after it), or the window
+//     spans the whole table; otherwise the window grows and the search repeats.
+//
+// One "group" (a warp, NT = 32, or a whole CTA) owns one key; candidates live
+// in a group workspace (shared memory, or a global scratch for huge windows).
+#pragma once
+#include "emu_internal.cuh"
+
+namespace emu {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int64_t kInfW = 1LL << 40;
+
+// ----------------------------------------------------------- group primitives
+template <int NT>
+struct Grp {  // whole CTA of NT threads (NT multiple of 32, <= 1024)
+  static constexpr int kWarps = NT / 32;
+  __device__ static int rank() { return threadIdx.x; }
+  __device__ static void sync() { __syncthreads(); }
+  // exclusive scan; scr must hold >= kWarps + 1 long longs.
+  __device__ static long long excl_scan(long long v, long long& total, long long* scr) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) scr[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      long long s = lane < kWarps ? scr[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(kFull, s, o);
+        if (lane >= o) s += y;
+      }
+      if (lane < kWarps) scr[lane] = s;  // inclusive warp prefix
+    }
+    __syncthreads();
+    long long base = w ? scr[w - 1] : 0;
+    total = scr[kWarps - 1];
+    __syncthreads();
+    return base + x - v;
+  }
+  __device__ static int count(bool p, long long* scr) {
+    long long tot;
+    excl_scan(p ? 1 : 0, tot, scr);
+    return (int)tot;
+  }
+};
+
+template <>
+struct Grp<32> {
+  __device__ static int rank() { return threadIdx.x & 31; }
+  __device__ static void sync() { __syncwarp(); }
+  __device__ static long long excl_scan(long long v, long long& total, long long*) {
+    int lane = threadIdx.x & 31;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    total = __shfl_sync(kFull, x, 31);
+    return x - v;
+  }
+  __device__ static int count(bool p, long long*) { return __popc(__ballot_sync(kFull, p)); }
+};
+
+// ----------------------------------------------------------- workspace
+struct PoolWS {
+  double* d;      // cap candidate distances
+  int32_t* b;     // cap candidate bucket indices
+  int64_t cap;    // power of two
+  long long* scr; // >= 33 long longs (scan scratch)
+  double* dsh;    // >= 2 doubles (broadcast)
+};
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* a, int64_t lo, int64_t hi, int64_t v) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int64_t upper_bound_i32(const int32_t* a, int64_t lo, int64_t hi, int64_t v) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] <= v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ bool cand_less(double da, int32_t ba, double db, int32_t bb) {
+  return da < db || (da == db && ba < bb);
+}
+
+template <int NT>
+__device__ void bitonic_sort(double* d, int32_t* b, int64_t P) {
+  using G = Grp<NT>;
+  for (int64_t k = 2; k <= P; k <<= 1) {
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t i = G::rank(); i < P; i += NT) {
+        int64_t ixj = i ^ j;
+        if (ixj > i) {
+          double da = d[i], db = d[ixj];
+          int32_t ba = b[i], bb = b[ixj];
+          bool up = (i & k) == 0;
+          bool sw = up ? cand_less(db, bb, da, ba) : cand_less(da, ba, db, bb);
+          if (sw) {
+            d[i] = db;
+            d[ixj] = da;
+            b[i] = bb;
+            b[ixj] = ba;
+          }
+        }
+      }
+      G::sync();
+    }
+  }
+}
+
+// Initial normalized window radius: the disc that would hold `floor` samples
+// if the table's samples were spread uniformly over its normalized extent.
+__device__ __forceinline__ double initial_radius(const DevTable& T, int64_t mfloor) {
+  double n = (double)(T.ns > 0 ? T.ns : 1);
+  double r = sqrt((double)mfloor / (3.141592653589793 * n));
+  return r > 1e-12 ? r : 1e-12;
+}
+
+// Search one key.  On success returns K >= 1 with the sorted pool in
+// ws.d[0..K) / ws.b[0..K); returns -1 if a window needs more than ws.cap
+// candidates (caller escalates to a bigger workspace).  T must be nonempty.
+template <int NT>
+__device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws) {
+  using G = Grp<NT>;
+  const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
+  const double r0 = initial_radius(T, mfloor);
+  double gt = 0.0, gc = 0.0;
+  if (span_t) {
+    int64_t g = max(max((int64_t)T.tt_lo - t, (int64_t)t - T.tt_hi), (int64_t)0);
+    gt = (double)g / (double)span_t;
+  }
+  if (span_c) {
+    int64_t g = max(max((int64_t)T.c_lo - c, (int64_t)c - T.c_hi), (int64_t)0);
+    gc = (double)g / (double)span_c;
+  }
+  const double rb = fmax(gt, gc);
+  int64_t prevWt = -1, prevWc = -1;
+  for (int it = 0; it < 200; it++) {
+    double r = rb + r0 * exp2((double)it);
+    int64_t Wt = kInfW, Wc = kInfW;
+    if (span_t) {
+      double w = floor(r * (double)span_t);
+      Wt = w >= (double)kInfW ? kInfW : (int64_t)w;
+    }
+    if (span_c) {
+      double w = floor(r * (double)span_c);
+      Wc = w >= (double)kInfW ? kInfW : (int64_t)w;
+    }
+    if (Wt == prevWt && Wc == prevWc) continue;
+    prevWt = Wt;
+    prevWc = Wc;
+    const bool cov_t = Wt >= kInfW || ((int64_t)t - Wt <= T.tt_lo && (int64_t)t + Wt >= T.tt_hi);
+    const bool cov_c = Wc >= kInfW || ((int64_t)c - Wc <= T.c_lo && (int64_t)c + Wc >= T.c_hi);
+    const int64_t rlo = lower_bound_i32(T.row_tt, 0, T.nrows, (int64_t)t - Wt);
+    const int64_t rhi = upper_bound_i32(T.row_tt, rlo, T.nrows, (int64_t)t + Wt);
+    // ---- enumerate window candidates (one row per thread per round)
+    long long C = 0;
+    bool ovf = false;
+    for (int64_t base = rlo; base < rhi; base += NT) {
+      int64_t r_ = base + G::rank();
+      int64_t blo = 0, bhi = 0;
+      int32_t rtt = 0;
+      if (r_ < rhi) {
+        rtt = T.row_tt[r_];
+        int64_t rs = T.row_start[r_], re = T.row_start[r_ + 1];
+        if (Wc >= kInfW) {
+          blo = rs;
+          bhi = re;
+        } else {
+          blo = lower_bound_i32(T.bkt_conc, rs, re, (int64_t)c - Wc);
+          bhi = upper_bound_i32(T.bkt_conc, blo, re, (int64_t)c + Wc);
+        }
+      }
+      long long len = bhi - blo, tot;
+      long long ex = G::excl_scan(len, tot, ws.scr);
+      if (C + tot > ws.cap) {
+        ovf = true;
+        break;
+      }
+      for (int64_t k = 0; k < len; k++) {
+        int64_t bb = blo + k;
+        ws.d[C + ex + k] = norm_dist((int64_t)t - rtt, (int64_t)c - T.bkt_conc[bb], span_t, span_c);
+        ws.b[C + ex + k] = (int32_t)bb;
+      }
+      C += tot;
+    }
+    if (ovf) return -1;
+    int64_t P = 1;
+    while (P < C) P <<= 1;
+    for (int64_t i = C + G::rank(); i < P; i += NT) {
+      ws.d[i] = __longlong_as_double(0x7ff0000000000000LL);
+      ws.b[i] = 0x7fffffff;
+    }
+    G::sync();
+    if (P > 1) bitonic_sort<NT>(ws.d, ws.b, P);
+    // ---- shortest prefix reaching the floor (K <= floor since counts >= 1)
+    const int64_t lim = C < mfloor ? C : mfloor;
+    long long carry = 0;
+    int64_t K = -1;
+    for (int64_t base = 0; base < lim; base += NT) {
+      int64_t j = base + G::rank();
+      long long cnt = 0;
+      if (j < lim) {
+        int32_t bb = ws.b[j];
+        cnt = T.bkt_off[bb + 1] - T.bkt_off[bb];
+      }
+      long long tot;
+      long long ex = G::excl_scan(cnt, tot, ws.scr);
+      long long incl = carry + ex + cnt;
+      int below = G::count(j < lim && incl < mfloor, ws.scr);
+      if (carry + tot >= mfloor) {
+        K = base + below + 1;
+        break;
+      }
+      carry += tot;
+    }
+    if (K < 0) {
+      if (cov_t && cov_c) return C;  // the table holds fewer than mfloor samples
+      continue;
+    }
+    double et = cov_t ? __longlong_as_double(0x7ff0000000000000LL) : norm_dist(Wt + 1, 0, span_t, span_c);
+    double ec = cov_c ? __longlong_as_double(0x7ff0000000000000LL) : norm_dist(0, Wc + 1, span_t, span_c);
+    double d_edge = fmin(et, ec);
+    if (ws.d[K - 1] < d_edge) return K;
+  }
+  return -1;  // unreachable for a finite table
+}
+
+// Shepard weights -> probabilities -> cdf for the pool in ws[0..K), numpy order.
+// Writes (optionally) bucket/dist/prob/cdf arrays and/or cache slots.
+template <int NT>
+__device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, const PoolWS& ws, Slot* slots,
+                            int32_t* o_bkt, double* o_dist, double* o_prob, double* o_cdf) {
+  using G = Grp<NT>;
+  for (int64_t j = G::rank(); j < K; j += NT) {
+    int32_t bb = ws.b[j];
+    double d = ws.d[j];
+    int64_t n = T.bkt_off[bb + 1] - T.bkt_off[bb];
+    if (o_bkt) o_bkt[j] = bb;
+    if (o_dist) o_dist[j] = d;
+    double x = d > eps ? d : eps;  // np.maximum(d, eps)
+    double w = __ddiv_rn(1.0, shepard_pow(x, p));
+    ws.d[j] = __dmul_rn(w, (double)n);  // mass
+  }
+  G::sync();
+  if (G::rank() == 0) ws.dsh[0] = pairwise_sum(ws.d, K);
+  G::sync();
+  const double S = ws.dsh[0];
+  for (int64_t j = G::rank(); j < K; j += NT) {
+    double pr = __ddiv_rn(ws.d[j], S);
+    ws.d[j] = pr;
+    if (o_prob) o_prob[j] = pr;
+  }
+  G::sync();
+  if (G::rank() == 0) {  // np.cumsum: strictly sequential
+    double acc = ws.d[0];
+    for (int64_t j = 1; j < K; j++) {
+      acc = __dadd_rn(acc, ws.d[j]);
+      ws.d[j] = acc;
+    }
+  }
+  G::sync();
+  const double last = ws.d[K - 1];
+  for (int64_t j = G::rank(); j < K; j += NT) {
+    double cdf = __ddiv_rn(ws.d[j], last);
+    if (o_cdf) o_cdf[j] = cdf;
+    if (slots) {
+      int32_t bb = ws.b[j];
+      int64_t o0 = T.bkt_off[bb];
+      Slot s;
+      s.cdf = cdf;
+      s.soff = (int32_t)o0;
+      s.n = (int32_t)(T.bkt_off[bb + 1] - o0);
+      slots[j] = s;
+    }
+  }
+  G::sync();
+}
+
+}  // namespace emu

@@ -1,0 +1,106 @@
+// scan.cuh -- device-wide exclusive scan (reduce-then-scan, 3 kernels).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace emu {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T& total, T* sm /* >= 33 */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    T s = lane < nw ? sm[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) sm[lane] = s;
+  }
+  __syncthreads();
+  T base = w ? sm[w - 1] : T(0);
+  total = sm[nw - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+// in(i) is a functor giving element i (i < n).
+template <typename T, typename In>
+__global__ void k_scan_reduce(In in, int64_t n, T* partial) {
+  __shared__ T sm[33];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  T acc = 0;
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
+    if (i < n) acc += in(i);
+  }
+  T tot;
+  block_excl_scan<T>(acc, tot, sm);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+template <typename T>
+__global__ void k_scan_partials(T* partial, int64_t nb, T* total_out) {
+  __shared__ T sm[33];
+  T carry = 0;
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    T v = i < nb ? partial[i] : T(0);
+    T tot;
+    T ex = block_excl_scan<T>(v, tot, sm);
+    if (i < nb) partial[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = carry;
+}
+
+// out(i, excl) receives each element's exclusive prefix.
+template <typename T, typename In, typename Out>
+__global__ void k_scan_down(In in, Out out, int64_t n, const T* partial) {
+  __shared__ T sm[33];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  // thread t owns kScanItems consecutive elements
+  T v[kScanItems];
+  T acc = 0;
+  const int64_t my = base + (int64_t)threadIdx.x * kScanItems;
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = my + k;
+    v[k] = i < n ? in(i) : T(0);
+    acc += v[k];
+  }
+  T tot;
+  T ex = block_excl_scan<T>(acc, tot, sm) + partial[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = my + k;
+    if (i < n) out(i, ex);
+    ex += v[k];
+  }
+}
+
+// Exclusive scan of in(0..n) into out(i, excl); *total_dev receives the sum.
+// partial must hold ceil(n / kScanTile) elements.
+template <typename T, typename In, typename Out>
+cudaError_t device_excl_scan(In in, Out out, int64_t n, T* partial, T* total_dev, cudaStream_t s) {
+  int64_t nb = (n + kScanTile - 1) / kScanTile;
+  if (nb < 1) nb = 1;
+  k_scan_reduce<T, In><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, partial);
+  k_scan_partials<T><<<1, 1024, 0, s>>>(partial, nb, total_dev);
+  k_scan_down<T, In, Out><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, partial);
+  return cudaGetLastError();
+}
+
+}  // namespace emu

@@ -1,0 +1,221 @@
+// tables.cu -- device-resident profile tables (emu_tables_* of emu_abi.h).
+//
+// HBM layout per table (SoA, 64-byte aligned cudaMalloc blocks):
+//   bkt_tt   i32[B]   bucket keys, sorted by (tt, conc)        (PhaseTable.from_buckets,
+//   bkt_conc i32[B]                                            profile.py:122-129)
+//   bkt_off  i64[B+1] sample offsets (bucket b = samples[off[b]:off[b+1]])
+//   samples  f64[N]   latencies, the pack's own order inside a bucket
+//   row_tt   i32[R]   distinct tt values (row index for the neighbour window)
+//   row_start i64[R+1] first bucket of each row
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "emu_internal.cuh"
+#include "tables.h"
+
+namespace emu {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " + what;
+  return EMU_ERR_CUDA;
+}
+
+void TableBuf::release() {
+  cudaFree(bkt_tt);
+  cudaFree(bkt_conc);
+  cudaFree(bkt_off);
+  cudaFree(samples);
+  cudaFree(row_tt);
+  cudaFree(row_start);
+  *this = TableBuf();
+}
+
+DevTable TableBuf::view() const {
+  DevTable t;
+  t.bkt_tt = bkt_tt;
+  t.bkt_conc = bkt_conc;
+  t.bkt_off = bkt_off;
+  t.samples = samples;
+  t.row_tt = row_tt;
+  t.row_start = row_start;
+  t.nb = nb;
+  t.ns = ns;
+  t.nrows = nrows;
+  t.tt_lo = tt_lo;
+  t.tt_hi = tt_hi;
+  t.c_lo = c_lo;
+  t.c_hi = c_hi;
+  return t;
+}
+
+template <typename T>
+static int dev_alloc(T** p, int64_t n) {
+  *p = nullptr;
+  size_t bytes = sizeof(T) * (size_t)(n > 0 ? n : 1);
+  EMU_CUDA(cudaMalloc((void**)p, bytes));
+  return EMU_OK;
+}
+
+// Host-side copy of a (host or device) array.
+template <typename T>
+static int to_host(std::vector<T>& out, const T* src, int64_t n, cudaStream_t s) {
+  out.resize((size_t)(n > 0 ? n : 0));
+  if (n > 0) {
+    EMU_CUDA(cudaMemcpyAsync(out.data(), src, sizeof(T) * (size_t)n, cudaMemcpyDefault, s));
+    EMU_CUDA(cudaStreamSynchronize(s));
+  }
+  return EMU_OK;
+}
+
+// Upload one table and derive its row index + ranges.  Host-resident copies
+// of keys/offsets are kept for validation (ProfilePack.validate,
+// profile.py:178-194); this is construction, not the per-query path.
+static int upload_table(const emu_table_view* v, const char* name, cudaStream_t s, TableBuf& tb) {
+  tb = TableBuf();
+  if (!v) return fail(EMU_ERR_INVALID, std::string(name) + " table view is NULL");
+  int64_t nb = v->n_buckets, ns = v->n_samples;
+  if (nb < 0 || ns < 0) return fail(EMU_ERR_INVALID, std::string(name) + " table has negative sizes");
+  std::vector<int32_t> tt, cc;
+  std::vector<int64_t> off;
+  std::vector<double> smp;
+  int rc;
+  if ((rc = to_host(tt, v->bkt_tt, nb, s))) return rc;
+  if ((rc = to_host(cc, v->bkt_conc, nb, s))) return rc;
+  if ((rc = to_host(off, v->bkt_off, nb + 1, s))) return rc;
+  if ((rc = to_host(smp, v->samples, ns, s))) return rc;
+  if (nb == 0 && ns != 0) return fail(EMU_ERR_INVALID, std::string(name) + " table has samples but no buckets");
+  if (off.empty() || off[0] != 0 || off[nb] != ns)
+    return fail(EMU_ERR_INVALID, std::string(name) + " table offsets do not span its samples");
+  if (ns >= (1LL << 31)) return fail(EMU_ERR_INVALID, std::string(name) + " table holds >= 2^31 samples");
+  std::vector<int32_t> row_tt;
+  std::vector<int64_t> row_start;
+  for (int64_t i = 0; i < nb; i++) {
+    if (tt[i] < 1 || cc[i] < 1)
+      return fail(EMU_ERR_INVALID, std::string("bucket key (") + std::to_string(tt[i]) + ", " +
+                                       std::to_string(cc[i]) + ") must be positive");
+    if (off[i + 1] <= off[i])
+      return fail(EMU_ERR_INVALID, std::string("bucket (") + std::to_string(tt[i]) + ", " +
+                                       std::to_string(cc[i]) + ") has no samples");
+    if (i > 0) {
+      bool ordered = tt[i] > tt[i - 1] || (tt[i] == tt[i - 1] && cc[i] > cc[i - 1]);
+      if (!ordered) {
+        if (tt[i] == tt[i - 1] && cc[i] == cc[i - 1])
+          return fail(EMU_ERR_INVALID, std::string(name) + " table has duplicate bucket (" +
+                                           std::to_string(tt[i]) + ", " + std::to_string(cc[i]) + ")");
+        return fail(EMU_ERR_INVALID, std::string(name) + " table buckets are not sorted by (tt, conc)");
+      }
+    }
+    if (i == 0 || tt[i] != tt[i - 1]) {
+      row_tt.push_back(tt[i]);
+      row_start.push_back(i);
+    }
+  }
+  row_start.push_back(nb);
+  for (int64_t i = 0; i < ns; i++)
+    if (!(smp[i] > 0.0)) return fail(EMU_ERR_INVALID, std::string(name) + " table has a nonpositive sample");
+  tb.nb = nb;
+  tb.ns = ns;
+  tb.nrows = (int64_t)row_tt.size();
+  if (nb > 0) {
+    tb.tt_lo = tt[0];
+    tb.tt_hi = tt[nb - 1];
+    tb.c_lo = *std::min_element(cc.begin(), cc.end());
+    tb.c_hi = *std::max_element(cc.begin(), cc.end());
+  }
+  if ((rc = dev_alloc(&tb.bkt_tt, nb)) || (rc = dev_alloc(&tb.bkt_conc, nb)) || (rc = dev_alloc(&tb.bkt_off, nb + 1)) ||
+      (rc = dev_alloc(&tb.samples, ns)) || (rc = dev_alloc(&tb.row_tt, tb.nrows)) ||
+      (rc = dev_alloc(&tb.row_start, tb.nrows + 1))) {
+    tb.release();
+    return rc;
+  }
+  EMU_CUDA(cudaMemcpyAsync(tb.bkt_tt, tt.data(), 4 * nb, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.bkt_conc, cc.data(), 4 * nb, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.bkt_off, off.data(), 8 * (nb + 1), cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.samples, smp.data(), 8 * ns, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.row_tt, row_tt.data(), 4 * tb.nrows, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.row_start, row_start.data(), 8 * (tb.nrows + 1), cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  return EMU_OK;
+}
+
+}  // namespace emu
+
+using namespace emu;
+
+extern "C" {
+
+const char* emu_last_error(void) { return g_last_error.c_str(); }
+int emu_version(void) { return 1; }
+
+int emu_tables_create(const emu_table_view* decode, const emu_table_view* mixed, const emu_table_view* combined,
+                      void* stream, emu_tables_t* out) {
+  if (!out) return fail(EMU_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  cudaStream_t s = as_stream(stream);
+  auto* t = new emu_tables_s();
+  const emu_table_view* v[3] = {decode, mixed, combined};
+  const char* names[3] = {"decode", "mixed", "combined"};
+  for (int i = 0; i < 3; i++) {
+    int rc = upload_table(v[i], names[i], s, t->tab[i]);
+    if (rc) {
+      for (int j = 0; j < 3; j++) t->tab[j].release();
+      delete t;
+      return rc;
+    }
+  }
+  if (t->tab[2].ns != t->tab[0].ns + t->tab[1].ns) {
+    std::string m = "combined table inconsistent: " + std::to_string(t->tab[2].ns) + " samples != decode+mixed " +
+                    std::to_string(t->tab[0].ns + t->tab[1].ns);
+    for (int j = 0; j < 3; j++) t->tab[j].release();
+    delete t;
+    return fail(EMU_ERR_INVALID, m);
+  }
+  *out = t;
+  return EMU_OK;
+}
+
+int emu_tables_info(emu_tables_t t, int table_id, emu_table_info* out) {
+  if (!t || !out || table_id < 0 || table_id > 2) return fail(EMU_ERR_INVALID, "bad emu_tables_info arguments");
+  const TableBuf& b = t->tab[table_id];
+  out->n_buckets = b.nb;
+  out->n_samples = b.ns;
+  out->tt_lo = b.tt_lo;
+  out->tt_hi = b.tt_hi;
+  out->conc_lo = b.c_lo;
+  out->conc_hi = b.c_hi;
+  return EMU_OK;
+}
+
+int emu_tables_device(emu_tables_t t, int table_id, emu_table_dev* out) {
+  if (!t || !out || table_id < 0 || table_id > 2) return fail(EMU_ERR_INVALID, "bad emu_tables_device arguments");
+  const TableBuf& b = t->tab[table_id];
+  out->n_buckets = b.nb;
+  out->n_samples = b.ns;
+  out->n_rows = b.nrows;
+  out->bkt_tt = b.bkt_tt;
+  out->bkt_conc = b.bkt_conc;
+  out->bkt_off = b.bkt_off;
+  out->samples = b.samples;
+  out->row_tt = b.row_tt;
+  out->row_start = b.row_start;
+  return EMU_OK;
+}
+
+void emu_tables_destroy(emu_tables_t t) {
+  if (!t) return;
+  for (int i = 0; i < 3; i++) t->tab[i].release();
+  delete t;
+}
+
+}  // extern "C"

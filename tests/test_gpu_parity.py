@@ -1,0 +1,329 @@
+"""CUDA path vs the CPU oracle and the reference's golden vectors (B200 only).
+
+Bit-exact bar: bins, neighbour sets, distances, sample indices, latencies,
+token ids, bucket counts; CDF values bit-exact at p = 2 and within 1e-6
+relative for other Shepard powers (north_star tolerance).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import emu_oracle as O
+from paper_2605_00616_b200 import (
+    LatencyOracle,
+    NoProfileDataError,
+    OracleConfig,
+    build_pack_arrays,
+)
+from paper_2605_00616_b200.device import DeviceTables
+from paper_2605_00616_b200.profile import PackValidationError, TableSoA
+from paper_2605_00616_b200.workloads import explicit_uniforms, queries_llama, queries_sparse, records_llama, \
+    records_sparse
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+    return t.to(dtype) if dtype is not None else t
+
+
+def soa_equal(got: TableSoA, want: O.Table):
+    return (np.array_equal(got.tt, want.tt) and np.array_equal(got.conc, want.conc)
+            and np.array_equal(got.off, want.off) and np.array_equal(got.samples, want.samples))
+
+
+def to_oracle_tables(pack):
+    return [O.Table(s.tt, s.conc, s.off, s.samples) for s in pack.soas()]
+
+
+@pytest.fixture(scope="module")
+def c1_pack(c1_records):
+    return build_pack_arrays(*c1_records, num_gpu_blocks=1000, canonical=True)
+
+
+@pytest.fixture(scope="module")
+def c1_oracle(c1_pack):
+    return LatencyOracle(c1_pack, OracleConfig(reliability_floor=32, rng_seed=0))
+
+
+# ------------------------------------------------------------------ build
+@pytest.mark.parametrize("canonical", [True, False])
+def test_gpu_build_matches_oracle(c1_records, canonical):
+    pack = build_pack_arrays(*c1_records, num_gpu_blocks=1000, canonical=canonical)
+    want = O.build(*c1_records, canonical=canonical)
+    for got, w in zip(pack.soas(), want):
+        assert soa_equal(got, w)
+    assert pack.combined_table.total_samples == len(c1_records[0])
+    assert pack.decode_table.total_samples + pack.mixed_table.total_samples == len(c1_records[0])
+
+
+def test_gpu_build_edge_cases():
+    # empty input
+    pack = build_pack_arrays(np.zeros(0), np.zeros(0), np.zeros(0), np.zeros(0), 5)
+    assert all(t.is_empty and t.tt_range is None for t in (pack.decode_table, pack.mixed_table,
+                                                           pack.combined_table))
+    # single bucket, one phase
+    pack = build_pack_arrays([3, 3, 3], [3, 3, 3], [0, 0, 0], [0.012, 0.010, 0.011], 10)
+    assert pack.decode_table.buckets[0].samples == [0.012, 0.010, 0.011]  # capture order kept
+    assert pack.mixed_table.is_empty and len(pack.combined_table.buckets) == 1
+    # wide keys (tt up to 2^31-1) and ragged random inputs vs oracle
+    rng = np.random.default_rng(3)
+    for n in (1, 7, 4095, 4096, 4097, 100_003):
+        conc = rng.integers(1, 1 << rng.integers(1, 20), n)
+        ph = rng.integers(0, 2, n)
+        tt = np.where(ph == 0, conc + rng.integers(0, 5, n), rng.integers(1, 2**31 - 1, n))
+        lat = rng.random(n) + 1e-6
+        lat[rng.random(n) < 0.3] = 0.5  # duplicate latencies
+        for canonical in (True, False):
+            pack = build_pack_arrays(tt, conc, ph, lat, 4, canonical=canonical)
+            for got, w in zip(pack.soas(), O.build(tt, conc, ph, lat, canonical=canonical)):
+                assert soa_equal(got, w)
+
+
+@pytest.mark.parametrize("bad,index,msg", [
+    (dict(lat=0.0), 1, "latency_s must be > 0, got 0.0"),
+    (dict(lat=-1.0), 1, "latency_s must be > 0, got -1.0"),
+    (dict(tt=0, ph=1), 1, "total_tokens must be >= 1, got 0"),
+    (dict(conc=0, ph=1), 1, "concurrency must be >= 1, got 0"),
+    (dict(tt=2, conc=3, ph=0), 1, "decode-only step has total_tokens=2 < concurrency=3"),
+    (dict(step=-1), 1, "step_index must be >= 0, got -1"),
+])
+def test_gpu_build_invalid_record_names_index(bad, index, msg):
+    tt, conc, ph, lat, step = [2, 3, 2], [2, 3, 2], [0, 0, 0], [0.01, 0.01, 0.01], [0, 1, 2]
+    for k, v in bad.items():
+        {"tt": tt, "conc": conc, "ph": ph, "lat": lat, "step": step}[k][index] = v
+    with pytest.raises(PackValidationError, match=f"trace record {index}: {msg}"):
+        build_pack_arrays(tt, conc, ph, lat, 10, step=step)
+
+
+def test_gpu_build_from_records_api():
+    from paper_2605_00616_b200 import StepPhase, StepTraceRecord, build_pack, load_pack, save_pack
+
+    recs = [StepTraceRecord(0, 3, 3, StepPhase.DECODE_ONLY, 0.012), StepTraceRecord(1, 3, 3, StepPhase.DECODE_ONLY,
+                                                                                    0.010),
+            StepTraceRecord(2, 64, 1, StepPhase.PREFILL_OR_MIXED, 0.05),
+            StepTraceRecord(3, 7, 2, StepPhase.PREFILL_OR_MIXED, 0.02)]
+    pack = build_pack(recs, 7, {"model": "toy", "gpu": "none"})
+    assert load_pack(save_pack(pack)) == pack
+    with pytest.raises(PackValidationError, match="trace record 1"):
+        build_pack([recs[0], StepTraceRecord(1, 0, 1, StepPhase.PREFILL_OR_MIXED, 0.1)], 10)
+
+
+# ------------------------------------------------------------------ pools
+def test_pools_match_golden(c1_oracle, c1_golden, c1_pack):
+    uk = c1_golden["uk"]
+    off, bkt, dist, prob, cdf, tid = c1_oracle.pools(uk[:, 0], uk[:, 1], uk[:, 2])
+    assert np.array_equal(off, c1_golden["p_off"])
+    soas = c1_pack.soas()
+    tt = np.concatenate([soas[t].tt[bkt[off[u]:off[u + 1]]] for u, t in enumerate(tid)])
+    cc = np.concatenate([soas[t].conc[bkt[off[u]:off[u + 1]]] for u, t in enumerate(tid)])
+    assert np.array_equal(tt, c1_golden["p_tt"]) and np.array_equal(cc, c1_golden["p_conc"])
+    assert np.array_equal(dist, c1_golden["p_dist"])
+    assert np.array_equal(prob, c1_golden["p_prob"])
+
+
+@pytest.mark.parametrize("floor,power", [(1, 2.0), (32, 2.0), (256, 2.0), (32, 1.0), (32, 0.5), (16, 1.5),
+                                         (10**9, 2.0)])
+def test_pools_match_oracle_random_keys(c1_pack, floor, power):
+    tabs = to_oracle_tables(c1_pack)
+    rng = np.random.default_rng(floor)
+    n = 400 if floor < 10**9 else 8
+    kt = rng.integers(-5, 3000, n)
+    kc = rng.integers(-3, 300, n)
+    kp = rng.integers(0, 2, n)
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=floor, shepard_power=power))
+    got = orc.pools(kt, kc, kp)
+    want = O.pools(tabs, kt, kc, kp, floor, p=power)
+    for g, w in zip(got[:3], want[:3]):
+        assert np.array_equal(g, w)
+    assert np.array_equal(got[5], want[5])
+    if power in (2.0, 1.0, 0.5):
+        assert np.array_equal(got[3], want[3]) and np.array_equal(got[4], want[4])
+    else:
+        np.testing.assert_allclose(got[4], want[4], rtol=1e-6, atol=0)
+
+
+def test_sparse_long_context_pools(tmp_path):
+    rec = records_sparse(200_000, 0)
+    pack = build_pack_arrays(*rec, num_gpu_blocks=1000, canonical=True)
+    tabs = to_oracle_tables(pack)
+    qt, qc, qp = queries_sparse(300, 5)
+    for floor in (32, 256):
+        orc = LatencyOracle(pack, OracleConfig(reliability_floor=floor))
+        got = orc.pools(qt, qc, qp)
+        want = O.pools(tabs, qt, qc, qp, floor)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+
+
+# ------------------------------------------------------------------ draws
+def test_pcg64_replay_matches_reference_stream(c1_pack, c1_trace, c1_golden):
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32, rng_seed=0))
+    lat, _ = orc.sample_batch(c1_trace["tt"], c1_trace["conc"], c1_trace["phase"], rng="pcg64")
+    assert np.array_equal(lat, c1_golden["lat_seq"])
+    st = orc.rng_state()
+    g = c1_golden["final_state"]
+    assert st["state"]["state"] == (int(g[0]) << 64) | int(g[1]) and st["has_uint32"] == int(g[4])
+
+
+def test_stepwise_calls_match_reference_stream(c1_pack, c1_trace, c1_golden):
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32, rng_seed=0))
+    n = 2000
+    seq = [orc(int(a), int(b), int(c)) for a, b, c in zip(c1_trace["tt"][:n], c1_trace["conc"][:n],
+                                                         c1_trace["phase"][:n])]
+    assert np.array_equal(np.array(seq), c1_golden["lat_seq"][:n])
+    # the batched replay continues the same stream
+    lat, _ = orc.sample_batch(c1_trace["tt"][n:], c1_trace["conc"][n:], c1_trace["phase"][n:], rng="pcg64")
+    assert np.array_equal(lat, c1_golden["lat_seq"][n:])
+
+
+def test_pcg64_other_knobs(c1_pack, c1_trace, c1_golden):
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=8, shepard_power=1.5, rng_seed=12345))
+    n = len(c1_golden["lat_seq_m8_p15"])
+    lat, _ = orc.sample_batch(c1_trace["tt"][:n], c1_trace["conc"][:n], c1_trace["phase"][:n], rng="pcg64")
+    assert np.mean(lat == c1_golden["lat_seq_m8_p15"]) >= 0.999
+
+
+@pytest.mark.parametrize("mode", ["explicit", "philox"])
+def test_batched_modes_match_oracle(c1_pack, mode):
+    tabs = to_oracle_tables(c1_pack)
+    qt, qc, qp = queries_llama(200_000, 11)
+    us, ui = explicit_uniforms(len(qt), 12)
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32))
+    lat, sidx = orc.sample_batch(dev(qt), dev(qc), dev(qp), rng=mode, u_sel=dev(us.view(np.int64)),
+                                 u_idx=dev(ui.view(np.int32)), seed=99, ctr_base=5)
+    lat_o, sidx_o = O.sample_batch(tabs, qt, qc, qp, 32, mode=mode, u_sel=us, u_idx=ui, seed=99, ctr_base=5,
+                                   threads=8)
+    assert np.array_equal(sidx.cpu().numpy(), sidx_o)
+    assert np.array_equal(lat.cpu().numpy(), lat_o)
+    # host-buffer entry point (the e2e path) gives the same answers
+    lat_h, sidx_h = orc.sample_batch(qt, qc, qp, rng=mode, u_sel=us, u_idx=ui, seed=99, ctr_base=5)
+    assert np.array_equal(sidx_h, sidx_o)
+
+
+def test_rejection_words_explicit_mode():
+    """Force Lemire rejections: a bucket with n = 3*2^30 is impossible, so use
+    words that land below the threshold for a small n and compare to the oracle."""
+    rec_tt = np.array([5] * 7)
+    pack = build_pack_arrays(rec_tt, rec_tt, np.zeros(7), np.arange(1, 8) * 0.001, 1, canonical=True)
+    tabs = to_oracle_tables(pack)
+    n = 7
+    thr = (2**32 - n) % n  # = 4
+    words = np.array([w for w in range(0, 2**32, 2**32 // 64)][:64], dtype=np.uint64)
+    ui = np.concatenate([np.arange(0, 8, dtype=np.uint32), words.astype(np.uint32)])
+    us = np.arange(len(ui), dtype=np.uint64) * 12345
+    q = np.full(len(ui), 5)
+    orc = LatencyOracle(pack, OracleConfig(reliability_floor=1))
+    lat, sidx = orc.sample_batch(q, q, np.zeros(len(ui)), rng="explicit", u_sel=us, u_idx=ui)
+    lat_o, sidx_o = O.sample_batch(tabs, q, q, np.zeros(len(ui)), 1, mode="explicit", u_sel=us, u_idx=ui)
+    assert thr > 0 and np.array_equal(sidx, sidx_o)
+
+
+def test_full_scale_properties(c1_pack):
+    """Config-2-sized sweep: every draw is a literal pack value of a pooled
+    bucket, results are deterministic, and a subsample matches the oracle."""
+    rec = records_llama(1_000_000, 0)
+    pack = build_pack_arrays(*rec, num_gpu_blocks=1000, canonical=True)
+    tabs = to_oracle_tables(pack)
+    Q = 4_000_000
+    qt, qc, qp = queries_llama(Q, 1)
+    orc = LatencyOracle(pack, OracleConfig(reliability_floor=32))
+    lat, sidx = orc.sample_batch(dev(qt), dev(qc), dev(qp), rng="philox", seed=1)
+    lat2, sidx2 = orc.sample_batch(dev(qt), dev(qc), dev(qp), rng="philox", seed=1)
+    assert torch.equal(sidx, sidx2)
+    s = sidx.cpu().numpy()
+    lt = lat.cpu().numpy()
+    plane = np.where(qp == 1, 1, 0)
+    assert (s >= 0).all()
+    samples = [tabs[0].samples, tabs[1].samples]
+    for p in (0, 1):
+        m = plane == p
+        assert np.array_equal(lt[m], samples[p][s[m]])
+    k0 = 1_234_567  # a contiguous window: Philox counters are absolute query indices
+    lat_o, sidx_o = O.sample_batch(tabs, qt[k0:k0 + 20_000], qc[k0:k0 + 20_000], qp[k0:k0 + 20_000], 32,
+                                   mode="philox", seed=1, ctr_base=k0, threads=8)
+    assert np.array_equal(s[k0:k0 + 20_000], sidx_o)
+    assert np.array_equal(lt[k0:k0 + 20_000], lat_o)
+
+
+def test_small_arena_forces_flush_and_retry(c1_pack):
+    tabs = to_oracle_tables(c1_pack)
+    qt, qc, qp = queries_llama(50_000, 21)
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32), arena_slots=4096, hash_slots=2)
+    lat, sidx = orc.sample_batch(qt, qc, qp, rng="philox", seed=3)
+    lat_o, sidx_o = O.sample_batch(tabs, qt, qc, qp, 32, mode="philox", seed=3, threads=8)
+    assert np.array_equal(sidx, sidx_o)
+
+
+def test_out_of_domain_keys_use_hash_map(c1_pack):
+    tabs = to_oracle_tables(c1_pack)
+    rng = np.random.default_rng(8)
+    n = 20_000
+    qt = rng.integers(-100, 100_000, n)
+    qc = rng.integers(-10, 2000, n)
+    qp = rng.integers(0, 2, n)
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32), hash_slots=64)
+    lat, sidx = orc.sample_batch(qt, qc, qp, rng="philox", seed=4)
+    lat_o, sidx_o = O.sample_batch(tabs, qt, qc, qp, 32, mode="philox", seed=4, threads=8)
+    assert np.array_equal(sidx, sidx_o)
+
+
+def test_empty_and_fallback_packs():
+    empty = build_pack_arrays(np.zeros(0), np.zeros(0), np.zeros(0), np.zeros(0), 5)
+    orc = LatencyOracle(empty)
+    with pytest.raises(NoProfileDataError):
+        orc.sample(3, 3, 0)
+    with pytest.raises(NoProfileDataError):
+        orc.sample_batch(np.array([3]), np.array([3]), np.array([0]))
+    only_mixed = build_pack_arrays([64, 64, 64], [1, 1, 1], [1, 1, 1], [0.05, 0.06, 0.07], 5)
+    orc = LatencyOracle(only_mixed, OracleConfig(reliability_floor=1))
+    for _ in range(20):
+        assert orc.sample(3, 3, 0) in (0.05, 0.06, 0.07)  # decode -> combined fallback
+
+
+def test_token_fill_matches_golden_and_oracle(c1_trace):
+    from paper_2605_00616_b200 import token_fill
+
+    t = c1_trace
+    cols = [dev(t[k]) for k in ("tok_is_prefill", "tok_chunk", "tok_progress", "tok_prompt_len", "tok_generated",
+                                "tok_target")]
+    ids, fin = token_fill(*cols)
+    assert np.array_equal(ids.cpu().numpy(), t["tok_ids"])
+    assert np.array_equal(fin.cpu().numpy(), t["tok_fin"])
+    rng = np.random.default_rng(1)
+    for n in (1, 3, 4, 5, 1023, 1_000_001):
+        pre = rng.integers(0, 2, n)
+        plen = rng.integers(1, 100, n)
+        prog = rng.integers(0, 100, n) % plen
+        chunk = np.where(rng.random(n) < 0.5, plen - prog, rng.integers(1, 50, n))
+        gen = rng.integers(0, 50, n)
+        tgt = rng.integers(1, 60, n)
+        ids, fin = token_fill(*[dev(a) for a in (pre, chunk, prog, plen, gen, tgt)])
+        wi, wf = O.token_fill(pre, chunk, prog, plen, gen, tgt)
+        assert np.array_equal(ids.cpu().numpy(), wi) and np.array_equal(fin.cpu().numpy(), wf)
+        # unaligned views take the scalar path
+        ids2, _ = token_fill(*[dev(np.concatenate([[0], a]))[1:] for a in (pre, chunk, prog, plen, gen, tgt)])
+        assert np.array_equal(ids2.cpu().numpy(), wi)
+
+
+def test_distance_kernel_matches_oracle():
+    from paper_2605_00616_b200 import normalized_distance
+
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        lo_t, lo_c = rng.integers(1, 100, 2)
+        hi_t, hi_c = lo_t + rng.integers(0, 3000), lo_c + rng.integers(0, 300)
+        q = (int(rng.integers(-10, 4000)), int(rng.integers(-5, 400)))
+        b = (int(rng.integers(lo_t, hi_t + 1)), int(rng.integers(lo_c, hi_c + 1)))
+        assert normalized_distance(q, b, (lo_t, hi_t), (lo_c, hi_c)) == O.distance(q, b, (lo_t, hi_t), (lo_c, hi_c))
+
+
+def test_device_tables_roundtrip(c1_pack):
+    dt = DeviceTables.from_soas(c1_pack.soas())
+    for i, s in enumerate(dt.to_host()):
+        assert soa_equal(s, O.Table(*[getattr(c1_pack.soas()[i], k) for k in ("tt", "conc", "off", "samples")]))
+    arrs = dt.device_arrays(2)
+    assert arrs["row_start"][-1].item() == dt.info(2)["n_buckets"]
