@@ -204,6 +204,16 @@ int emu_token_fill(const uint8_t* is_prefill, const int32_t* chunk, const int32_
                    const int32_t* prompt_len, const int32_t* generated, const int32_t* target_len,
                    int64_t n, int32_t* out_ids, uint8_t* out_finished, void* stream);
 
+/* ------------------------------------------------------------ profiling --
+ * Every kernel the library launches goes through one launch macro that counts
+ * it and, when profiling is on, brackets it with CUDA events recorded on the
+ * launching stream.  emu_profile_read synchronizes the device, folds all
+ * pending event pairs of `kernel` (e.g. "sample", "pool_warp", "mark") into
+ * (*total_ms, *launches) and resets that kernel's accumulator. */
+int64_t emu_launch_count(void);
+int emu_profile_enable(int on);
+int emu_profile_read(const char* kernel, double* total_ms, int64_t* launches);
+
 /* ---------------------------------------------------------------- misc --- */
 const char* emu_last_error(void);
 int emu_version(void);

@@ -62,6 +62,9 @@ SIGNATURES = {
     "emu_oracle_stats": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "emu_distance": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "emu_token_fill": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "emu_launch_count": (c_i64, []),
+    "emu_profile_enable": (c_int, [c_int]),
+    "emu_profile_read": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
     "emu_last_error": (ctypes.c_char_p, []),
     "emu_version": (c_int, []),
 }
@@ -152,3 +155,19 @@ def ptr(t) -> ctypes.c_void_p:
     if hasattr(t, "data_ptr"):
         return ctypes.c_void_p(t.data_ptr())
     return ctypes.c_void_p(t.ctypes.data)
+
+
+def launch_count() -> int:
+    """Kernels launched by libemu_b200 in this process."""
+    return int(lib().emu_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    check(lib().emu_profile_enable(1 if on else 0))
+
+
+def profile_read(kernel: str) -> tuple[float, int]:
+    """(total ms, launches) of `kernel` since the last read (CUDA events on the launch stream)."""
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    check(lib().emu_profile_read(kernel.encode(), ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value

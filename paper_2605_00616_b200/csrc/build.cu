@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "emu_internal.cuh"
+#include "prof.h"
 #include "scan.cuh"
 #include "tables.h"
 
@@ -301,7 +302,7 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
   // ranges
   int mm_init[2] = {0x7fffffff, 0};
   EMU_CUDA(cudaMemcpyAsync(mm_dev, mm_init, 8, cudaMemcpyHostToDevice, s));
-  k_conc_range<<<grid_of(nb, 256, 1024), 256, 0, s>>>(tb.bkt_conc, nb, mm_dev);
+  EMU_LAUNCH("conc_range", s, k_conc_range<<<grid_of(nb, 256, 1024), 256, 0, s>>>(tb.bkt_conc, nb, mm_dev));
   EMU_CUDA(cudaGetLastError());
   int mm[2];
   int32_t t0 = 0, t1 = 0;
@@ -401,7 +402,7 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   if (cudaMemcpyAsync(first_bad, &fb_init, 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
       cudaMemcpyAsync(small, mv_init, 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return bail(cuda_fail(cudaGetLastError(), "build init"));
-  k_validate<<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, first_bad, small);
+  EMU_LAUNCH("validate", s, k_validate<<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, first_bad, small));
   unsigned long long fb = 0;
   int mv[2];
   if (cudaMemcpyAsync(&fb, first_bad, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -427,7 +428,7 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
     return bail(rc);
   for (void* p : {(void*)hi0, (void*)lo0, (void*)hi1, (void*)lo1, (void*)counts, (void*)hist, (void*)partial})
     owned.push_back(p);
-  k_make_keys<<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, cbits, hi0, lo0);
+  EMU_LAUNCH("make_keys", s, k_make_keys<<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, cbits, hi0, lo0));
   // 3. which digit positions actually vary
   PassSet ps{};
   if (canonical)
@@ -440,7 +441,7 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
     ps.shift[ps.n++] = sft;
   }
   if (cudaMemsetAsync(hist, 0, 4 * 16 * 256, s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "memset"));
-  k_digit_hist<<<grid_of(n, 256, kNumSMs * 4), 256, ps.n * 256 * 4, s>>>(hi0, lo0, n, ps, hist);
+  EMU_LAUNCH("digit_hist", s, k_digit_hist<<<grid_of(n, 256, kNumSMs * 4), 256, ps.n * 256 * 4, s>>>(hi0, lo0, n, ps, hist));
   std::vector<unsigned int> hh(16 * 256);
   if (cudaMemcpyAsync(hh.data(), hist, 4 * 16 * 256, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess)
@@ -450,12 +451,12 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
     unsigned int mx = *std::max_element(hh.begin() + p * 256, hh.begin() + (p + 1) * 256);
     if ((int64_t)mx == n) continue;  // all records share this digit: pass is the identity
     const uint64_t* key = ps.word[p] ? hi0 : lo0;
-    k_radix_up<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], n, nblk, counts);
+    EMU_LAUNCH("radix_up", s, k_radix_up<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], n, nblk, counts));
     cudaError_t e = device_excl_scan<unsigned int>(
         [counts] __device__(int64_t i) { return counts[i]; },
         [counts] __device__(int64_t i, unsigned int ex) { counts[i] = ex; }, ncount, partial, total_dev, s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "radix scan"));
-    k_radix_scatter<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], hi0, lo0, hi1, lo1, n, nblk, counts);
+    EMU_LAUNCH("radix_scatter", s, k_radix_scatter<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], hi0, lo0, hi1, lo1, n, nblk, counts));
     std::swap(hi0, hi1);
     std::swap(lo0, lo1);
   }

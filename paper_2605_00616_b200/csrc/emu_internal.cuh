@@ -64,29 +64,66 @@ __device__ __forceinline__ double shepard_pow(double x, double p) {
 // n < 8 sequential; n <= 128 eight interleaved accumulators combined as
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then a sequential tail; larger n splits
 // at n2 = n/2 - (n/2)%8 and adds the two halves.
-static __device__ __noinline__ double pairwise_sum(const double* a, int64_t n) {
+__device__ __forceinline__ double pairwise_leaf(const double* a, int64_t n) {
   if (n < 8) {
     double res = 0.0;
     for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
     return res;
   }
-  if (n <= 128) {
-    double r[8];
+  double r[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) r[j] = a[j];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8) {
+  for (int j = 0; j < 8; j++) r[j] = a[j];
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; i++) res = __dadd_rn(res, a[i]);
-    return res;
+    for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
   }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; i++) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// Iterative post-order evaluation of numpy's recursion (no device-stack
+// recursion: pools can hold every bucket of a table).
+static __device__ __noinline__ double pairwise_sum(const double* a, int64_t n) {
+  if (n <= 128) return pairwise_leaf(a, n);
+  int64_t lo_[24], n_[24];
+  double left_[24];
+  int state_[24];
+  int sp = 0;
+  lo_[0] = 0;
+  n_[0] = n;
+  state_[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    const int64_t fl = lo_[sp], fn = n_[sp];
+    if (fn <= 128) {
+      ret = pairwise_leaf(a + fl, fn);
+      sp--;
+      continue;
+    }
+    int64_t n2 = fn / 2;
+    n2 -= n2 % 8;
+    if (state_[sp] == 0) {
+      state_[sp] = 1;
+      sp++;
+      lo_[sp] = fl;
+      n_[sp] = n2;
+      state_[sp] = 0;
+    } else if (state_[sp] == 1) {
+      left_[sp] = ret;
+      state_[sp] = 2;
+      sp++;
+      lo_[sp] = fl + n2;
+      n_[sp] = fn - n2;
+      state_[sp] = 0;
+    } else {
+      ret = __dadd_rn(left_[sp], ret);
+      sp--;
+    }
+  }
+  return ret;
 }
 
 // ------------------------------------------------------------------- RNGs

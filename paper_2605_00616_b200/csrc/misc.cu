@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include "emu_internal.cuh"
+#include "prof.h"
 
 namespace emu {
 
@@ -75,8 +76,8 @@ int emu_distance(const int32_t* q_tt, const int32_t* q_conc, const int32_t* b_tt
                  int32_t tt_lo, int32_t tt_hi, int32_t conc_lo, int32_t conc_hi, double* out, void* stream) {
   if (n < 0) return fail(EMU_ERR_INVALID, "negative length");
   if (n == 0) return EMU_OK;
-  k_distance<<<grid_n(n, 256), 256, 0, as_stream(stream)>>>(q_tt, q_conc, b_tt, b_conc, n, tt_lo, tt_hi, conc_lo, conc_hi,
-                                                           out);
+  EMU_LAUNCH("distance", as_stream(stream), k_distance<<<grid_n(n, 256), 256, 0, as_stream(stream)>>>(q_tt, q_conc, b_tt, b_conc, n, tt_lo, tt_hi, conc_lo, conc_hi,
+                                                           out));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
 }
@@ -91,11 +92,11 @@ int emu_token_fill(const uint8_t* is_prefill, const int32_t* chunk, const int32_
                    al(generated, 16) && al(target_len, 16) && al(out_ids, 16) && al(out_finished, 4);
   cudaStream_t s = as_stream(stream);
   if (vec)
-    k_token_fill<<<grid_n((n + 3) / 4, 256), 256, 0, s>>>(is_prefill, chunk, prefill_progress, prompt_len, generated,
-                                                         target_len, n, out_ids, out_finished);
+    EMU_LAUNCH("token_fill", s, k_token_fill<<<grid_n((n + 3) / 4, 256), 256, 0, s>>>(is_prefill, chunk, prefill_progress, prompt_len, generated,
+                                                         target_len, n, out_ids, out_finished));
   else
-    k_token_fill_scalar<<<grid_n(n, 256), 256, 0, s>>>(is_prefill, chunk, prefill_progress, prompt_len, generated,
-                                                      target_len, n, out_ids, out_finished);
+    EMU_LAUNCH("token_fill", s, k_token_fill_scalar<<<grid_n(n, 256), 256, 0, s>>>(is_prefill, chunk, prefill_progress, prompt_len, generated,
+                                                      target_len, n, out_ids, out_finished));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
 }

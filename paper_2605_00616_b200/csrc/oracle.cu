@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "emu_internal.cuh"
+#include "prof.h"
 #include "pool.cuh"
 #include "tables.h"
 
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
   __shared__ long long s_idx, s_e;
   const DevTable& T = ph ? P1 : P0;
   if (threadIdx.x == 0) {
+    *sk.flags = 0;
     int64_t idx = map_find<true>(sk.map, ph, t, c);
     long long e = -2;
     if (idx >= 0) {
@@ -483,7 +485,7 @@ static Sink make_sink(emu_oracle_t o) {
 static int oracle_flush(emu_oracle_t o, cudaStream_t s) {
   int64_t D = 2LL * o->map.dom_tt * o->map.dom_conc;
   EMU_CUDA(cudaMemsetAsync(o->map.dense, 0, sizeof(long long) * D, s));
-  k_fill_u64<<<grid_for(2 * o->map.hcap, 256, 4096), 256, 0, s>>>(o->map.hkeys, 2 * o->map.hcap, kHashEmpty);
+  EMU_LAUNCH("flush", s, k_fill_u64<<<grid_for(2 * o->map.hcap, 256, 4096), 256, 0, s>>>(o->map.hkeys, 2 * o->map.hcap, kHashEmpty));
   EMU_CUDA(cudaGetLastError());
   EMU_CUDA(cudaMemsetAsync(o->map.hvals, 0, sizeof(long long) * 2 * o->map.hcap, s));
   EMU_CUDA(cudaMemsetAsync(o->arena_used, 0, sizeof(unsigned long long), s));
@@ -621,16 +623,16 @@ int emu_oracle_stats(emu_oracle_t o, int64_t* n_pools, int64_t* n_slots) {
 static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t Q,
                          cudaStream_t s) {
   EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
-  k_mark<<<grid_for(Q, 256, kNumSMs * 16), 256, 0, s>>>(o->map, qt, qc, qp, Q, o->nk_tt, o->nk_c, o->nk_p, o->nk_e,
-                                                         o->ctl);
+  EMU_LAUNCH("mark", s, k_mark<<<grid_for(Q, 256, kNumSMs * 16), 256, 0, s>>>(o->map, qt, qc, qp, Q, o->nk_tt, o->nk_c, o->nk_p, o->nk_e,
+                                                         o->ctl));
   EMU_CUDA(cudaGetLastError());
   Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
   Sink sk = make_sink(o);
-  k_pool_warp<0><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
-                                                                           &o->ctl->work, o->esc, &o->ctl->esc_count);
+  EMU_LAUNCH("pool_warp", s, k_pool_warp<0><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
+                                                                           &o->ctl->work, o->esc, &o->ctl->esc_count));
   EMU_CUDA(cudaGetLastError());
-  k_pool_cta<0><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk, &o->ctl->esc_work,
-                                                         o->esc, &o->ctl->esc_count, o->gd, o->gb, o->gcap);
+  EMU_LAUNCH("pool_cta", s, k_pool_cta<0><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk, &o->ctl->esc_work,
+                                                         o->esc, &o->ctl->esc_count, o->gd, o->gb, o->gcap));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
 }
@@ -679,18 +681,18 @@ int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc
     if (rc) return rc;
     const int grid = grid_for(n, kSampleThreads, kNumSMs * 16);
     if (rng_mode == EMU_RNG_EXPLICIT)
-      k_sample<EMU_RNG_EXPLICIT><<<grid, kSampleThreads, 0, s>>>(
+      EMU_LAUNCH("sample", s, k_sample<EMU_RNG_EXPLICIT><<<grid, kSampleThreads, 0, s>>>(
           o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done, q_conc + done, q_phase + done, n,
-          u_sel + done, u_idx + done, seed, ctr_base + (uint64_t)done, out_lat + done, out_sidx + done, &o->ctl->flags);
+          u_sel + done, u_idx + done, seed, ctr_base + (uint64_t)done, out_lat + done, out_sidx + done, &o->ctl->flags));
     else
-      k_sample<EMU_RNG_PHILOX><<<grid, kSampleThreads, 0, s>>>(
+      EMU_LAUNCH("sample", s, k_sample<EMU_RNG_PHILOX><<<grid, kSampleThreads, 0, s>>>(
           o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done, q_conc + done, q_phase + done, n,
-          nullptr, nullptr, seed, ctr_base + (uint64_t)done, out_lat + done, out_sidx + done, &o->ctl->flags);
+          nullptr, nullptr, seed, ctr_base + (uint64_t)done, out_lat + done, out_sidx + done, &o->ctl->flags));
     EMU_CUDA(cudaGetLastError());
     int flags = 0;
     if ((rc = read_flags(o, s, &flags))) return rc;
     if (flags) {
-      if (++attempts > 64) return fail(EMU_ERR_CUDA, "oracle could not fit the batch after 64 retries");
+      if (++attempts > 16) return fail(EMU_ERR_CUDA, "oracle could not fit a chunk after 16 retries");
       if (!(flags & (FLAG_ARENA | FLAG_HASH)))
         return fail(EMU_ERR_CUDA, "internal error: pool missing after build (flags=" + std::to_string(flags) + ")");
       chunk = recover(o, flags, n, s, &rc);
@@ -699,6 +701,7 @@ int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc
       continue;
     }
     done += n;
+    attempts = 0;
   }
   return EMU_OK;
 }
@@ -717,14 +720,14 @@ int emu_oracle_sample_pcg64(emu_oracle_t o, const int32_t* q_tt, const int32_t* 
     const int64_t n = std::min(chunk, Q - done);
     int rc = build_missing(o, q_tt + done, q_conc + done, q_phase + done, n, s);
     if (rc) return rc;
-    k_sample_pcg<<<1, 32, 0, s>>>(o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done,
+    EMU_LAUNCH("sample_pcg", s, k_sample_pcg<<<1, 32, 0, s>>>(o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done,
                                   q_conc + done, q_phase + done, n, pcg_state, out_lat + done, out_sidx + done,
-                                  &o->ctl->flags);
+                                  &o->ctl->flags));
     EMU_CUDA(cudaGetLastError());
     int flags = 0;
     if ((rc = read_flags(o, s, &flags))) return rc;
     if (flags) {
-      if (++attempts > 64) return fail(EMU_ERR_CUDA, "oracle could not fit the batch after 64 retries");
+      if (++attempts > 16) return fail(EMU_ERR_CUDA, "oracle could not fit a chunk after 16 retries");
       if (!(flags & (FLAG_ARENA | FLAG_HASH)))
         return fail(EMU_ERR_CUDA, "internal error: pool missing after build (flags=" + std::to_string(flags) + ")");
       chunk = recover(o, flags, n, s, &rc);
@@ -733,6 +736,7 @@ int emu_oracle_sample_pcg64(emu_oracle_t o, const int32_t* q_tt, const int32_t* 
       continue;
     }
     done += n;
+    attempts = 0;
   }
   return EMU_OK;
 }
@@ -800,8 +804,8 @@ int emu_oracle_step(emu_oracle_t o, int32_t tt, int32_t conc, int32_t phase, dou
   cudaStream_t s = 0;
   for (int attempt = 0; attempt < 4; attempt++) {
     Sink sk = make_sink(o);
-    k_step<<<1, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], o->cfg, sk, tt, conc, ph, o->pcg, o->gd, o->gb,
-                                            o->gcap, o->step_dev);
+    EMU_LAUNCH("step", s, k_step<<<1, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], o->cfg, sk, tt, conc, ph, o->pcg, o->gd, o->gb,
+                                            o->gcap, o->step_dev));
     EMU_CUDA(cudaGetLastError());
     EMU_CUDA(cudaMemcpyAsync(o->step_host, o->step_dev, sizeof(StepOut), cudaMemcpyDeviceToHost, s));
     EMU_CUDA(cudaStreamSynchronize(s));
@@ -865,12 +869,12 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
     sk.x_prob = xp;
     sk.x_cdf = xc;
     sk.x_K = xK;
-    k_pool_warp<1><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
-                                                                             &o->ctl->work, o->esc, &o->ctl->esc_count);
+    EMU_LAUNCH("pool_warp", s, k_pool_warp<1><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
+                                                                             &o->ctl->work, o->esc, &o->ctl->esc_count));
     EMU_CUDA(cudaGetLastError());
-    k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
+    EMU_LAUNCH("pool_cta", s, k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
                                                            &o->ctl->esc_work, o->esc, &o->ctl->esc_count, o->gd, o->gb,
-                                                           o->gcap);
+                                                           o->gcap));
     EMU_CUDA(cudaGetLastError());
     EMU_CUDA(cudaMemcpyAsync(hK.data(), xK, 8 * n, cudaMemcpyDeviceToHost, s));
     EMU_CUDA(cudaStreamSynchronize(s));
@@ -878,8 +882,8 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
     if (off[u0 + n] > cap) over = true;
     if (!over) {
       EMU_CUDA(cudaMemcpyAsync(doff, off.data() + u0, 8 * n, cudaMemcpyHostToDevice, s));
-      k_gather_pools<<<grid_for(n * 32, 256, 4096), 256, 0, s>>>(xK, doff, n, kmax, 0, xb, xd, xp, xc, pool_bkt,
-                                                                 pool_dist, pool_prob, pool_cdf, cap);
+      EMU_LAUNCH("gather", s, k_gather_pools<<<grid_for(n * 32, 256, 4096), 256, 0, s>>>(xK, doff, n, kmax, 0, xb, xd, xp, xc, pool_bkt,
+                                                                 pool_dist, pool_prob, pool_cdf, cap));
       EMU_CUDA(cudaGetLastError());
       EMU_CUDA(cudaStreamSynchronize(s));
     }
@@ -887,7 +891,7 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
   cleanup();
   EMU_CUDA(cudaMemcpyAsync(pool_off, off.data(), 8 * (U + 1), cudaMemcpyHostToDevice, s));
   if (table_of_key) {
-    k_table_of_key<<<grid_for(U, 256, 1024), 256, 0, s>>>(key_phase, U, o->plane_tab[0], o->plane_tab[1], table_of_key);
+    EMU_LAUNCH("table_of_key", s, k_table_of_key<<<grid_for(U, 256, 1024), 256, 0, s>>>(key_phase, U, o->plane_tab[0], o->plane_tab[1], table_of_key));
     EMU_CUDA(cudaGetLastError());
   }
   EMU_CUDA(cudaStreamSynchronize(s));

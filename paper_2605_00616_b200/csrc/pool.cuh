@@ -182,6 +182,7 @@ __device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t 
     if (Wt == prevWt && Wc == prevWc) continue;
     prevWt = Wt;
     prevWc = Wc;
+    G::sync();  // every thread has finished reading the previous window's workspace
     const bool cov_t = Wt >= kInfW || ((int64_t)t - Wt <= T.tt_lo && (int64_t)t + Wt >= T.tt_hi);
     const bool cov_c = Wc >= kInfW || ((int64_t)c - Wc <= T.c_lo && (int64_t)c + Wc >= T.c_hi);
     const int64_t rlo = lower_bound_i32(T.row_tt, 0, T.nrows, (int64_t)t - Wt);

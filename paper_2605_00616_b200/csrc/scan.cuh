@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "prof.h"
+
 namespace emu {
 
 constexpr int kScanThreads = 256;
@@ -97,9 +99,9 @@ template <typename T, typename In, typename Out>
 cudaError_t device_excl_scan(In in, Out out, int64_t n, T* partial, T* total_dev, cudaStream_t s) {
   int64_t nb = (n + kScanTile - 1) / kScanTile;
   if (nb < 1) nb = 1;
-  k_scan_reduce<T, In><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, partial);
-  k_scan_partials<T><<<1, 1024, 0, s>>>(partial, nb, total_dev);
-  k_scan_down<T, In, Out><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, partial);
+  EMU_LAUNCH("scan", s, k_scan_reduce<T, In><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, partial));
+  EMU_LAUNCH("scan", s, k_scan_partials<T><<<1, 1024, 0, s>>>(partial, nb, total_dev));
+  EMU_LAUNCH("scan", s, k_scan_down<T, In, Out><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, partial));
   return cudaGetLastError();
 }
 

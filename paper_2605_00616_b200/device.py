@@ -66,6 +66,21 @@ class DeviceTables:
         return cls(h, list(soas))
 
     @classmethod
+    def from_device(cls, flat: list) -> "DeviceTables":
+        """Tables from 12 device tensors [tt, conc, off, samples] x (decode, mixed, combined)."""
+        _lib.require_cuda()
+        views = []
+        for i in range(3):
+            tt, conc, off, smp = flat[4 * i:4 * i + 4]
+            views.append(_lib.TableView(tt.numel(), smp.numel(), tt.data_ptr(), conc.data_ptr(), off.data_ptr(),
+                                        smp.data_ptr()))
+        h = ctypes.c_void_p()
+        rc = _lib.lib().emu_tables_create(ctypes.byref(views[0]), ctypes.byref(views[1]), ctypes.byref(views[2]),
+                                          _lib.stream_ptr(), ctypes.byref(h))
+        _lib.check(rc, invalid_exc=PackValidationError)
+        return cls(h, None)
+
+    @classmethod
     def from_pack(cls, pack) -> "DeviceTables":
         """Tables of any pack (this package's or the reference's, by duck type)."""
         dev = getattr(pack, "_device", None)
