@@ -317,7 +317,13 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
   tb.tt_hi = t1;
   tb.c_lo = mm[0];
   tb.c_hi = mm[1];
-  return EMU_OK;
+  std::vector<int32_t> htt((size_t)nb), hcc((size_t)nb);
+  std::vector<int64_t> hoff((size_t)nb + 1);
+  EMU_CUDA(cudaMemcpyAsync(htt.data(), tb.bkt_tt, 4 * nb, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaMemcpyAsync(hcc.data(), tb.bkt_conc, 4 * nb, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaMemcpyAsync(hoff.data(), tb.bkt_off, 8 * (nb + 1), cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  return build_search_index(tb, htt.data(), hcc.data(), hoff.data(), s);
 }
 
 static bool is_device_ptr(const void* p) {

@@ -43,6 +43,16 @@ struct DevTable {
   const int64_t* row_start;  // nrows + 1
   int64_t nb, ns, nrows;
   int32_t tt_lo, tt_hi, c_lo, c_hi;
+  // Summed-area tables over the dense key grid (tt - tt_lo, conc - c_lo):
+  // bsat/ssat[(i)*(gnc+1) + j] = buckets / samples with tt index < i and conc
+  // index < j.  gnt = gnc = 0 when the grid would be too large (fallback search).
+  const int32_t* bsat;
+  const int32_t* ssat;
+  int64_t gnt, gnc;
+  // sq_t[k] = (k / span_t)^2 rounded exactly like norm_dist, k < lt (same for conc).
+  const double* sq_t;
+  const double* sq_c;
+  int64_t lt, lc;
 };
 
 // normalized_distance (oracle.py:62-77): exact integer deltas, IEEE rn ops.

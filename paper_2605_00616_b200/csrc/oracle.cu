@@ -31,7 +31,7 @@ enum : int { FLAG_ARENA = 1, FLAG_HASH = 2, FLAG_MISSING = 4 };
 constexpr int kWarpCap = 512;  // candidates per warp workspace
 constexpr int kWarpsPerCta = 4;
 constexpr int kWarpThreads = 32 * kWarpsPerCta;
-constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 2 * 8;  // d, b, scr, dsh
+constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 2 * 8 + 3 * 32 * 4;  // d, b, scr, dsh, rows
 constexpr int kWarpGrid = kNumSMs * 8;
 constexpr int kCtaThreads = 256;
 constexpr int kCtaCap = 8192;  // candidates in shared memory per CTA
@@ -87,7 +87,8 @@ template <int NT, int MODE>
 __device__ bool process_key(const DevTable& T, int64_t w, int32_t t, int32_t c, int64_t entry_idx, const Cfg& cfg,
                             const PoolWS& ws, const Sink& sk) {
   using G = Grp<NT>;
-  int64_t K = pool_search<NT>(T, t, c, cfg.floor, ws);
+  int64_t soff = 0;
+  int64_t K = pool_search<NT>(T, t, c, cfg.floor, ws, soff);
   if (K < 0) return false;
   if (MODE == 0) {
     if (G::rank() == 0) {
@@ -100,14 +101,14 @@ __device__ bool process_key(const DevTable& T, int64_t w, int32_t t, int32_t c, 
     const long long start = ws.scr[36];
     G::sync();
     if (start < 0) return true;
-    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, sk.arena + start, nullptr, nullptr, nullptr, nullptr);
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, sk.arena + start, nullptr, nullptr, nullptr, nullptr);
     if (G::rank() == 0) {
       __threadfence();
       atomicExch((unsigned long long*)map_entry_ptr(sk.map, entry_idx), (unsigned long long)make_entry(K, start));
     }
   } else {
     const int64_t base = w * sk.kmax;
-    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, nullptr, sk.x_bkt + base, sk.x_dist + base, sk.x_prob + base,
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, nullptr, sk.x_bkt + base, sk.x_dist + base, sk.x_prob + base,
                     sk.x_cdf + base);
     if (G::rank() == 0) sk.x_K[w] = K;
   }
@@ -148,6 +149,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_pool_warp(DevTable P0, DevTabl
   ws.b = (int32_t*)(base + kWarpCap * 8);
   ws.scr = (long long*)(base + kWarpCap * 12);
   ws.dsh = (double*)(base + kWarpCap * 12 + 40 * 8);
+  ws.rows = (int32_t*)(base + kWarpCap * 12 + 40 * 8 + 2 * 8);
   ws.cap = kWarpCap;
   const int64_t n = keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
   for (;;) {
@@ -173,8 +175,9 @@ __global__ void __launch_bounds__(kCtaThreads) k_pool_cta(DevTable P0, DevTable 
   __shared__ long long scr[40];
   __shared__ double dsh[2];
   __shared__ int s_w;
-  PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh};
-  PoolWS wg{gd + (int64_t)blockIdx.x * gcap, gb + (int64_t)blockIdx.x * gcap, gcap, scr, dsh};
+  __shared__ int32_t rows[3 * kCtaThreads];
+  PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh, rows};
+  PoolWS wg{gd + (int64_t)blockIdx.x * gcap, gb + (int64_t)blockIdx.x * gcap, gcap, scr, dsh, rows};
   const int n = *esc_count;
   for (;;) {
     if (threadIdx.x == 0) s_w = atomicAdd(esc_work, 1);
@@ -334,6 +337,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
   __shared__ long long scr[40];
   __shared__ double dsh[2];
   __shared__ long long s_idx, s_e;
+  __shared__ int32_t rows[3 * kCtaThreads];
   const DevTable& T = ph ? P1 : P0;
   if (threadIdx.x == 0) {
     *sk.flags = 0;
@@ -354,10 +358,10 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
     return;
   }
   if (s_e == kEntryEmpty) {
-    PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh};
+    PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh, rows};
     bool ok = process_key<kCtaThreads, 0>(T, 0, t, c, idx, cfg, ws, sk);
     if (!ok && gd != nullptr) {
-      PoolWS wg{gd, gb, gcap, scr, dsh};
+      PoolWS wg{gd, gb, gcap, scr, dsh, rows};
       ok = process_key<kCtaThreads, 0>(T, 0, t, c, idx, cfg, wg, sk);
     }
   }

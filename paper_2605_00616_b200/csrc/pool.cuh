@@ -86,8 +86,9 @@ struct PoolWS {
   double* d;      // cap candidate distances
   int32_t* b;     // cap candidate bucket indices
   int64_t cap;    // power of two
-  long long* scr; // >= 33 long longs (scan scratch)
+  long long* scr; // >= 40 long longs (scan scratch + broadcasts)
   double* dsh;    // >= 2 doubles (broadcast)
+  int32_t* rows;  // 3 * NT ints: per-round row bucket start, prefix, |dt|
 };
 
 __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* a, int64_t lo, int64_t hi, int64_t v) {
@@ -153,7 +154,7 @@ __device__ __forceinline__ double initial_radius(const DevTable& T, int64_t mflo
 // ws.d[0..K) / ws.b[0..K); returns -1 if a window needs more than ws.cap
 // candidates (caller escalates to a bigger workspace).  T must be nonempty.
 template <int NT>
-__device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws) {
+__device__ int64_t pool_search_grow(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws) {
   using G = Grp<NT>;
   const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
   const double r0 = initial_radius(T, mfloor);
@@ -260,12 +261,267 @@ __device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t 
   return -1;  // unreachable for a finite table
 }
 
+// ---------------------------------------------------------------- SAT search
+// Squared normalized delta |k| / span, bit-identical to norm_dist's terms.
+__device__ __forceinline__ double sq_delta(int64_t k, int64_t span, const double* tab, int64_t len) {
+  if (span == 0) return 0.0;
+  if (k < 0) k = -k;
+  if (k < len) return tab[k];
+  const double q = __ddiv_rn((double)k, (double)span);
+  return __dmul_rn(q, q);
+}
+
+__device__ __forceinline__ double dist_tab(const DevTable& T, int64_t dtt, int64_t dc, int64_t span_t, int64_t span_c) {
+  return __dsqrt_rn(__dadd_rn(sq_delta(dtt, span_t, T.sq_t, T.lt), sq_delta(dc, span_c, T.sq_c, T.lc)));
+}
+
+struct Win {
+  int64_t Wt, Wc;
+  int64_t i0, i1, j0, j1;  // clipped grid index ranges (empty if i0 > i1 or j0 > j1)
+  bool cov_t, cov_c;
+};
+
+__device__ __forceinline__ int64_t radius_to_w(double r, int64_t span) {
+  if (!span) return kInfW;
+  const double w = floor(r * (double)span);
+  return w >= (double)kInfW ? kInfW : (int64_t)w;
+}
+
+__device__ __forceinline__ Win make_win(const DevTable& T, int32_t t, int32_t c, int64_t Wt, int64_t Wc) {
+  Win w;
+  w.Wt = Wt;
+  w.Wc = Wc;
+  w.cov_t = Wt >= kInfW || ((int64_t)t - Wt <= T.tt_lo && (int64_t)t + Wt >= T.tt_hi);
+  w.cov_c = Wc >= kInfW || ((int64_t)c - Wc <= T.c_lo && (int64_t)c + Wc >= T.c_hi);
+  const int64_t gt = T.gnt - 1, gc = T.gnc - 1;
+  w.i0 = Wt >= kInfW ? 0 : max((int64_t)0, (int64_t)t - Wt - T.tt_lo);
+  w.i1 = Wt >= kInfW ? gt : min(gt, (int64_t)t + Wt - T.tt_lo);
+  w.j0 = Wc >= kInfW ? 0 : max((int64_t)0, (int64_t)c - Wc - T.c_lo);
+  w.j1 = Wc >= kInfW ? gc : min(gc, (int64_t)c + Wc - T.c_lo);
+  return w;
+}
+
+__device__ __forceinline__ long long sat_rect(const int32_t* S, int64_t st, const Win& w) {
+  if (w.i0 > w.i1 || w.j0 > w.j1) return 0;
+  return (long long)S[(w.i1 + 1) * st + w.j1 + 1] - S[w.i0 * st + w.j1 + 1] - S[(w.i1 + 1) * st + w.j0] +
+         S[w.i0 * st + w.j0];
+}
+
+// Rank-sort C <= cap/2 candidates of ws[0..C) into ws[cap/2 ..) (stable by
+// construction: keys (d, bucket) are unique).
+template <int NT>
+__device__ void rank_sort(const PoolWS& ws, int64_t C) {
+  using G = Grp<NT>;
+  double* sd = ws.d + ws.cap / 2;
+  int32_t* sb = ws.b + ws.cap / 2;
+  if (NT == 32 && C <= 32) {
+    const int lane = G::rank();
+    const double dm = lane < C ? ws.d[lane] : __longlong_as_double(0x7ff0000000000000LL);
+    const int32_t bm = lane < C ? ws.b[lane] : 0x7fffffff;
+    int r = 0;
+    for (int k = 0; k < C; k++) {
+      const double dk = __shfl_sync(kFull, dm, k);
+      const int32_t bk = __shfl_sync(kFull, bm, k);
+      r += cand_less(dk, bk, dm, bm) ? 1 : 0;
+    }
+    if (lane < C) {
+      sd[r] = dm;
+      sb[r] = bm;
+    }
+  } else {
+    for (int64_t i = G::rank(); i < C; i += NT) {
+      const double di = ws.d[i];
+      const int32_t bi = ws.b[i];
+      int64_t r = 0;
+      for (int64_t k = 0; k < C; k++) r += cand_less(ws.d[k], ws.b[k], di, bi) ? 1 : 0;
+      sd[r] = di;
+      sb[r] = bi;
+    }
+  }
+  G::sync();
+}
+
+// Shortest prefix of the sorted candidates (sd, sb)[0..C) reaching the floor,
+// or -1 if the C candidates hold fewer than mfloor samples.
+template <int NT>
+__device__ int64_t prefix_k(const DevTable& T, const int32_t* sb, int64_t C, int64_t mfloor, const PoolWS& ws) {
+  using G = Grp<NT>;
+  const int64_t lim = C < mfloor ? C : mfloor;
+  long long carry = 0;
+  for (int64_t base = 0; base < lim; base += NT) {
+    const int64_t j = base + G::rank();
+    long long cnt = 0;
+    if (j < lim) {
+      const int32_t bb = sb[j];
+      cnt = T.bkt_off[bb + 1] - T.bkt_off[bb];
+    }
+    long long tot;
+    const long long ex = G::excl_scan(cnt, tot, ws.scr);
+    const int below = G::count(j < lim && carry + ex + cnt < mfloor, ws.scr);
+    if (carry + tot >= mfloor) return base + below + 1;
+    carry += tot;
+  }
+  return -1;
+}
+
+// Windowed search driven by the summed-area tables:
+//   1. each of 32 lanes sizes a window for one radius r_l (geometric grid) and
+//      counts its samples in O(1) from ssat; the first radius r1 whose window
+//      holds >= floor samples (or spans the table) wins;
+//   2. every sample of that window lies within sqrt(2)*r1, so the window for
+//      r2 = sqrt(2)*r1 contains the whole pool and passes the exact d_edge
+//      test (checked anyway; -2 asks the caller for the growth fallback);
+//   3. the r2 window's buckets are enumerated row by row (bsat gives each
+//      row's conc sub-range in O(1)) or by scanning the tt slab, whichever is
+//      fewer items; distances use the exact squared-delta tables;
+//   4. candidates are rank-sorted (small C) or bitonic-sorted.
+// Returns K, -1 if the window exceeds ws.cap (escalate), -2 to fall back.
+template <int NT>
+__device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws,
+                                   int64_t& sorted_off) {
+  using G = Grp<NT>;
+  const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
+  const int64_t st = T.gnc + 1;
+  double gtd = 0.0, gcd = 0.0;
+  if (span_t) gtd = (double)max(max((int64_t)T.tt_lo - t, (int64_t)t - T.tt_hi), (int64_t)0) / (double)span_t;
+  if (span_c) gcd = (double)max(max((int64_t)T.c_lo - c, (int64_t)c - T.c_hi), (int64_t)0) / (double)span_c;
+  const double rb = fmax(gtd, gcd);
+  const double r0 = initial_radius(T, mfloor);
+  // ---- 1. radius search
+  double r1 = -1.0;
+  for (int round = 0; round < 10 && r1 < 0.0; round++) {
+    bool ok = true;
+    double rl = 0.0;
+    if (G::rank() < 32) {
+      const int l = G::rank() + 32 * round;
+      rl = (l == 0) ? rb : rb + r0 * exp2((double)(l - 8) * 0.25);
+      const Win w = make_win(T, t, c, radius_to_w(rl, span_t), radius_to_w(rl, span_c));
+      ok = (w.cov_t && w.cov_c) || sat_rect(T.ssat, st, w) >= mfloor;
+    }
+    const int first = G::count(!ok, ws.scr);  // ok is monotone in the radius
+    if (first < 32) {
+      if (G::rank() == first) ws.dsh[1] = rl;
+      G::sync();
+      r1 = ws.dsh[1];
+      G::sync();
+    }
+  }
+  if (r1 < 0.0) return -2;
+  // ---- 2. the guaranteed window
+  const double r2 = r1 * 1.4142135623730951 * (1.0 + 1e-9);
+  const Win w = make_win(T, t, c, radius_to_w(r2, span_t), radius_to_w(r2, span_c));
+  const long long C = sat_rect(T.bsat, st, w);
+  if (C > ws.cap) return -1;
+  // ---- 3. enumerate
+  long long pos = 0;
+  if (C > 0) {
+    const int64_t nri = w.i1 - w.i0 + 1;
+    const int64_t b0 = T.bsat[w.i0 * st + T.gnc], b1 = T.bsat[(w.i1 + 1) * st + T.gnc];
+    if (b1 - b0 <= 2 * nri || C == b1 - b0) {  // scan the tt slab
+      const int64_t clo = (int64_t)T.c_lo + w.j0, chi = (int64_t)T.c_lo + w.j1;
+      for (int64_t base = b0; base < b1; base += NT) {
+        const int64_t b = base + G::rank();
+        bool in = false;
+        int32_t bc = 0;
+        if (b < b1) {
+          bc = T.bkt_conc[b];
+          in = bc >= clo && bc <= chi;
+        }
+        long long tot;
+        const long long ex = G::excl_scan(in ? 1 : 0, tot, ws.scr);
+        if (in) {
+          ws.d[pos + ex] = dist_tab(T, (int64_t)t - T.bkt_tt[b], (int64_t)c - bc, span_t, span_c);
+          ws.b[pos + ex] = (int32_t)b;
+        }
+        pos += tot;
+      }
+    } else {  // row by row: bsat gives each row's conc sub-range
+      for (int64_t base = w.i0; base <= w.i1; base += NT) {
+        const int64_t i = base + G::rank();
+        long long len = 0;
+        int32_t lo = 0;
+        if (i <= w.i1) {
+          const int64_t rs = T.bsat[i * st + T.gnc];
+          lo = (int32_t)(rs + T.bsat[(i + 1) * st + w.j0] - T.bsat[i * st + w.j0]);
+          const int64_t hi = rs + T.bsat[(i + 1) * st + w.j1 + 1] - T.bsat[i * st + w.j1 + 1];
+          len = hi - lo;
+        }
+        long long tot;
+        const long long ex = G::excl_scan(len, tot, ws.scr);
+        ws.rows[G::rank()] = lo;
+        ws.rows[NT + G::rank()] = (int32_t)ex;
+        ws.rows[2 * NT + G::rank()] = (int32_t)((int64_t)t - (T.tt_lo + i));
+        G::sync();
+        const int nrow = (int)min((int64_t)NT, w.i1 - base + 1);
+        for (long long k = G::rank(); k < tot; k += NT) {
+          int lo_r = 0, hi_r = nrow;  // last row with prefix <= k
+          while (hi_r - lo_r > 1) {
+            const int mid = (lo_r + hi_r) >> 1;
+            if (ws.rows[NT + mid] <= k)
+              lo_r = mid;
+            else
+              hi_r = mid;
+          }
+          const int32_t bb = ws.rows[lo_r] + (int32_t)(k - ws.rows[NT + lo_r]);
+          ws.d[pos + k] = dist_tab(T, ws.rows[2 * NT + lo_r], (int64_t)c - T.bkt_conc[bb], span_t, span_c);
+          ws.b[pos + k] = bb;
+        }
+        pos += tot;
+        G::sync();
+      }
+    }
+  }
+  G::sync();
+  // ---- 4. order
+  if (2 * pos <= ws.cap && pos <= (NT == 32 ? 128 : NT)) {
+    rank_sort<NT>(ws, pos);
+    sorted_off = ws.cap / 2;
+  } else {
+    int64_t P = 1;
+    while (P < pos) P <<= 1;
+    for (int64_t i = pos + G::rank(); i < P; i += NT) {
+      ws.d[i] = __longlong_as_double(0x7ff0000000000000LL);
+      ws.b[i] = 0x7fffffff;
+    }
+    G::sync();
+    if (P > 1) bitonic_sort<NT>(ws.d, ws.b, P);
+    sorted_off = 0;
+  }
+  const double* sd = ws.d + sorted_off;
+  const int32_t* sb = ws.b + sorted_off;
+  const int64_t K = prefix_k<NT>(T, sb, pos, mfloor, ws);
+  if (K < 0) return (w.cov_t && w.cov_c) ? pos : -2;
+  const double et = w.cov_t ? __longlong_as_double(0x7ff0000000000000LL) : norm_dist(w.Wt + 1, 0, span_t, span_c);
+  const double ec = w.cov_c ? __longlong_as_double(0x7ff0000000000000LL) : norm_dist(0, w.Wc + 1, span_t, span_c);
+  return sd[K - 1] < fmin(et, ec) ? K : -2;
+}
+
+// Dispatcher: SAT search when the table has a grid, else (or if the SAT
+// window fails its exact check) the window-growth search.  The sorted pool
+// is at ws.d/ws.b + sorted_off.
+template <int NT>
+__device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws,
+                               int64_t& sorted_off) {
+  sorted_off = 0;
+  if (T.gnt > 0) {
+    const int64_t K = pool_search_sat<NT>(T, t, c, mfloor, ws, sorted_off);
+    if (K != -2) return K;
+    Grp<NT>::sync();
+    sorted_off = 0;
+  }
+  return pool_search_grow<NT>(T, t, c, mfloor, ws);
+}
+
 // Shepard weights -> probabilities -> cdf for the pool in ws[0..K), numpy order.
 // Writes (optionally) bucket/dist/prob/cdf arrays and/or cache slots.
 template <int NT>
-__device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, const PoolWS& ws, Slot* slots,
+__device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, const PoolWS& ws_in,
+                            int64_t sorted_off, Slot* slots,
                             int32_t* o_bkt, double* o_dist, double* o_prob, double* o_cdf) {
   using G = Grp<NT>;
+  PoolWS ws = ws_in;
+  ws.d += sorted_off;
+  ws.b += sorted_off;
   for (int64_t j = G::rank(); j < K; j += NT) {
     int32_t bb = ws.b[j];
     double d = ws.d[j];

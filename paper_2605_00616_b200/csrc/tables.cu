@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "emu_internal.cuh"
+#include "prof.h"
 #include "tables.h"
 
 namespace emu {
@@ -38,6 +39,10 @@ void TableBuf::release() {
   cudaFree(samples);
   cudaFree(row_tt);
   cudaFree(row_start);
+  cudaFree(bsat);
+  cudaFree(ssat);
+  cudaFree(sq_t);
+  cudaFree(sq_c);
   *this = TableBuf();
 }
 
@@ -56,7 +61,64 @@ DevTable TableBuf::view() const {
   t.tt_hi = tt_hi;
   t.c_lo = c_lo;
   t.c_hi = c_hi;
+  t.bsat = bsat;
+  t.ssat = ssat;
+  t.gnt = gnt;
+  t.gnc = gnc;
+  t.sq_t = sq_t;
+  t.sq_c = sq_c;
+  t.lt = lt;
+  t.lc = lc;
   return t;
+}
+
+__global__ void k_sq_table(double* out, int64_t n, int64_t span) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    double q = span ? __ddiv_rn((double)k, (double)span) : 0.0;
+    out[k] = __dmul_rn(q, q);
+  }
+}
+
+constexpr int64_t kMaxGridCells = 1LL << 27;  // per summed-area table (512 MB of int32)
+constexpr int64_t kMaxSqTable = 1LL << 22;
+
+int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, const int64_t* h_off, cudaStream_t s) {
+  if (tb.nb == 0) return EMU_OK;
+  const int64_t span_t = (int64_t)tb.tt_hi - tb.tt_lo, span_c = (int64_t)tb.c_hi - tb.c_lo;
+  tb.lt = std::min<int64_t>(span_t + 1, kMaxSqTable);
+  tb.lc = std::min<int64_t>(span_c + 1, kMaxSqTable);
+  EMU_CUDA(cudaMalloc((void**)&tb.sq_t, 8 * tb.lt));
+  EMU_CUDA(cudaMalloc((void**)&tb.sq_c, 8 * tb.lc));
+  EMU_LAUNCH("index", s, k_sq_table<<<(unsigned)std::min<int64_t>(1024, (tb.lt + 255) / 256), 256, 0, s>>>(tb.sq_t, tb.lt, span_t));
+  EMU_LAUNCH("index", s, k_sq_table<<<(unsigned)std::min<int64_t>(1024, (tb.lc + 255) / 256), 256, 0, s>>>(tb.sq_c, tb.lc, span_c));
+  EMU_CUDA(cudaGetLastError());
+  const int64_t gnt = span_t + 1, gnc = span_c + 1;
+  if (gnt > kMaxGridCells || gnc > kMaxGridCells || (gnt + 1) * (gnc + 1) > kMaxGridCells) return EMU_OK;
+  const int64_t st = gnc + 1, cells = (gnt + 1) * st;
+  std::vector<int32_t> B((size_t)cells, 0), S((size_t)cells, 0);
+  for (int64_t b = 0; b < tb.nb; b++) {
+    const int64_t i = (int64_t)h_tt[b] - tb.tt_lo, j = (int64_t)h_cc[b] - tb.c_lo;
+    B[(size_t)((i + 1) * st + (j + 1))] = 1;
+    S[(size_t)((i + 1) * st + (j + 1))] = (int32_t)(h_off[b + 1] - h_off[b]);
+  }
+  for (int64_t i = 1; i <= gnt; i++) {
+    int64_t rb = 0, rs = 0;
+    const size_t row = (size_t)(i * st), prev = (size_t)((i - 1) * st);
+    for (int64_t j = 1; j <= gnc; j++) {
+      rb += B[row + j];
+      rs += S[row + j];
+      B[row + j] = (int32_t)(B[prev + j] + rb);
+      S[row + j] = (int32_t)(S[prev + j] + rs);
+    }
+  }
+  EMU_CUDA(cudaMalloc((void**)&tb.bsat, 4 * cells));
+  EMU_CUDA(cudaMalloc((void**)&tb.ssat, 4 * cells));
+  EMU_CUDA(cudaMemcpyAsync(tb.bsat, B.data(), 4 * cells, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.ssat, S.data(), 4 * cells, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  tb.gnt = gnt;
+  tb.gnc = gnc;
+  return EMU_OK;
 }
 
 template <typename T>
@@ -146,7 +208,7 @@ static int upload_table(const emu_table_view* v, const char* name, cudaStream_t 
   EMU_CUDA(cudaMemcpyAsync(tb.row_tt, row_tt.data(), 4 * tb.nrows, cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMemcpyAsync(tb.row_start, row_start.data(), 8 * (tb.nrows + 1), cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaStreamSynchronize(s));
-  return EMU_OK;
+  return build_search_index(tb, tt.data(), cc.data(), off.data(), s);
 }
 
 }  // namespace emu

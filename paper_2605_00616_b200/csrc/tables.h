@@ -13,9 +13,19 @@ struct TableBuf {
   int64_t* row_start = nullptr;
   int64_t nb = 0, ns = 0, nrows = 0;
   int32_t tt_lo = 0, tt_hi = 0, c_lo = 0, c_hi = 0;
+  int32_t* bsat = nullptr;
+  int32_t* ssat = nullptr;
+  int64_t gnt = 0, gnc = 0;
+  double* sq_t = nullptr;
+  double* sq_c = nullptr;
+  int64_t lt = 0, lc = 0;
   void release();
   DevTable view() const;
 };
+
+// Build the search index (summed-area tables + squared-delta tables) from
+// host copies of the bucket keys/offsets (construction time, not per query).
+int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, const int64_t* h_off, cudaStream_t s);
 
 }  // namespace emu
 
