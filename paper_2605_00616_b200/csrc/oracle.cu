@@ -31,7 +31,7 @@ enum : int { FLAG_ARENA = 1, FLAG_HASH = 2, FLAG_MISSING = 4 };
 constexpr int kWarpCap = 512;  // candidates per warp workspace
 constexpr int kWarpsPerCta = 4;
 constexpr int kWarpThreads = 32 * kWarpsPerCta;
-constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 2 * 8 + 3 * 32 * 4;  // d, b, scr, dsh, rows
+constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 32 * 4;  // d, b, scr, dsh, rows
 constexpr int kWarpGrid = kNumSMs * 8;
 constexpr int kCtaThreads = 256;
 constexpr int kCtaCap = 8192;  // candidates in shared memory per CTA
@@ -102,10 +102,8 @@ __device__ bool process_key(const DevTable& T, int64_t w, int32_t t, int32_t c, 
     G::sync();
     if (start < 0) return true;
     pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, sk.arena + start, nullptr, nullptr, nullptr, nullptr);
-    if (G::rank() == 0) {
-      __threadfence();
-      atomicExch((unsigned long long*)map_entry_ptr(sk.map, entry_idx), (unsigned long long)make_entry(K, start));
-    }
+    // entries are consumed by a later kernel: stream order publishes them
+    if (G::rank() == 0) *map_entry_ptr(sk.map, entry_idx) = make_entry(K, start);
   } else {
     const int64_t base = w * sk.kmax;
     pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, nullptr, sk.x_bkt + base, sk.x_dist + base, sk.x_prob + base,
@@ -139,7 +137,7 @@ __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t*
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kWarpThreads) k_pool_warp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
+__global__ void __launch_bounds__(kWarpThreads, 7) k_pool_warp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
                                                             int* work, int* esc_list, int* esc_count) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,7 +147,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_pool_warp(DevTable P0, DevTabl
   ws.b = (int32_t*)(base + kWarpCap * 8);
   ws.scr = (long long*)(base + kWarpCap * 12);
   ws.dsh = (double*)(base + kWarpCap * 12 + 40 * 8);
-  ws.rows = (int32_t*)(base + kWarpCap * 12 + 40 * 8 + 2 * 8);
+  ws.rows = (int32_t*)(base + kWarpCap * 12 + 40 * 8 + 10 * 8);
   ws.cap = kWarpCap;
   const int64_t n = keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
   for (;;) {
@@ -173,7 +171,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_pool_cta(DevTable P0, DevTable 
                                                           double* gd, int32_t* gb, int64_t gcap) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ long long scr[40];
-  __shared__ double dsh[2];
+  __shared__ double dsh[10];
   __shared__ int s_w;
   __shared__ int32_t rows[3 * kCtaThreads];
   PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh, rows};
@@ -335,7 +333,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
                                                       StepOut* out) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ long long scr[40];
-  __shared__ double dsh[2];
+  __shared__ double dsh[10];
   __shared__ long long s_idx, s_e;
   __shared__ int32_t rows[3 * kCtaThreads];
   const DevTable& T = ph ? P1 : P0;

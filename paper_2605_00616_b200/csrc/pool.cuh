@@ -87,7 +87,7 @@ struct PoolWS {
   int32_t* b;     // cap candidate bucket indices
   int64_t cap;    // power of two
   long long* scr; // >= 40 long longs (scan scratch + broadcasts)
-  double* dsh;    // >= 2 doubles (broadcast)
+  double* dsh;    // >= 10 doubles (broadcast + pairwise accumulators)
   int32_t* rows;  // 3 * NT ints: per-round row bucket start, prefix, |dt|
 };
 
@@ -314,9 +314,10 @@ __device__ void rank_sort(const PoolWS& ws, int64_t C) {
   using G = Grp<NT>;
   double* sd = ws.d + ws.cap / 2;
   int32_t* sb = ws.b + ws.cap / 2;
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   if (NT == 32 && C <= 32) {
     const int lane = G::rank();
-    const double dm = lane < C ? ws.d[lane] : __longlong_as_double(0x7ff0000000000000LL);
+    const double dm = lane < C ? ws.d[lane] : kInf;
     const int32_t bm = lane < C ? ws.b[lane] : 0x7fffffff;
     int r = 0;
     for (int k = 0; k < C; k++) {
@@ -329,13 +330,34 @@ __device__ void rank_sort(const PoolWS& ws, int64_t C) {
       sb[r] = bm;
     }
   } else {
-    for (int64_t i = G::rank(); i < C; i += NT) {
-      const double di = ws.d[i];
-      const int32_t bi = ws.b[i];
-      int64_t r = 0;
-      for (int64_t k = 0; k < C; k++) r += cand_less(ws.d[k], ws.b[k], di, bi) ? 1 : 0;
-      sd[r] = di;
-      sb[r] = bi;
+    // each thread ranks up to 4 own candidates held in registers against a
+    // single broadcast pass over all C candidates
+    constexpr int kOwn = 4;
+    for (int64_t base = 0; base < C; base += (int64_t)NT * kOwn) {
+      double od[kOwn];
+      int32_t ob[kOwn];
+      int orank[kOwn];
+#pragma unroll
+      for (int q = 0; q < kOwn; q++) {
+        const int64_t i = base + G::rank() + (int64_t)q * NT;
+        od[q] = i < C ? ws.d[i] : kInf;
+        ob[q] = i < C ? ws.b[i] : 0x7fffffff;
+        orank[q] = 0;
+      }
+      for (int64_t k = 0; k < C; k++) {
+        const double dk = ws.d[k];
+        const int32_t bk = ws.b[k];
+#pragma unroll
+        for (int q = 0; q < kOwn; q++) orank[q] += cand_less(dk, bk, od[q], ob[q]) ? 1 : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < kOwn; q++) {
+        const int64_t i = base + G::rank() + (int64_t)q * NT;
+        if (i < C) {
+          sd[orank[q]] = od[q];
+          sb[orank[q]] = ob[q];
+        }
+      }
     }
   }
   G::sync();
@@ -387,8 +409,8 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
   if (span_c) gcd = (double)max(max((int64_t)T.c_lo - c, (int64_t)c - T.c_hi), (int64_t)0) / (double)span_c;
   const double rb = fmax(gtd, gcd);
   const double r0 = initial_radius(T, mfloor);
-  // ---- 1. radius search
-  double r1 = -1.0;
+  // ---- 1. radius search (32 radii per round, then 32 between the last miss and the first hit)
+  double r1 = -1.0, rmiss = -1.0;
   for (int round = 0; round < 10 && r1 < 0.0; round++) {
     bool ok = true;
     double rl = 0.0;
@@ -399,20 +421,41 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
       ok = (w.cov_t && w.cov_c) || sat_rect(T.ssat, st, w) >= mfloor;
     }
     const int first = G::count(!ok, ws.scr);  // ok is monotone in the radius
+    if (G::rank() == (first == 0 ? 0 : first - 1)) ws.dsh[0] = rl;
+    if (first < 32 && G::rank() == first) ws.dsh[1] = rl;
+    G::sync();
     if (first < 32) {
-      if (G::rank() == first) ws.dsh[1] = rl;
-      G::sync();
       r1 = ws.dsh[1];
-      G::sync();
+      if (first > 0 || round > 0) rmiss = (first > 0) ? ws.dsh[0] : rmiss;
+    } else {
+      rmiss = ws.dsh[0];
     }
+    G::sync();
   }
   if (r1 < 0.0) return -2;
-  // ---- 2. the guaranteed window
+  if (rmiss >= 0.0 && r1 > rmiss) {  // refine inside (rmiss, r1]
+    bool ok = true;
+    double rl = r1;
+    if (G::rank() < 32) {
+      rl = (G::rank() == 31) ? r1 : rmiss + (r1 - rmiss) * (double)(G::rank() + 1) * (1.0 / 32.0);
+      const Win w = make_win(T, t, c, radius_to_w(rl, span_t), radius_to_w(rl, span_c));
+      ok = (w.cov_t && w.cov_c) || sat_rect(T.ssat, st, w) >= mfloor;
+    }
+    const int first = G::count(!ok, ws.scr);
+    if (first < 32 && G::rank() == first) ws.dsh[1] = rl;
+    G::sync();
+    if (first < 32) r1 = ws.dsh[1];
+    G::sync();
+  }
+  // ---- 2. the guaranteed window; pool members lie within dmax of the query
   const double r2 = r1 * 1.4142135623730951 * (1.0 + 1e-9);
   const Win w = make_win(T, t, c, radius_to_w(r2, span_t), radius_to_w(r2, span_c));
+  const Win w1 = make_win(T, t, c, radius_to_w(r1, span_t), radius_to_w(r1, span_c));
+  const bool exhaust = w1.cov_t && w1.cov_c && sat_rect(T.ssat, st, w1) < mfloor;
+  const double dmax = exhaust ? __longlong_as_double(0x7ff0000000000000LL) : r2 * (1.0 + 1e-9);
   const long long C = sat_rect(T.bsat, st, w);
   if (C > ws.cap) return -1;
-  // ---- 3. enumerate
+  // ---- 3. enumerate (candidates beyond dmax cannot be pooled and are dropped)
   long long pos = 0;
   if (C > 0) {
     const int64_t nri = w.i1 - w.i0 + 1;
@@ -422,15 +465,18 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
       for (int64_t base = b0; base < b1; base += NT) {
         const int64_t b = base + G::rank();
         bool in = false;
-        int32_t bc = 0;
+        double d = 0.0;
         if (b < b1) {
-          bc = T.bkt_conc[b];
-          in = bc >= clo && bc <= chi;
+          const int32_t bc = T.bkt_conc[b];
+          if (bc >= clo && bc <= chi) {
+            d = dist_tab(T, (int64_t)t - T.bkt_tt[b], (int64_t)c - bc, span_t, span_c);
+            in = d <= dmax;
+          }
         }
         long long tot;
         const long long ex = G::excl_scan(in ? 1 : 0, tot, ws.scr);
         if (in) {
-          ws.d[pos + ex] = dist_tab(T, (int64_t)t - T.bkt_tt[b], (int64_t)c - bc, span_t, span_c);
+          ws.d[pos + ex] = d;
           ws.b[pos + ex] = (int32_t)b;
         }
         pos += tot;
@@ -453,20 +499,32 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
         ws.rows[2 * NT + G::rank()] = (int32_t)((int64_t)t - (T.tt_lo + i));
         G::sync();
         const int nrow = (int)min((int64_t)NT, w.i1 - base + 1);
-        for (long long k = G::rank(); k < tot; k += NT) {
-          int lo_r = 0, hi_r = nrow;  // last row with prefix <= k
-          while (hi_r - lo_r > 1) {
-            const int mid = (lo_r + hi_r) >> 1;
-            if (ws.rows[NT + mid] <= k)
-              lo_r = mid;
-            else
-              hi_r = mid;
+        for (long long kb = 0; kb < tot; kb += NT) {
+          const long long k = kb + G::rank();
+          bool in = false;
+          double d = 0.0;
+          int32_t bb = 0;
+          if (k < tot) {
+            int lo_r = 0, hi_r = nrow;  // last row with prefix <= k
+            while (hi_r - lo_r > 1) {
+              const int mid = (lo_r + hi_r) >> 1;
+              if (ws.rows[NT + mid] <= k)
+                lo_r = mid;
+              else
+                hi_r = mid;
+            }
+            bb = ws.rows[lo_r] + (int32_t)(k - ws.rows[NT + lo_r]);
+            d = dist_tab(T, ws.rows[2 * NT + lo_r], (int64_t)c - T.bkt_conc[bb], span_t, span_c);
+            in = d <= dmax;
           }
-          const int32_t bb = ws.rows[lo_r] + (int32_t)(k - ws.rows[NT + lo_r]);
-          ws.d[pos + k] = dist_tab(T, ws.rows[2 * NT + lo_r], (int64_t)c - T.bkt_conc[bb], span_t, span_c);
-          ws.b[pos + k] = bb;
+          long long kt;
+          const long long ex2 = G::excl_scan(in ? 1 : 0, kt, ws.scr);
+          if (in) {
+            ws.d[pos + ex2] = d;
+            ws.b[pos + ex2] = bb;
+          }
+          pos += kt;
         }
-        pos += tot;
         G::sync();
       }
     }
@@ -533,7 +591,31 @@ __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, 
     ws.d[j] = __dmul_rn(w, (double)n);  // mass
   }
   G::sync();
-  if (G::rank() == 0) ws.dsh[0] = pairwise_sum(ws.d, K);
+  if (K <= 128) {  // numpy's 8-accumulator leaf: lanes 0..7 own one accumulator each
+    double r = 0.0;
+    const int64_t body = K < 8 ? 0 : K - (K % 8);
+    if (G::rank() < 8 && K >= 8) {
+      r = ws.d[G::rank()];
+      for (int64_t i = 8 + G::rank(); i < body; i += 8) r = __dadd_rn(r, ws.d[i]);
+      ws.dsh[2 + G::rank()] = r;
+    }
+    G::sync();
+    if (G::rank() == 0) {
+      double res;
+      if (K < 8) {
+        res = 0.0;
+        for (int64_t i = 0; i < K; i++) res = __dadd_rn(res, ws.d[i]);
+      } else {
+        const double* q = ws.dsh + 2;
+        res = __dadd_rn(__dadd_rn(__dadd_rn(q[0], q[1]), __dadd_rn(q[2], q[3])),
+                        __dadd_rn(__dadd_rn(q[4], q[5]), __dadd_rn(q[6], q[7])));
+        for (int64_t i = body; i < K; i++) res = __dadd_rn(res, ws.d[i]);
+      }
+      ws.dsh[0] = res;
+    }
+  } else if (G::rank() == 0) {
+    ws.dsh[0] = pairwise_sum(ws.d, K);
+  }
   G::sync();
   const double S = ws.dsh[0];
   for (int64_t j = G::rank(); j < K; j += NT) {
