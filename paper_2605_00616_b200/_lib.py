@@ -11,7 +11,7 @@ import os
 import subprocess
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libemu_b200.so")
+LIB_PATH = os.environ.get("EMU_LIB_PATH") or os.path.join(_PKG, "libemu_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 
 EMU_OK, EMU_ERR_NO_DATA, EMU_ERR_INVALID, EMU_ERR_CUDA, EMU_ERR_CAPACITY = 0, 1, 2, 3, 4

@@ -49,6 +49,13 @@ struct DevTable {
   const int32_t* bsat;
   const int32_t* ssat;
   int64_t gnt, gnc;
+  // Occupancy bitmap of the same grid: row i, word k holds conc indices
+  // 32k..32k+31 (bit set = bucket exists); wpre = set bits in earlier words of
+  // the row; rowbase[i] = first bucket of tt index i.  wpr words per row.
+  const uint32_t* bmap;
+  const int32_t* wpre;
+  const int32_t* rowbase;
+  int32_t wpr;
   // sq_t[k] = (k / span_t)^2 rounded exactly like norm_dist, k < lt (same for conc).
   const double* sq_t;
   const double* sq_c;

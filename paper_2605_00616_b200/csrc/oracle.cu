@@ -28,24 +28,26 @@ namespace emu {
 
 enum : int { FLAG_ARENA = 1, FLAG_HASH = 2, FLAG_MISSING = 4 };
 
-constexpr int kWarpCap = 512;  // candidates per warp workspace
+constexpr int kWarpCap = 256;  // candidates per warp workspace
 constexpr int kWarpsPerCta = 4;
 constexpr int kWarpThreads = 32 * kWarpsPerCta;
-constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 32 * 4;  // d, b, scr, dsh, rows
+constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 128 * 4 + kWarpCap * 4;  // d,b,scr,dsh,rows,n,o
 constexpr int kWarpGrid = kNumSMs * 8;
 constexpr int kCtaThreads = 256;
 constexpr int kCtaCap = 8192;  // candidates in shared memory per CTA
 constexpr int kCtaSmem = kCtaCap * 12;
+constexpr int kCtaCache = 1024;  // cached counts/offsets per CTA workspace
 constexpr int kCtaGrid = kNumSMs;
 constexpr int kSampleThreads = 256;
 
 struct BatchCtl {
+  unsigned long long cand_used;  // candidate scratch bump pointer
   int new_count;
   int work;
   int esc_count;
   int esc_work;
   int flags;
-  int pad[3];
+  int pad;
 };
 
 struct Keys {
@@ -83,34 +85,103 @@ struct StepOut {
 };
 
 // --------------------------------------------------------------- kernels
+// Write a found pool (K entries sorted in ws at soff) to the sink.  MODE 0:
+// cache arena slots at `reserved` (or freshly allocated when reserved == -1;
+// reserved == -2 means the arena overflowed in prep: leave the key pending)
+// and publish its map entry.  MODE 1: explicit fixed-stride outputs.
+template <int NT, int MODE>
+__device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry_idx, int64_t soff, bool cached,
+                          long long reserved, const Cfg& cfg, const PoolWS& ws, const Sink& sk) {
+  using G = Grp<NT>;
+  if (MODE == 0) {
+    long long start = reserved;
+    if (start == -1) {
+      if (G::rank() == 0) {
+        unsigned long long st = atomicAdd(sk.arena_used, (unsigned long long)K);
+        long long s = (st + (unsigned long long)K <= (unsigned long long)sk.arena_cap) ? (long long)st : -2LL;
+        if (s < 0) atomicOr(sk.flags, FLAG_ARENA);
+        ws.scr[36] = s;
+      }
+      G::sync();
+      start = ws.scr[36];
+      G::sync();
+    }
+    if (start < 0) return;
+    EMU_PHASE_BEGIN();
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, sk.arena + start, nullptr, nullptr, nullptr, nullptr);
+    // entries are consumed by a later kernel: stream order publishes them
+    if (G::rank() == 0) *map_entry_ptr(sk.map, entry_idx) = make_entry(K, start);
+    EMU_PHASE(6);
+  } else {
+    const int64_t base = w * sk.kmax;
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, nullptr, sk.x_bkt + base, sk.x_dist + base,
+                    sk.x_prob + base, sk.x_cdf + base);
+    if (G::rank() == 0) sk.x_K[w] = K;
+  }
+}
+
+// Full in-group search (no precomputed candidates).  false = window too big
+// for this workspace.
 template <int NT, int MODE>
 __device__ bool process_key(const DevTable& T, int64_t w, int32_t t, int32_t c, int64_t entry_idx, const Cfg& cfg,
                             const PoolWS& ws, const Sink& sk) {
-  using G = Grp<NT>;
   int64_t soff = 0;
-  int64_t K = pool_search<NT>(T, t, c, cfg.floor, ws, soff);
+  bool cached = false;
+  const int64_t K = pool_search<NT>(T, t, c, cfg.floor, ws, soff, cached);
   if (K < 0) return false;
-  if (MODE == 0) {
-    if (G::rank() == 0) {
-      unsigned long long st = atomicAdd(sk.arena_used, (unsigned long long)K);
-      long long s = (st + (unsigned long long)K <= (unsigned long long)sk.arena_cap) ? (long long)st : -1LL;
-      if (s < 0) atomicOr(sk.flags, FLAG_ARENA);
-      ws.scr[36] = s;
-    }
-    G::sync();
-    const long long start = ws.scr[36];
-    G::sync();
-    if (start < 0) return true;
-    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, sk.arena + start, nullptr, nullptr, nullptr, nullptr);
-    // entries are consumed by a later kernel: stream order publishes them
-    if (G::rank() == 0) *map_entry_ptr(sk.map, entry_idx) = make_entry(K, start);
-  } else {
-    const int64_t base = w * sk.kmax;
-    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, nullptr, sk.x_bkt + base, sk.x_dist + base, sk.x_prob + base,
-                    sk.x_cdf + base);
-    if (G::rank() == 0) sk.x_K[w] = K;
-  }
+  emit_pool<NT, MODE>(T, w, K, entry_idx, soff, cached, -1, cfg, ws, sk);
   return true;
+}
+
+// Warp-aggregated bump allocation: each lane asks for `need`, one atomic per warp.
+__device__ __forceinline__ long long warp_alloc(unsigned long long* counter, long long need) {
+  const int lane = threadIdx.x & 31;
+  long long x = need;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  const long long total = __shfl_sync(kFull, x, 31);
+  unsigned long long base = 0;
+  if (lane == 31 && total > 0) base = atomicAdd(counter, (unsigned long long)total);
+  base = __shfl_sync(kFull, base, 31);
+  return (long long)base + x - need;
+}
+
+// Thread per new key: SAT radius search -> window (KeyWin) and (MODE 0) the
+// pool's arena reservation min(floor, window buckets), one atomic per warp.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk, KeyWin* kw,
+                                                   long long* resv) {
+  const int64_t n = keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t w = base + threadIdx.x;
+    const bool valid = w < n;
+    KeyWin k;
+    k.flags = 0;
+    k.cap = 0;
+    bool ready = false;
+    if (valid) {
+      const DevTable& T = keys.ph[w] ? P1 : P0;
+      ready = key_window(T, keys.tt[w], keys.conc[w], cfg.floor, k) && k.cap <= kWarpCap;
+    }
+    if (!ready) k.flags = 0;
+    long long r = -1;
+    if (MODE == 0) {
+      const long long need = ready ? (k.cap < cfg.floor ? k.cap : cfg.floor) : 0;
+      const long long st = warp_alloc(sk.arena_used, need);
+      if (ready) {
+        r = (st + need <= sk.arena_cap) ? st : -2;
+        if (r == -2) atomicOr(sk.flags, FLAG_ARENA);
+      }
+    }
+    if (valid) {
+      kw[w] = k;
+      resv[w] = r;
+    }
+  }
 }
 
 __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t* __restrict__ qc,
@@ -136,9 +207,13 @@ __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t*
   }
 }
 
+// Warp per new key: precomputed candidates -> register sort -> prefix ->
+// Shepard CDF; keys without a fast-path window run the full in-warp search,
+// and windows too large for a warp are escalated to k_pool_cta.
 template <int MODE>
 __global__ void __launch_bounds__(kWarpThreads, 7) k_pool_warp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
-                                                            int* work, int* esc_list, int* esc_count) {
+                                                            const KeyWin* kw, const long long* resv, int* work,
+                                                            int* esc_list, int* esc_count) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = smem + warp * kWarpBytes;
@@ -148,19 +223,39 @@ __global__ void __launch_bounds__(kWarpThreads, 7) k_pool_warp(DevTable P0, DevT
   ws.scr = (long long*)(base + kWarpCap * 12);
   ws.dsh = (double*)(base + kWarpCap * 12 + 40 * 8);
   ws.rows = (int32_t*)(base + kWarpCap * 12 + 40 * 8 + 10 * 8);
+  ws.n = (int32_t*)(base + kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 128 * 4);
+  ws.o = ws.n + kWarpCap / 2;
+  ws.ncache = kWarpCap / 2;
   ws.cap = kWarpCap;
   const int64_t n = keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
+  int64_t w_end = 0, w = 0;
   for (;;) {
-    int w = 0;
-    if (lane == 0) w = atomicAdd(work, 1);
-    w = __shfl_sync(kFull, w, 0);
+    if (w >= w_end) {  // grab keys two at a time (dynamic balance, half the atomics)
+      int g = 0;
+      if (lane == 0) g = atomicAdd(work, 2);
+      w = __shfl_sync(kFull, g, 0);
+      w_end = w + 2;
+    }
     if (w >= n) break;
-    const bool mixed = keys.ph[w] != 0;
-    const bool ok = process_key<32, MODE>(mixed ? P1 : P0, w, keys.tt[w], keys.conc[w], keys.entry ? keys.entry[w] : 0,
-                                          cfg, ws, sk);
+    const int64_t wk = w++;
+    const bool mixed = keys.ph[wk] != 0;
+    const DevTable& T = mixed ? P1 : P0;
+    const int64_t ent = keys.entry ? keys.entry[wk] : 0;
+    const KeyWin k = kw[wk];
+    if (k.flags & kWinReady) {
+      const long long r = MODE == 0 ? resv[wk] : -1;
+      if (r == -2) continue;  // arena overflow: the host flushes and retries
+      const int64_t K = pool_from_window(T, keys.tt[wk], keys.conc[wk], cfg.floor, k, ws);
+      if (K >= 0) {
+        emit_pool<32, MODE>(T, wk, K, ent, 0, true, r, cfg, ws, sk);
+        continue;
+      }
+      __syncwarp();
+    }
+    const bool ok = process_key<32, MODE>(T, wk, keys.tt[wk], keys.conc[wk], ent, cfg, ws, sk);
     if (!ok && lane == 0) {
       int e = atomicAdd(esc_count, 1);
-      esc_list[e] = w;
+      esc_list[e] = (int)wk;
     }
   }
 }
@@ -174,8 +269,11 @@ __global__ void __launch_bounds__(kCtaThreads) k_pool_cta(DevTable P0, DevTable 
   __shared__ double dsh[10];
   __shared__ int s_w;
   __shared__ int32_t rows[3 * kCtaThreads];
-  PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh, rows};
-  PoolWS wg{gd + (int64_t)blockIdx.x * gcap, gb + (int64_t)blockIdx.x * gcap, gcap, scr, dsh, rows};
+  __shared__ int32_t ncache[2 * kCtaCache];
+  PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh, rows, ncache, ncache + kCtaCache,
+            kCtaCache};
+  PoolWS wg{gd + (int64_t)blockIdx.x * gcap, gb + (int64_t)blockIdx.x * gcap, gcap, scr, dsh, rows, ncache,
+            ncache + kCtaCache, kCtaCache};
   const int n = *esc_count;
   for (;;) {
     if (threadIdx.x == 0) s_w = atomicAdd(esc_work, 1);
@@ -336,6 +434,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
   __shared__ double dsh[10];
   __shared__ long long s_idx, s_e;
   __shared__ int32_t rows[3 * kCtaThreads];
+  __shared__ int32_t ncache[2 * kCtaCache];
   const DevTable& T = ph ? P1 : P0;
   if (threadIdx.x == 0) {
     *sk.flags = 0;
@@ -356,10 +455,11 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
     return;
   }
   if (s_e == kEntryEmpty) {
-    PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh, rows};
+    PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh, rows, ncache,
+              ncache + kCtaCache, kCtaCache};
     bool ok = process_key<kCtaThreads, 0>(T, 0, t, c, idx, cfg, ws, sk);
     if (!ok && gd != nullptr) {
-      PoolWS wg{gd, gb, gcap, scr, dsh, rows};
+      PoolWS wg{gd, gb, gcap, scr, dsh, rows, ncache, ncache + kCtaCache, kCtaCache};
       ok = process_key<kCtaThreads, 0>(T, 0, t, c, idx, cfg, wg, sk);
     }
   }
@@ -459,6 +559,12 @@ struct emu_oracle_s {
   int64_t* nk_e = nullptr;
   int* esc = nullptr;
   int64_t chunk_cap = 0;
+  int64_t nk_cap = 0;  // allocated new-key capacity (lazy)
+  KeyWin* kw = nullptr;
+  long long* resv = nullptr;
+  double* cd = nullptr;
+  int32_t* cb = nullptr;
+  int64_t cand_cap = 0;
   // CTA global scratch
   double* gd = nullptr;
   int32_t* gb = nullptr;
@@ -556,9 +662,7 @@ int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, doubl
   o->gcap = pow2_at_least(max_nb);
   bool need_global = o->gcap > kCtaCap;
   if ((rc = dalloc(&o->map.dense, 2 * dt * dc)) || (rc = alloc_hash(o, hcap)) || (rc = dalloc(&o->arena, o->arena_cap)) ||
-      (rc = dalloc(&o->arena_used, 1)) || (rc = dalloc(&o->ctl, 1)) || (rc = dalloc(&o->nk_tt, o->chunk_cap)) ||
-      (rc = dalloc(&o->nk_c, o->chunk_cap)) || (rc = dalloc(&o->nk_p, o->chunk_cap)) ||
-      (rc = dalloc(&o->nk_e, o->chunk_cap)) || (rc = dalloc(&o->esc, o->chunk_cap)) || (rc = dalloc(&o->pcg, 6)) ||
+      (rc = dalloc(&o->arena_used, 1)) || (rc = dalloc(&o->ctl, 1)) || (rc = dalloc(&o->pcg, 6)) ||
       (rc = dalloc(&o->step_dev, 1)) ||
       (need_global && ((rc = dalloc(&o->gd, kCtaGrid * o->gcap)) || (rc = dalloc(&o->gb, kCtaGrid * o->gcap))))) {
     emu_oracle_destroy(o);
@@ -595,6 +699,10 @@ void emu_oracle_destroy(emu_oracle_t o) {
   cudaFree(o->nk_p);
   cudaFree(o->nk_e);
   cudaFree(o->esc);
+  cudaFree(o->kw);
+  cudaFree(o->resv);
+  cudaFree(o->cd);
+  cudaFree(o->cb);
   cudaFree(o->gd);
   cudaFree(o->gb);
   cudaFree(o->pcg);
@@ -621,20 +729,65 @@ int emu_oracle_stats(emu_oracle_t o, int64_t* n_pools, int64_t* n_slots) {
 
 }  // extern "C"
 
-// Build missing pools for a chunk of queries (mark + warp + CTA kernels).
+// Per-batch key scratch, sized lazily: a batch of n queries (or n explicit
+// keys) has at most min(n, map entries) new keys.
+static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
+  int64_t need = std::max<int64_t>(4096, pow2_at_least(n_keys));
+  if (need <= o->nk_cap) return EMU_OK;
+  cudaFree(o->nk_tt);
+  cudaFree(o->nk_c);
+  cudaFree(o->nk_p);
+  cudaFree(o->nk_e);
+  cudaFree(o->esc);
+  cudaFree(o->kw);
+  cudaFree(o->resv);
+  cudaFree(o->cd);
+  cudaFree(o->cb);
+  o->nk_tt = nullptr;
+  o->nk_c = nullptr;
+  o->nk_p = nullptr;
+  o->nk_e = nullptr;
+  o->esc = nullptr;
+  o->kw = nullptr;
+  o->resv = nullptr;
+  o->cd = nullptr;
+  o->cb = nullptr;
+  o->nk_cap = 0;
+  int rc;
+  if ((rc = dalloc(&o->nk_tt, need)) || (rc = dalloc(&o->nk_c, need)) || (rc = dalloc(&o->nk_p, need)) ||
+      (rc = dalloc(&o->nk_e, need)) || (rc = dalloc(&o->esc, need)) || (rc = dalloc(&o->kw, need)) ||
+      (rc = dalloc(&o->resv, need)))
+    return rc;
+  o->nk_cap = need;
+  return EMU_OK;
+}
+
+static int64_t map_entries(emu_oracle_t o) { return 2LL * o->map.dom_tt * o->map.dom_conc + 2 * o->map.hcap; }
+
+constexpr int kPrepGrid = kNumSMs * 4;
+
+// Build missing pools for a chunk of queries: mark -> prep (thread/key) ->
+// warp (sort, prefix, CDF) -> CTA escalation.  No host round trip.
 static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t Q,
                          cudaStream_t s) {
+  int rc = ensure_key_capacity(o, std::min<int64_t>(Q, map_entries(o)));
+  if (rc) return rc;
   EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
-  EMU_LAUNCH("mark", s, k_mark<<<grid_for(Q, 256, kNumSMs * 16), 256, 0, s>>>(o->map, qt, qc, qp, Q, o->nk_tt, o->nk_c, o->nk_p, o->nk_e,
-                                                         o->ctl));
+  EMU_LAUNCH("mark", s, k_mark<<<grid_for(Q, 256, kNumSMs * 16), 256, 0, s>>>(o->map, qt, qc, qp, Q, o->nk_tt, o->nk_c,
+                                                                             o->nk_p, o->nk_e, o->ctl));
   EMU_CUDA(cudaGetLastError());
   Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
   Sink sk = make_sink(o);
-  EMU_LAUNCH("pool_warp", s, k_pool_warp<0><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
-                                                                           &o->ctl->work, o->esc, &o->ctl->esc_count));
+  EMU_LAUNCH("pool_prep", s, k_pool_prep<0><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw,
+                                                                      o->resv));
   EMU_CUDA(cudaGetLastError());
-  EMU_LAUNCH("pool_cta", s, k_pool_cta<0><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk, &o->ctl->esc_work,
-                                                         o->esc, &o->ctl->esc_count, o->gd, o->gb, o->gcap));
+  EMU_LAUNCH("pool_warp", s, k_pool_warp<0><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
+                                 o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, &o->ctl->work, o->esc, &o->ctl->esc_count));
+  EMU_CUDA(cudaGetLastError());
+  EMU_LAUNCH("pool_cta", s, k_pool_cta<0><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg,
+                                                                                  sk, &o->ctl->esc_work, o->esc,
+                                                                                  &o->ctl->esc_count, o->gd, o->gb,
+                                                                                  o->gcap));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
 }
@@ -859,6 +1012,10 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
     cleanup();
     return rc;
   }
+  if ((rc = ensure_key_capacity(o, chunkU))) {
+    cleanup();
+    return rc;
+  }
   std::vector<int64_t> hK((size_t)chunkU);
   bool over = false;
   for (int64_t u0 = 0; u0 < U; u0 += chunkU) {
@@ -871,12 +1028,16 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
     sk.x_prob = xp;
     sk.x_cdf = xc;
     sk.x_K = xK;
-    EMU_LAUNCH("pool_warp", s, k_pool_warp<1><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
-                                                                             &o->ctl->work, o->esc, &o->ctl->esc_count));
+    EMU_LAUNCH("pool_prep", s, k_pool_prep<1><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
+                                                                        o->kw, o->resv));
     EMU_CUDA(cudaGetLastError());
-    EMU_LAUNCH("pool_cta", s, k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
-                                                           &o->ctl->esc_work, o->esc, &o->ctl->esc_count, o->gd, o->gb,
-                                                           o->gcap));
+    EMU_LAUNCH("pool_warp", s, k_pool_warp<1><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
+                                   o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, &o->ctl->work, o->esc, &o->ctl->esc_count));
+    EMU_CUDA(cudaGetLastError());
+    EMU_LAUNCH("pool_cta", s, k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys,
+                                                                                    o->cfg, sk, &o->ctl->esc_work,
+                                                                                    o->esc, &o->ctl->esc_count, o->gd,
+                                                                                    o->gb, o->gcap));
     EMU_CUDA(cudaGetLastError());
     EMU_CUDA(cudaMemcpyAsync(hK.data(), xK, 8 * n, cudaMemcpyDeviceToHost, s));
     EMU_CUDA(cudaStreamSynchronize(s));
@@ -902,3 +1063,12 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
 }
 
 }  // extern "C"
+
+#ifdef EMU_STATS
+extern "C" int emu_stats_read(unsigned long long* out32) {
+  EMU_CUDA(cudaMemcpyFromSymbol(out32, emu::g_stats, sizeof(unsigned long long) * 32));
+  unsigned long long z[32] = {0};
+  EMU_CUDA(cudaMemcpyToSymbol(emu::g_stats, z, sizeof(z)));
+  return EMU_OK;
+}
+#endif

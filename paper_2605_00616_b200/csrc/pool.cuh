@@ -21,6 +21,30 @@
 
 namespace emu {
 
+// Optional per-phase cycle accounting (build with -DEMU_STATS; see tools/pool_stats.py).
+#ifdef EMU_STATS
+__device__ unsigned long long g_stats[32];
+#define EMU_PHASE_BEGIN() long long _emu_ph = clock64()
+#define EMU_PHASE(i)                                                                   \
+  do {                                                                                 \
+    const long long _n = clock64();                                                    \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&::emu::g_stats[i], (unsigned long long)(_n - _emu_ph)); \
+    _emu_ph = _n;                                                                      \
+  } while (0)
+#define EMU_STAT(i, v) \
+  do { if ((threadIdx.x & 31) == 0) atomicAdd(&::emu::g_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define EMU_PHASE_BEGIN() \
+  do {                    \
+  } while (0)
+#define EMU_PHASE(i) \
+  do {               \
+  } while (0)
+#define EMU_STAT(i, v) \
+  do {                 \
+  } while (0)
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int64_t kInfW = 1LL << 40;
 
@@ -89,6 +113,9 @@ struct PoolWS {
   long long* scr; // >= 40 long longs (scan scratch + broadcasts)
   double* dsh;    // >= 10 doubles (broadcast + pairwise accumulators)
   int32_t* rows;  // 3 * NT ints: per-round row bucket start, prefix, |dt|
+  int32_t* n;     // ncache: sample count of sorted candidate j (filled by prefix_k)
+  int32_t* o;     // ncache: first sample of sorted candidate j
+  int64_t ncache;
 };
 
 __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* a, int64_t lo, int64_t hi, int64_t v) {
@@ -275,9 +302,11 @@ __device__ __forceinline__ double dist_tab(const DevTable& T, int64_t dtt, int64
   return __dsqrt_rn(__dadd_rn(sq_delta(dtt, span_t, T.sq_t, T.lt), sq_delta(dc, span_c, T.sq_c, T.lc)));
 }
 
+// A query window in grid coordinates.  Grids hold < 2^27 cells, so grid
+// indices and cell offsets fit in int32.
 struct Win {
   int64_t Wt, Wc;
-  int64_t i0, i1, j0, j1;  // clipped grid index ranges (empty if i0 > i1 or j0 > j1)
+  int32_t i0, i1, j0, j1;  // clipped grid index ranges (empty if i0 > i1 or j0 > j1)
   bool cov_t, cov_c;
 };
 
@@ -291,80 +320,100 @@ __device__ __forceinline__ Win make_win(const DevTable& T, int32_t t, int32_t c,
   Win w;
   w.Wt = Wt;
   w.Wc = Wc;
-  w.cov_t = Wt >= kInfW || ((int64_t)t - Wt <= T.tt_lo && (int64_t)t + Wt >= T.tt_hi);
-  w.cov_c = Wc >= kInfW || ((int64_t)c - Wc <= T.c_lo && (int64_t)c + Wc >= T.c_hi);
-  const int64_t gt = T.gnt - 1, gc = T.gnc - 1;
-  w.i0 = Wt >= kInfW ? 0 : max((int64_t)0, (int64_t)t - Wt - T.tt_lo);
-  w.i1 = Wt >= kInfW ? gt : min(gt, (int64_t)t + Wt - T.tt_lo);
-  w.j0 = Wc >= kInfW ? 0 : max((int64_t)0, (int64_t)c - Wc - T.c_lo);
-  w.j1 = Wc >= kInfW ? gc : min(gc, (int64_t)c + Wc - T.c_lo);
+  const int64_t lt = (int64_t)t - Wt, ht = (int64_t)t + Wt, lc = (int64_t)c - Wc, hc = (int64_t)c + Wc;
+  w.cov_t = lt <= T.tt_lo && ht >= T.tt_hi;
+  w.cov_c = lc <= T.c_lo && hc >= T.c_hi;
+  w.i0 = (int32_t)min(max((int64_t)0, lt - T.tt_lo), T.gnt);
+  w.i1 = (int32_t)max(min(T.gnt - 1, ht - T.tt_lo), (int64_t)-1);
+  w.j0 = (int32_t)min(max((int64_t)0, lc - T.c_lo), T.gnc);
+  w.j1 = (int32_t)max(min(T.gnc - 1, hc - T.c_lo), (int64_t)-1);
   return w;
 }
 
-__device__ __forceinline__ long long sat_rect(const int32_t* S, int64_t st, const Win& w) {
+__device__ __forceinline__ int sat_rect(const int32_t* __restrict__ S, int32_t st, const Win& w) {
   if (w.i0 > w.i1 || w.j0 > w.j1) return 0;
-  return (long long)S[(w.i1 + 1) * st + w.j1 + 1] - S[w.i0 * st + w.j1 + 1] - S[(w.i1 + 1) * st + w.j0] +
-         S[w.i0 * st + w.j0];
+  const int32_t r0 = w.i0 * st, r1 = (w.i1 + 1) * st;
+  return S[r1 + w.j1 + 1] - S[r0 + w.j1 + 1] - S[r1 + w.j0] + S[r0 + w.j0];
 }
 
-// Rank-sort C <= cap/2 candidates of ws[0..C) into ws[cap/2 ..) (stable by
-// construction: keys (d, bucket) are unique).
-template <int NT>
-__device__ void rank_sort(const PoolWS& ws, int64_t C) {
-  using G = Grp<NT>;
-  double* sd = ws.d + ws.cap / 2;
-  int32_t* sb = ws.b + ws.cap / 2;
-  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  if (NT == 32 && C <= 32) {
-    const int lane = G::rank();
-    const double dm = lane < C ? ws.d[lane] : kInf;
-    const int32_t bm = lane < C ? ws.b[lane] : 0x7fffffff;
-    int r = 0;
-    for (int k = 0; k < C; k++) {
-      const double dk = __shfl_sync(kFull, dm, k);
-      const int32_t bk = __shfl_sync(kFull, bm, k);
-      r += cand_less(dk, bk, dm, bm) ? 1 : 0;
-    }
-    if (lane < C) {
-      sd[r] = dm;
-      sb[r] = bm;
-    }
-  } else {
-    // each thread ranks up to 4 own candidates held in registers against a
-    // single broadcast pass over all C candidates
-    constexpr int kOwn = 4;
-    for (int64_t base = 0; base < C; base += (int64_t)NT * kOwn) {
-      double od[kOwn];
-      int32_t ob[kOwn];
-      int orank[kOwn];
+// 2^((l - 8) / 4): the radius grid of the SAT probe.
+__constant__ double kRadiusStep[32] = {
+    0.25, 0.29730177875068026, 0.3535533905932738, 0.42044820762685725, 0.5, 0.5946035575013605,
+    0.7071067811865476, 0.8408964152537145, 1.0, 1.189207115002721, 1.4142135623730951, 1.681792830507429,
+    2.0, 2.378414230005442, 2.8284271247461903, 3.363585661014858, 4.0, 4.756828460010884, 5.656854249492381,
+    6.727171322029716, 8.0, 9.513656920021768, 11.313708498984761, 13.454342644059432, 16.0, 19.027313840043536,
+    22.627416997969522, 26.908685288118864, 32.0, 38.05462768008707, 45.254833995939045, 53.81737057623773};
+
+// Bitonic sort of 32*E (d, bucket) keys held E per lane (element q*32 + lane).
+template <int E>
+__device__ __forceinline__ void warp_bitonic(double (&d)[E], int32_t (&b)[E]) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-      for (int q = 0; q < kOwn; q++) {
-        const int64_t i = base + G::rank() + (int64_t)q * NT;
-        od[q] = i < C ? ws.d[i] : kInf;
-        ob[q] = i < C ? ws.b[i] : 0x7fffffff;
-        orank[q] = 0;
-      }
-      for (int64_t k = 0; k < C; k++) {
-        const double dk = ws.d[k];
-        const int32_t bk = ws.b[k];
+  for (int k = 2; k <= 32 * E; k <<= 1) {
 #pragma unroll
-        for (int q = 0; q < kOwn; q++) orank[q] += cand_less(dk, bk, od[q], ob[q]) ? 1 : 0;
-      }
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
 #pragma unroll
-      for (int q = 0; q < kOwn; q++) {
-        const int64_t i = base + G::rank() + (int64_t)q * NT;
-        if (i < C) {
-          sd[orank[q]] = od[q];
-          sb[orank[q]] = ob[q];
+        for (int q = 0; q < E; q++) {
+          const int p = q ^ (j >> 5);
+          if (p > q) {
+            const bool asc = ((q * 32 + lane) & k) == 0;
+            const bool sw = asc ? cand_less(d[p], b[p], d[q], b[q]) : cand_less(d[q], b[q], d[p], b[p]);
+            if (sw) {
+              const double td = d[q];
+              const int32_t tb = b[q];
+              d[q] = d[p];
+              b[q] = b[p];
+              d[p] = td;
+              b[p] = tb;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < E; q++) {
+          const double pd = __shfl_xor_sync(kFull, d[q], j);
+          const int32_t pb = __shfl_xor_sync(kFull, b[q], j);
+          const bool asc = ((q * 32 + lane) & k) == 0;
+          const bool lower = (lane & j) == 0;
+          const bool mine_less = cand_less(d[q], b[q], pd, pb);
+          if (mine_less != (lower == asc)) {
+            d[q] = pd;
+            b[q] = pb;
+          }
         }
       }
     }
   }
-  G::sync();
+}
+
+template <int E>
+__device__ __forceinline__ void warp_sort_ws(const PoolWS& ws, int C) {
+  const int lane = threadIdx.x & 31;
+  double d[E];
+  int32_t b[E];
+#pragma unroll
+  for (int q = 0; q < E; q++) {
+    const int i = q * 32 + lane;
+    d[q] = i < C ? ws.d[i] : __longlong_as_double(0x7ff0000000000000LL);
+    b[q] = i < C ? ws.b[i] : 0x7fffffff;
+  }
+  warp_bitonic<E>(d, b);
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < E; q++) {
+    const int i = q * 32 + lane;
+    if (i < C) {
+      ws.d[i] = d[q];
+      ws.b[i] = b[q];
+    }
+  }
+  __syncwarp();
 }
 
 // Shortest prefix of the sorted candidates (sd, sb)[0..C) reaching the floor,
-// or -1 if the C candidates hold fewer than mfloor samples.
+// or -1 if the C candidates hold fewer than mfloor samples.  Caches each
+// scanned candidate's sample count / first sample in ws.n / ws.o.
 template <int NT>
 __device__ int64_t prefix_k(const DevTable& T, const int32_t* sb, int64_t C, int64_t mfloor, const PoolWS& ws) {
   using G = Grp<NT>;
@@ -375,7 +424,12 @@ __device__ int64_t prefix_k(const DevTable& T, const int32_t* sb, int64_t C, int
     long long cnt = 0;
     if (j < lim) {
       const int32_t bb = sb[j];
-      cnt = T.bkt_off[bb + 1] - T.bkt_off[bb];
+      const int64_t o0 = T.bkt_off[bb];
+      cnt = T.bkt_off[bb + 1] - o0;
+      if (j < ws.ncache) {
+        ws.n[j] = (int32_t)cnt;
+        ws.o[j] = (int32_t)o0;
+      }
     }
     long long tot;
     const long long ex = G::excl_scan(cnt, tot, ws.scr);
@@ -388,50 +442,67 @@ __device__ int64_t prefix_k(const DevTable& T, const int32_t* sb, int64_t C, int
 
 // Windowed search driven by the summed-area tables:
 //   1. each of 32 lanes sizes a window for one radius r_l (geometric grid) and
-//      counts its samples in O(1) from ssat; the first radius r1 whose window
-//      holds >= floor samples (or spans the table) wins;
-//   2. every sample of that window lies within sqrt(2)*r1, so the window for
+//      counts its samples in O(1) from ssat; the first radius whose window
+//      holds >= floor samples (or spans the table) wins, refined by a second
+//      32-lane probe between the last miss and that hit -> r1;
+//   2. every sample of the r1 window lies within sqrt(2)*r1, so the window for
 //      r2 = sqrt(2)*r1 contains the whole pool and passes the exact d_edge
 //      test (checked anyway; -2 asks the caller for the growth fallback);
+//      candidates farther than r2 cannot be pooled and are dropped;
 //   3. the r2 window's buckets are enumerated row by row (bsat gives each
 //      row's conc sub-range in O(1)) or by scanning the tt slab, whichever is
 //      fewer items; distances use the exact squared-delta tables;
-//   4. candidates are rank-sorted (small C) or bitonic-sorted.
+//   4. candidates are sorted in registers (warp bitonic, <= 128) or shared
+//      memory, then the prefix reaching the floor is taken.
 // Returns K, -1 if the window exceeds ws.cap (escalate), -2 to fall back.
 template <int NT>
 __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws,
                                    int64_t& sorted_off) {
   using G = Grp<NT>;
+  EMU_PHASE_BEGIN();
   const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
-  const int64_t st = T.gnc + 1;
+  const int32_t st = (int32_t)T.gnc + 1;
   double gtd = 0.0, gcd = 0.0;
   if (span_t) gtd = (double)max(max((int64_t)T.tt_lo - t, (int64_t)t - T.tt_hi), (int64_t)0) / (double)span_t;
   if (span_c) gcd = (double)max(max((int64_t)T.c_lo - c, (int64_t)c - T.c_hi), (int64_t)0) / (double)span_c;
   const double rb = fmax(gtd, gcd);
   const double r0 = initial_radius(T, mfloor);
-  // ---- 1. radius search (32 radii per round, then 32 between the last miss and the first hit)
+  // ---- 1. radius search
   double r1 = -1.0, rmiss = -1.0;
-  for (int round = 0; round < 10 && r1 < 0.0; round++) {
+  double scale = 1.0;
+  for (int round = 0; round < 10 && r1 < 0.0; round++, scale *= 256.0) {
     bool ok = true;
     double rl = 0.0;
     if (G::rank() < 32) {
-      const int l = G::rank() + 32 * round;
-      rl = (l == 0) ? rb : rb + r0 * exp2((double)(l - 8) * 0.25);
+      const int l = G::rank();
+      rl = (round == 0 && l == 0) ? rb : rb + r0 * scale * kRadiusStep[l];
       const Win w = make_win(T, t, c, radius_to_w(rl, span_t), radius_to_w(rl, span_c));
       ok = (w.cov_t && w.cov_c) || sat_rect(T.ssat, st, w) >= mfloor;
     }
     const int first = G::count(!ok, ws.scr);  // ok is monotone in the radius
-    if (G::rank() == (first == 0 ? 0 : first - 1)) ws.dsh[0] = rl;
-    if (first < 32 && G::rank() == first) ws.dsh[1] = rl;
-    G::sync();
-    if (first < 32) {
-      r1 = ws.dsh[1];
-      if (first > 0 || round > 0) rmiss = (first > 0) ? ws.dsh[0] : rmiss;
+    if (NT == 32) {
+      const double hit = __shfl_sync(kFull, rl, first & 31);
+      const double miss = __shfl_sync(kFull, rl, (first + 31) & 31);
+      if (first < 32) {
+        r1 = hit;
+        if (first > 0) rmiss = miss;
+      } else {
+        rmiss = miss;
+      }
     } else {
-      rmiss = ws.dsh[0];
+      if (G::rank() == (first == 0 ? 0 : first - 1)) ws.dsh[0] = rl;
+      if (first < 32 && G::rank() == first) ws.dsh[1] = rl;
+      G::sync();
+      if (first < 32) {
+        r1 = ws.dsh[1];
+        if (first > 0) rmiss = ws.dsh[0];
+      } else {
+        rmiss = ws.dsh[0];
+      }
+      G::sync();
     }
-    G::sync();
   }
+  EMU_PHASE(0);
   if (r1 < 0.0) return -2;
   if (rmiss >= 0.0 && r1 > rmiss) {  // refine inside (rmiss, r1]
     bool ok = true;
@@ -442,28 +513,35 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
       ok = (w.cov_t && w.cov_c) || sat_rect(T.ssat, st, w) >= mfloor;
     }
     const int first = G::count(!ok, ws.scr);
-    if (first < 32 && G::rank() == first) ws.dsh[1] = rl;
-    G::sync();
-    if (first < 32) r1 = ws.dsh[1];
-    G::sync();
+    if (NT == 32) {
+      r1 = __shfl_sync(kFull, rl, first & 31);
+    } else {
+      if (first < 32 && G::rank() == first) ws.dsh[1] = rl;
+      G::sync();
+      if (first < 32) r1 = ws.dsh[1];
+      G::sync();
+    }
   }
+  EMU_PHASE(1);
   // ---- 2. the guaranteed window; pool members lie within dmax of the query
   const double r2 = r1 * 1.4142135623730951 * (1.0 + 1e-9);
   const Win w = make_win(T, t, c, radius_to_w(r2, span_t), radius_to_w(r2, span_c));
   const Win w1 = make_win(T, t, c, radius_to_w(r1, span_t), radius_to_w(r1, span_c));
   const bool exhaust = w1.cov_t && w1.cov_c && sat_rect(T.ssat, st, w1) < mfloor;
   const double dmax = exhaust ? __longlong_as_double(0x7ff0000000000000LL) : r2 * (1.0 + 1e-9);
-  const long long C = sat_rect(T.bsat, st, w);
+  const int C = sat_rect(T.bsat, st, w);
+  EMU_STAT(8, C);
+  EMU_PHASE(2);
   if (C > ws.cap) return -1;
   // ---- 3. enumerate (candidates beyond dmax cannot be pooled and are dropped)
-  long long pos = 0;
+  int pos = 0;
   if (C > 0) {
-    const int64_t nri = w.i1 - w.i0 + 1;
-    const int64_t b0 = T.bsat[w.i0 * st + T.gnc], b1 = T.bsat[(w.i1 + 1) * st + T.gnc];
+    const int32_t nri = w.i1 - w.i0 + 1;
+    const int32_t b0 = T.bsat[w.i0 * st + (st - 1)], b1 = T.bsat[(w.i1 + 1) * st + (st - 1)];
     if (b1 - b0 <= 2 * nri || C == b1 - b0) {  // scan the tt slab
-      const int64_t clo = (int64_t)T.c_lo + w.j0, chi = (int64_t)T.c_lo + w.j1;
-      for (int64_t base = b0; base < b1; base += NT) {
-        const int64_t b = base + G::rank();
+      const int32_t clo = T.c_lo + w.j0, chi = T.c_lo + w.j1;
+      for (int32_t base = b0; base < b1; base += NT) {
+        const int32_t b = base + G::rank();
         bool in = false;
         double d = 0.0;
         if (b < b1) {
@@ -474,37 +552,37 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
           }
         }
         long long tot;
-        const long long ex = G::excl_scan(in ? 1 : 0, tot, ws.scr);
+        const int ex = (int)G::excl_scan(in ? 1 : 0, tot, ws.scr);
         if (in) {
           ws.d[pos + ex] = d;
-          ws.b[pos + ex] = (int32_t)b;
+          ws.b[pos + ex] = b;
         }
-        pos += tot;
+        pos += (int)tot;
       }
     } else {  // row by row: bsat gives each row's conc sub-range
-      for (int64_t base = w.i0; base <= w.i1; base += NT) {
-        const int64_t i = base + G::rank();
-        long long len = 0;
+      for (int32_t base = w.i0; base <= w.i1; base += NT) {
+        const int32_t i = base + G::rank();
+        int len = 0;
         int32_t lo = 0;
         if (i <= w.i1) {
-          const int64_t rs = T.bsat[i * st + T.gnc];
-          lo = (int32_t)(rs + T.bsat[(i + 1) * st + w.j0] - T.bsat[i * st + w.j0]);
-          const int64_t hi = rs + T.bsat[(i + 1) * st + w.j1 + 1] - T.bsat[i * st + w.j1 + 1];
-          len = hi - lo;
+          const int32_t r0i = i * st, r1i = r0i + st;
+          const int32_t rs = T.bsat[r0i + st - 1];
+          lo = rs + T.bsat[r1i + w.j0] - T.bsat[r0i + w.j0];
+          len = rs + T.bsat[r1i + w.j1 + 1] - T.bsat[r0i + w.j1 + 1] - lo;
         }
         long long tot;
-        const long long ex = G::excl_scan(len, tot, ws.scr);
+        const int ex = (int)G::excl_scan(len, tot, ws.scr);
         ws.rows[G::rank()] = lo;
-        ws.rows[NT + G::rank()] = (int32_t)ex;
+        ws.rows[NT + G::rank()] = ex;
         ws.rows[2 * NT + G::rank()] = (int32_t)((int64_t)t - (T.tt_lo + i));
         G::sync();
-        const int nrow = (int)min((int64_t)NT, w.i1 - base + 1);
-        for (long long kb = 0; kb < tot; kb += NT) {
-          const long long k = kb + G::rank();
+        const int nrow = min(NT, w.i1 - base + 1);
+        for (int kb = 0; kb < (int)tot; kb += NT) {
+          const int k = kb + G::rank();
           bool in = false;
           double d = 0.0;
           int32_t bb = 0;
-          if (k < tot) {
+          if (k < (int)tot) {
             int lo_r = 0, hi_r = nrow;  // last row with prefix <= k
             while (hi_r - lo_r > 1) {
               const int mid = (lo_r + hi_r) >> 1;
@@ -513,27 +591,34 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
               else
                 hi_r = mid;
             }
-            bb = ws.rows[lo_r] + (int32_t)(k - ws.rows[NT + lo_r]);
+            bb = ws.rows[lo_r] + (k - ws.rows[NT + lo_r]);
             d = dist_tab(T, ws.rows[2 * NT + lo_r], (int64_t)c - T.bkt_conc[bb], span_t, span_c);
             in = d <= dmax;
           }
           long long kt;
-          const long long ex2 = G::excl_scan(in ? 1 : 0, kt, ws.scr);
+          const int ex2 = (int)G::excl_scan(in ? 1 : 0, kt, ws.scr);
           if (in) {
             ws.d[pos + ex2] = d;
             ws.b[pos + ex2] = bb;
           }
-          pos += kt;
+          pos += (int)kt;
         }
         G::sync();
       }
     }
   }
   G::sync();
+  EMU_PHASE(3);
+  EMU_STAT(9, pos);
   // ---- 4. order
-  if (2 * pos <= ws.cap && pos <= (NT == 32 ? 128 : NT)) {
-    rank_sort<NT>(ws, pos);
-    sorted_off = ws.cap / 2;
+  sorted_off = 0;
+  if (NT == 32 && pos <= 128) {
+    if (pos <= 32)
+      warp_sort_ws<1>(ws, pos);
+    else if (pos <= 64)
+      warp_sort_ws<2>(ws, pos);
+    else
+      warp_sort_ws<4>(ws, pos);
   } else {
     int64_t P = 1;
     while (P < pos) P <<= 1;
@@ -543,15 +628,204 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
     }
     G::sync();
     if (P > 1) bitonic_sort<NT>(ws.d, ws.b, P);
-    sorted_off = 0;
   }
-  const double* sd = ws.d + sorted_off;
-  const int32_t* sb = ws.b + sorted_off;
-  const int64_t K = prefix_k<NT>(T, sb, pos, mfloor, ws);
+  EMU_PHASE(4);
+  const int64_t K = prefix_k<NT>(T, ws.b, pos, mfloor, ws);
+  EMU_PHASE(5);
+  EMU_STAT(10, K);
+  EMU_STAT(11, 1);
   if (K < 0) return (w.cov_t && w.cov_c) ? pos : -2;
-  const double et = w.cov_t ? __longlong_as_double(0x7ff0000000000000LL) : norm_dist(w.Wt + 1, 0, span_t, span_c);
-  const double ec = w.cov_c ? __longlong_as_double(0x7ff0000000000000LL) : norm_dist(0, w.Wc + 1, span_t, span_c);
-  return sd[K - 1] < fmin(et, ec) ? K : -2;
+  const double et = w.cov_t ? __longlong_as_double(0x7ff0000000000000LL) : dist_tab(T, w.Wt + 1, 0, span_t, span_c);
+  const double ec = w.cov_c ? __longlong_as_double(0x7ff0000000000000LL) : dist_tab(T, 0, w.Wc + 1, span_t, span_c);
+  return ws.d[K - 1] < fmin(et, ec) ? K : -2;
+}
+
+// ------------------------------------------------- thread-per-key SAT passes
+// The scalar parts of the SAT search run one key per THREAD (k_pool_win /
+// k_pool_enum); the warp kernel then only sorts, takes the prefix and builds
+// the CDF.  Same window rules as pool_search_sat (see its comment).
+struct KeyWin {
+  int64_t Wt, Wc;          // r2 window half-widths (kInfW = unbounded)
+  double dmax;             // candidates farther than this cannot be pooled
+  int32_t i0, i1, j0, j1;  // r2 window in grid coordinates
+  int32_t off, cap;        // candidate scratch slice [off, off + cap)
+  int32_t pos;             // candidates written (<= cap)
+  int32_t flags;           // kWinReady | kWinCovT | kWinCovC
+};
+constexpr int32_t kWinReady = 1, kWinCovT = 2, kWinCovC = 4;
+
+__device__ __forceinline__ bool win_ok(const DevTable& T, int32_t t, int32_t c, double r, int64_t span_t,
+                                       int64_t span_c, int32_t st, int64_t mfloor) {
+  const Win w = make_win(T, t, c, radius_to_w(r, span_t), radius_to_w(r, span_c));
+  return (w.cov_t && w.cov_c) || sat_rect(T.ssat, st, w) >= mfloor;
+}
+
+// Radius search by doubling + bisection on the SAT (thread level).  Returns
+// false if the table has no grid (the warp kernel then runs the full search).
+__device__ bool key_window(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, KeyWin& kw) {
+  kw.flags = 0;
+  kw.pos = 0;
+  if (T.gnt <= 0) return false;
+  const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
+  const int32_t st = (int32_t)T.gnc + 1;
+  double gtd = 0.0, gcd = 0.0;
+  if (span_t) gtd = (double)max(max((int64_t)T.tt_lo - t, (int64_t)t - T.tt_hi), (int64_t)0) / (double)span_t;
+  if (span_c) gcd = (double)max(max((int64_t)T.c_lo - c, (int64_t)c - T.c_hi), (int64_t)0) / (double)span_c;
+  const double rb = fmax(gtd, gcd);
+  double r1;
+  if (win_ok(T, t, c, rb, span_t, span_c, st, mfloor)) {
+    r1 = rb;
+  } else {
+    double lo = rb, step = initial_radius(T, mfloor), hi = rb + step;
+    int guard = 0;
+    while (!win_ok(T, t, c, hi, span_t, span_c, st, mfloor)) {
+      lo = hi;
+      step *= 2.0;
+      hi = rb + step;
+      if (++guard > 200) return false;
+    }
+    for (int it = 0; it < 12; it++) {
+      const double mid = 0.5 * (lo + hi);
+      if (win_ok(T, t, c, mid, span_t, span_c, st, mfloor))
+        hi = mid;
+      else
+        lo = mid;
+    }
+    r1 = hi;
+  }
+  const double r2 = r1 * 1.4142135623730951 * (1.0 + 1e-9);
+  const Win w = make_win(T, t, c, radius_to_w(r2, span_t), radius_to_w(r2, span_c));
+  const Win w1 = make_win(T, t, c, radius_to_w(r1, span_t), radius_to_w(r1, span_c));
+  const bool exhaust = w1.cov_t && w1.cov_c && sat_rect(T.ssat, st, w1) < mfloor;
+  kw.Wt = w.Wt;
+  kw.Wc = w.Wc;
+  kw.i0 = w.i0;
+  kw.i1 = w.i1;
+  kw.j0 = w.j0;
+  kw.j1 = w.j1;
+  kw.dmax = exhaust ? __longlong_as_double(0x7ff0000000000000LL) : r2 * (1.0 + 1e-9);
+  kw.cap = sat_rect(T.bsat, st, w);
+  kw.flags = kWinReady | (w.cov_t ? kWinCovT : 0) | (w.cov_c ? kWinCovC : 0);
+  return true;
+}
+
+// Warp: enumerate the window's candidates into ws[0..pos) from the occupancy
+// bitmap (one row per lane per round: the row's 1-2 bitmap words give its
+// buckets; bucket index = rowbase + wpre + popcount, conc = bit position), then
+// drop those farther than dmax.  Returns pos, or -1 if they do not fit.
+__device__ int warp_enumerate(const DevTable& T, int32_t t, int32_t c, const KeyWin& kw, const PoolWS& ws) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
+  if (kw.cap <= 0) return 0;
+  if (kw.cap > ws.cap) return -1;
+  const int32_t w0 = kw.j0 >> 5, w1 = kw.j1 >> 5;
+  int pos = 0;
+  for (int32_t rbase = kw.i0; rbase <= kw.i1; rbase += 32) {
+    const int32_t i = rbase + lane;
+    int cnt = 0;
+    if (i <= kw.i1) {
+      for (int32_t wd = w0; wd <= w1; wd++) {
+        uint32_t m = T.bmap[(int64_t)i * T.wpr + wd];
+        if (wd == w0) m &= 0xffffffffu << (kw.j0 & 31);
+        if (wd == w1 && (kw.j1 & 31) != 31) m &= (2u << (kw.j1 & 31)) - 1u;
+        cnt += __popc(m);
+      }
+    }
+    int x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (cnt) {
+      int p = pos + x - cnt;
+      const int32_t rb = T.rowbase[i];
+      const double sqt = sq_delta((int64_t)t - (T.tt_lo + i), span_t, T.sq_t, T.lt);
+      for (int32_t wd = w0; wd <= w1; wd++) {
+        const int64_t wi = (int64_t)i * T.wpr + wd;
+        const uint32_t word = T.bmap[wi];
+        uint32_t m = word;
+        if (wd == w0) m &= 0xffffffffu << (kw.j0 & 31);
+        if (wd == w1 && (kw.j1 & 31) != 31) m &= (2u << (kw.j1 & 31)) - 1u;
+        if (!m) continue;
+        const int32_t pre = rb + T.wpre[wi];
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1u;
+          const int32_t jj = wd * 32 + j;
+          ws.d[p] = __dsqrt_rn(__dadd_rn(sqt, sq_delta((int64_t)c - (T.c_lo + jj), span_c, T.sq_c, T.lc)));
+          ws.b[p] = pre + __popc(word & ((1u << j) - 1u));
+          p++;
+        }
+      }
+    }
+    pos += __shfl_sync(kFull, x, 31);
+  }
+  __syncwarp();
+  // in-place compaction: keep d <= dmax (write index never passes read index)
+  int out = 0;
+  for (int base = 0; base < pos; base += 32) {
+    const int k = base + lane;
+    double d = 0.0;
+    int32_t b = 0;
+    bool keep = false;
+    if (k < pos) {
+      d = ws.d[k];
+      b = ws.b[k];
+      keep = d <= kw.dmax;
+    }
+    const unsigned m = __ballot_sync(kFull, keep);
+    __syncwarp();
+    if (keep) {
+      ws.d[out + __popc(m & lt)] = d;
+      ws.b[out + __popc(m & lt)] = b;
+    }
+    out += __popc(m);
+    __syncwarp();
+  }
+  return out;
+}
+
+// Warp fast path from a thread-computed window: enumerate, sort, take the
+// prefix, verify.  Returns K (sorted pool in ws[0..K)), or -2 to fall back.
+__device__ int64_t pool_from_window(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const KeyWin& kw,
+                                    const PoolWS& ws) {
+  EMU_PHASE_BEGIN();
+  const int pos = warp_enumerate(T, t, c, kw, ws);
+  EMU_PHASE(3);
+  EMU_STAT(8, kw.cap);
+  EMU_STAT(9, pos);
+  if (pos < 0) return -2;
+  if (pos <= 32)
+    warp_sort_ws<1>(ws, pos);
+  else if (pos <= 64)
+    warp_sort_ws<2>(ws, pos);
+  else if (pos <= 128)
+    warp_sort_ws<4>(ws, pos);
+  else {
+    int64_t P = 1;
+    while (P < pos) P <<= 1;
+    if (P > ws.cap) return -2;
+    for (int64_t i = pos + (threadIdx.x & 31); i < P; i += 32) {
+      ws.d[i] = __longlong_as_double(0x7ff0000000000000LL);
+      ws.b[i] = 0x7fffffff;
+    }
+    __syncwarp();
+    bitonic_sort<32>(ws.d, ws.b, P);
+  }
+  EMU_PHASE(4);
+  const int64_t K = prefix_k<32>(T, ws.b, pos, mfloor, ws);
+  EMU_PHASE(5);
+  EMU_STAT(10, K);
+  EMU_STAT(11, 1);
+  const bool cov_t = kw.flags & kWinCovT, cov_c = kw.flags & kWinCovC;
+  if (K < 0) return (cov_t && cov_c) ? pos : -2;
+  const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  const double et = cov_t ? kInf : dist_tab(T, kw.Wt + 1, 0, span_t, span_c);
+  const double ec = cov_c ? kInf : dist_tab(T, 0, kw.Wc + 1, span_t, span_c);
+  return ws.d[K - 1] < fmin(et, ec) ? K : -2;
 }
 
 // Dispatcher: SAT search when the table has a grid, else (or if the SAT
@@ -559,14 +833,16 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
 // is at ws.d/ws.b + sorted_off.
 template <int NT>
 __device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws,
-                               int64_t& sorted_off) {
+                               int64_t& sorted_off, bool& cached) {
   sorted_off = 0;
+  cached = true;
   if (T.gnt > 0) {
     const int64_t K = pool_search_sat<NT>(T, t, c, mfloor, ws, sorted_off);
     if (K != -2) return K;
     Grp<NT>::sync();
     sorted_off = 0;
   }
+  cached = false;
   return pool_search_grow<NT>(T, t, c, mfloor, ws);
 }
 
@@ -574,16 +850,17 @@ __device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t 
 // Writes (optionally) bucket/dist/prob/cdf arrays and/or cache slots.
 template <int NT>
 __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, const PoolWS& ws_in,
-                            int64_t sorted_off, Slot* slots,
+                            int64_t sorted_off, bool cached, Slot* slots,
                             int32_t* o_bkt, double* o_dist, double* o_prob, double* o_cdf) {
   using G = Grp<NT>;
   PoolWS ws = ws_in;
   ws.d += sorted_off;
   ws.b += sorted_off;
+  const bool use_cache = cached && K <= ws.ncache;
   for (int64_t j = G::rank(); j < K; j += NT) {
     int32_t bb = ws.b[j];
     double d = ws.d[j];
-    int64_t n = T.bkt_off[bb + 1] - T.bkt_off[bb];
+    const int64_t n = use_cache ? (int64_t)ws.n[j] : T.bkt_off[bb + 1] - T.bkt_off[bb];
     if (o_bkt) o_bkt[j] = bb;
     if (o_dist) o_dist[j] = d;
     double x = d > eps ? d : eps;  // np.maximum(d, eps)
@@ -637,12 +914,17 @@ __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, 
     double cdf = __ddiv_rn(ws.d[j], last);
     if (o_cdf) o_cdf[j] = cdf;
     if (slots) {
-      int32_t bb = ws.b[j];
-      int64_t o0 = T.bkt_off[bb];
       Slot s;
       s.cdf = cdf;
-      s.soff = (int32_t)o0;
-      s.n = (int32_t)(T.bkt_off[bb + 1] - o0);
+      if (use_cache) {
+        s.soff = ws.o[j];
+        s.n = ws.n[j];
+      } else {
+        const int32_t bb = ws.b[j];
+        const int64_t o0 = T.bkt_off[bb];
+        s.soff = (int32_t)o0;
+        s.n = (int32_t)(T.bkt_off[bb + 1] - o0);
+      }
       slots[j] = s;
     }
   }

@@ -41,6 +41,9 @@ void TableBuf::release() {
   cudaFree(row_start);
   cudaFree(bsat);
   cudaFree(ssat);
+  cudaFree(bmap);
+  cudaFree(wpre);
+  cudaFree(rowbase);
   cudaFree(sq_t);
   cudaFree(sq_c);
   *this = TableBuf();
@@ -65,6 +68,10 @@ DevTable TableBuf::view() const {
   t.ssat = ssat;
   t.gnt = gnt;
   t.gnc = gnc;
+  t.bmap = bmap;
+  t.wpre = wpre;
+  t.rowbase = rowbase;
+  t.wpr = wpr;
   t.sq_t = sq_t;
   t.sq_c = sq_c;
   t.lt = lt;
@@ -111,11 +118,35 @@ int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, c
       S[row + j] = (int32_t)(S[prev + j] + rs);
     }
   }
+  // occupancy bitmap + per-word prefix counts + row bases
+  const int64_t wpr = (gnc + 31) / 32;
+  std::vector<uint32_t> bm((size_t)(gnt * wpr), 0u);
+  std::vector<int32_t> wp((size_t)(gnt * wpr), 0), rbase((size_t)gnt + 1, 0);
+  for (int64_t b = 0; b < tb.nb; b++) {
+    const int64_t i = (int64_t)h_tt[b] - tb.tt_lo, j = (int64_t)h_cc[b] - tb.c_lo;
+    bm[(size_t)(i * wpr + j / 32)] |= 1u << (j % 32);
+    rbase[(size_t)i + 1] += 1;
+  }
+  for (int64_t i = 0; i < gnt; i++) {
+    rbase[(size_t)i + 1] += rbase[(size_t)i];
+    int32_t acc = 0;
+    for (int64_t k = 0; k < wpr; k++) {
+      wp[(size_t)(i * wpr + k)] = acc;
+      acc += __builtin_popcount(bm[(size_t)(i * wpr + k)]);
+    }
+  }
   EMU_CUDA(cudaMalloc((void**)&tb.bsat, 4 * cells));
   EMU_CUDA(cudaMalloc((void**)&tb.ssat, 4 * cells));
+  EMU_CUDA(cudaMalloc((void**)&tb.bmap, 4 * gnt * wpr));
+  EMU_CUDA(cudaMalloc((void**)&tb.wpre, 4 * gnt * wpr));
+  EMU_CUDA(cudaMalloc((void**)&tb.rowbase, 4 * (gnt + 1)));
   EMU_CUDA(cudaMemcpyAsync(tb.bsat, B.data(), 4 * cells, cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMemcpyAsync(tb.ssat, S.data(), 4 * cells, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.bmap, bm.data(), 4 * gnt * wpr, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.wpre, wp.data(), 4 * gnt * wpr, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.rowbase, rbase.data(), 4 * (gnt + 1), cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaStreamSynchronize(s));
+  tb.wpr = (int32_t)wpr;
   tb.gnt = gnt;
   tb.gnc = gnc;
   return EMU_OK;

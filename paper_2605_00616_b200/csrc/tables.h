@@ -16,6 +16,10 @@ struct TableBuf {
   int32_t* bsat = nullptr;
   int32_t* ssat = nullptr;
   int64_t gnt = 0, gnc = 0;
+  uint32_t* bmap = nullptr;
+  int32_t* wpre = nullptr;
+  int32_t* rowbase = nullptr;
+  int32_t wpr = 0;
   double* sq_t = nullptr;
   double* sq_c = nullptr;
   int64_t lt = 0, lc = 0;
