@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -39,6 +41,7 @@ constexpr int kCtaSmem = kCtaCap * 12;
 constexpr int kCtaCache = 1024;  // cached counts/offsets per CTA workspace
 constexpr int kCtaGrid = kNumSMs;
 constexpr int kSampleThreads = 256;
+constexpr int kQPT = 4;  // queries per thread, interleaved for memory-level parallelism
 
 struct BatchCtl {
   unsigned long long cand_used;  // candidate scratch bump pointer
@@ -187,22 +190,47 @@ __global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Key
 __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t* __restrict__ qc,
                        const uint8_t* __restrict__ qp, int64_t Q, int32_t* nk_tt, int32_t* nk_c, uint8_t* nk_p,
                        int64_t* nk_e, BatchCtl* ctl) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Q; i += (int64_t)gridDim.x * blockDim.x) {
-    const int ph = qp[i] ? 1 : 0;
-    const int32_t t = qt[i], c = qc[i];
-    const int64_t idx = map_find<true>(m, ph, t, c);
-    if (idx < 0) {
-      atomicOr(&ctl->flags, FLAG_HASH);
-      continue;
+  const int64_t tile = (int64_t)blockDim.x * kQPT;
+  for (int64_t b0 = (int64_t)blockIdx.x * tile; b0 < Q; b0 += (int64_t)gridDim.x * tile) {  // warp-uniform trip count
+    const int64_t base = b0 + threadIdx.x;
+    int32_t t[kQPT], c[kQPT];
+    int ph[kQPT];
+    int64_t idx[kQPT];
+    long long cur[kQPT];
+#pragma unroll
+    for (int j = 0; j < kQPT; j++) {
+      const int64_t i = base + (int64_t)j * blockDim.x;
+      idx[j] = -2;
+      if (i < Q) {
+        ph[j] = qp[i] ? 1 : 0;  // kept in L2: k_sample re-reads the keys next
+        t[j] = qt[i];
+        c[j] = qc[i];
+        idx[j] = map_find<true>(m, ph[j], t[j], c[j]);
+      }
+      cur[j] = idx[j] >= 0 ? *(volatile long long*)map_entry_ptr(m, idx[j]) : -1;
     }
-    long long* e = map_entry_ptr(m, idx);
-    if (*(volatile long long*)e != kEntryEmpty) continue;
-    if (atomicCAS((unsigned long long*)e, 0ULL, (unsigned long long)kEntryPending) == 0ULL) {
-      int pos = atomicAdd(&ctl->new_count, 1);
-      nk_tt[pos] = t;
-      nk_c[pos] = c;
-      nk_p[pos] = (uint8_t)ph;
-      nk_e[pos] = idx;
+#pragma unroll
+    for (int j = 0; j < kQPT; j++)
+      if (idx[j] == -1) atomicOr(&ctl->flags, FLAG_HASH);
+    // claim empty entries; winners append their key (one atomic per warp)
+#pragma unroll
+    for (int j = 0; j < kQPT; j++) {
+      bool won = false;
+      if (idx[j] >= 0 && cur[j] == kEntryEmpty)
+        won = atomicCAS((unsigned long long*)map_entry_ptr(m, idx[j]), 0ULL, (unsigned long long)kEntryPending) == 0ULL;
+      const unsigned ballot = __ballot_sync(kFull, won);
+      if (!ballot) continue;
+      const int lane = threadIdx.x & 31;
+      int wbase = 0;
+      if (lane == __ffs(ballot) - 1) wbase = atomicAdd(&ctl->new_count, __popc(ballot));
+      wbase = __shfl_sync(kFull, wbase, __ffs(ballot) - 1);
+      if (won) {
+        const int pos = wbase + __popc(ballot & ((1u << lane) - 1u));
+        nk_tt[pos] = t[j];
+        nk_c[pos] = c[j];
+        nk_p[pos] = (uint8_t)ph[j];
+        nk_e[pos] = idx[j];
+      }
     }
   }
 }
@@ -303,8 +331,52 @@ __device__ __forceinline__ int64_t upper_bound_cdf(const Slot* __restrict__ P, i
   return lo;
 }
 
+// Lemire index for query qid after the first word w0 (EXPLICIT: hash32 chain;
+// PHILOX: the block-0 spare word, then blocks 1, 2, ... of Philox(qid)).
 template <int RNG>
-__global__ void __launch_bounds__(kSampleThreads) k_sample(MapView m, const Slot* __restrict__ arena,
+__device__ __forceinline__ uint32_t draw_index(uint32_t n, uint32_t w0, uint4 px, uint64_t qid, uint2 key) {
+  if (RNG == EMU_RNG_EXPLICIT) {
+    uint32_t st = w0;
+    return lemire_index(n, w0, [&]() {
+      st = hash32(st);
+      return st;
+    });
+  }
+  int pos = 3;
+  uint32_t blk = 0;
+  uint4 buf = px;
+  return lemire_index(n, w0, [&]() {
+    if (pos == 4) {
+      blk++;
+      buf = philox4x32_10(make_uint4((uint32_t)qid, (uint32_t)(qid >> 32), blk, 0u), key);
+      pos = 0;
+    }
+    const uint32_t v = pos == 0 ? buf.x : pos == 1 ? buf.y : pos == 2 ? buf.z : buf.w;
+    pos++;
+    return v;
+  });
+}
+
+
+// One thread handles kQPT queries (block-strided so every load stays
+// coalesced) and advances their dependent chains -- map entry, CDF binary
+// search, slot, sample -- in lockstep, so 4 independent loads are in flight
+// per step.  Per-query inputs/outputs are streamed with evict-first hints so
+// the key map, pool arena and samples stay L2-resident.
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p, bool hint) {
+  return hint ? __ldcs(p) : *p;
+}
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, T v, bool hint) {
+  if (hint)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
+template <int RNG, int QPT, bool HINT>
+__global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 : 4)) k_sample(MapView m, const Slot* __restrict__ arena,
                                                            const double* __restrict__ s0, const double* __restrict__ s1,
                                                            const int32_t* __restrict__ qt, const int32_t* __restrict__ qc,
                                                            const uint8_t* __restrict__ qp, int64_t Q,
@@ -312,59 +384,95 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(MapView m, const Slot
                                                            const uint32_t* __restrict__ uidx, uint64_t seed,
                                                            uint64_t ctr_base, double* __restrict__ out_lat,
                                                            int32_t* __restrict__ out_sidx, int* flags) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Q; i += (int64_t)gridDim.x * blockDim.x) {
-    const int ph = qp[i] ? 1 : 0;
-    const int64_t idx = map_find<false>(m, ph, qt[i], qc[i]);
-    const long long e = idx >= 0 ? *map_entry_ptr(m, idx) : 0;
-    if (e <= 0) {
-      out_lat[i] = __longlong_as_double(0x7ff8000000000000LL);
-      out_sidx[i] = -1;
-      atomicOr(flags, FLAG_MISSING);
-      continue;
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const int64_t tile = (int64_t)blockDim.x * QPT;
+  for (int64_t base = (int64_t)blockIdx.x * tile + threadIdx.x; base < Q; base += (int64_t)gridDim.x * tile) {
+    int64_t i[QPT];
+    bool v[QPT];
+    int ph[QPT];
+    long long e[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      i[j] = base + (int64_t)j * blockDim.x;
+      v[j] = i[j] < Q;
+      ph[j] = 0;
+      int32_t t = 0, c = 0;
+      if (v[j]) {
+        ph[j] = ld_stream(qp + i[j], HINT) ? 1 : 0;
+        t = ld_stream(qt + i[j], HINT);
+        c = ld_stream(qc + i[j], HINT);
+      }
+      const int64_t idx = v[j] ? map_find<false>(m, ph[j], t, c) : -1;
+      e[j] = idx >= 0 ? *map_entry_ptr(m, idx) : 0;
     }
-    const int64_t K = (int64_t)((unsigned long long)e >> 32);
-    const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
-    uint64_t us;
-    uint32_t w0;
-    uint4 px = make_uint4(0, 0, 0, 0);
-    const uint64_t qid = ctr_base + (uint64_t)i;
-    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    if (RNG == EMU_RNG_EXPLICIT) {
-      us = usel[i];
-      w0 = uidx[i];
-    } else {
-      px = philox4x32_10(make_uint4((uint32_t)qid, (uint32_t)(qid >> 32), 0u, 0u), key);
-      us = (uint64_t)px.x | ((uint64_t)px.y << 32);
-      w0 = px.z;
+    uint64_t us[QPT];
+    uint32_t w0[QPT];
+    uint4 px[QPT];
+    int32_t lo[QPT], hi[QPT], start[QPT];
+    double u[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      px[j] = make_uint4(0, 0, 0, 0);
+      if (RNG == EMU_RNG_EXPLICIT) {
+        us[j] = v[j] ? ld_stream(usel + i[j], HINT) : 0;
+        w0[j] = v[j] ? ld_stream(uidx + i[j], HINT) : 0;
+      } else {
+        const uint64_t qid = ctr_base + (uint64_t)i[j];
+        px[j] = philox4x32_10(make_uint4((uint32_t)qid, (uint32_t)(qid >> 32), 0u, 0u), key);
+        us[j] = (uint64_t)px[j].x | ((uint64_t)px[j].y << 32);
+        w0[j] = px[j].z;
+      }
+      u[j] = unit_double(us[j]);
+      const bool ok = v[j] && e[j] > 0;
+      start[j] = ok ? (int32_t)((unsigned long long)e[j] & 0xffffffffULL) : 0;
+      lo[j] = 0;
+      hi[j] = ok ? (int32_t)((unsigned long long)e[j] >> 32) : 0;
     }
-    const double u = unit_double(us);
-    const Slot* P = arena + start;
-    const Slot s = P[upper_bound_cdf(P, K, u)];
-    uint32_t j;
-    if (RNG == EMU_RNG_EXPLICIT) {
-      uint32_t st = w0;
-      j = lemire_index((uint32_t)s.n, w0, [&]() {
-        st = hash32(st);
-        return st;
-      });
-    } else {
-      int pos = 3;
-      uint32_t blk = 0;
-      uint4 buf = px;
-      j = lemire_index((uint32_t)s.n, w0, [&]() {
-        if (pos == 4) {
-          blk++;
-          buf = philox4x32_10(make_uint4((uint32_t)qid, (uint32_t)(qid >> 32), blk, 0u), key);
-          pos = 0;
+    // lockstep searchsorted(cdf, u, 'right') over the QPT pools
+    for (;;) {
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < QPT; j++) {
+        if (lo[j] < hi[j]) {
+          any = true;
+          const int32_t mid = (lo[j] + hi[j]) >> 1;
+          if (arena[start[j] + mid].cdf <= u[j])
+            lo[j] = mid + 1;
+          else
+            hi[j] = mid;
         }
-        uint32_t v = pos == 0 ? buf.x : pos == 1 ? buf.y : pos == 2 ? buf.z : buf.w;
-        pos++;
-        return v;
-      });
+      }
+      if (!any) break;
     }
-    const int32_t sidx = s.soff + (int32_t)j;
-    out_lat[i] = (ph ? s1 : s0)[sidx];
-    out_sidx[i] = sidx;
+    Slot sl[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; j++)
+      if (v[j] && e[j] > 0) sl[j] = arena[start[j] + lo[j]];
+    double lat[QPT];
+    int32_t sidx[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      if (!v[j]) continue;
+      if (e[j] <= 0) {
+        sidx[j] = -1;
+        continue;
+      }
+      const uint32_t k = draw_index<RNG>((uint32_t)sl[j].n, w0[j], px[j], ctr_base + (uint64_t)i[j], key);
+      sidx[j] = sl[j].soff + (int32_t)k;
+      lat[j] = (ph[j] ? s1 : s0)[sidx[j]];
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      if (!v[j]) continue;
+      if (sidx[j] < 0) {
+        st_stream(out_lat + i[j], __longlong_as_double(0x7ff8000000000000LL), HINT);
+        st_stream(out_sidx + i[j], -1, HINT);
+        atomicOr(flags, FLAG_MISSING);
+      } else {
+        st_stream(out_lat + i[j], lat[j], HINT);
+        st_stream(out_sidx + i[j], sidx[j], HINT);
+      }
+    }
   }
 }
 
@@ -773,7 +881,7 @@ static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, c
   int rc = ensure_key_capacity(o, std::min<int64_t>(Q, map_entries(o)));
   if (rc) return rc;
   EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
-  EMU_LAUNCH("mark", s, k_mark<<<grid_for(Q, 256, kNumSMs * 16), 256, 0, s>>>(o->map, qt, qc, qp, Q, o->nk_tt, o->nk_c,
+  EMU_LAUNCH("mark", s, k_mark<<<grid_for((Q + kQPT - 1) / kQPT, 256, kNumSMs * 16), 256, 0, s>>>(o->map, qt, qc, qp, Q, o->nk_tt, o->nk_c,
                                                                              o->nk_p, o->nk_e, o->ctl));
   EMU_CUDA(cudaGetLastError());
   Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
@@ -815,6 +923,56 @@ static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s,
   return chunk;
 }
 
+// Sampler variant: queries per thread and streaming-cache hints.  Default
+// (1, hints); EMU_SAMPLE_VARIANT="qpt,hint" overrides for tuning runs.
+static void sample_variant(int rng_mode, int* qpt, int* hint) {
+  static int q = -1, h = -1;
+  if (q < 0) {
+    q = 1;
+    h = -1;  // default: hints for EXPLICIT (streams 21 B/query), none for PHILOX (measured)
+    const char* v = getenv("EMU_SAMPLE_VARIANT");
+    if (v) sscanf(v, "%d,%d", &q, &h);
+    if (q != 1 && q != 2 && q != 4) q = 1;
+  }
+  *qpt = q;
+  *hint = h < 0 ? (rng_mode == EMU_RNG_EXPLICIT ? 1 : 0) : (h ? 1 : 0);
+}
+
+template <int RNG, int QPT, bool HINT>
+static void launch_sample_t(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t n,
+                            const uint64_t* us, const uint32_t* ui, uint64_t seed, uint64_t ctr, double* lat,
+                            int32_t* sidx, cudaStream_t s) {
+  const int grid = grid_for((n + QPT - 1) / QPT, kSampleThreads, kNumSMs * 16);
+  EMU_LAUNCH("sample", s, k_sample<RNG, QPT, HINT><<<grid, kSampleThreads, 0, s>>>(
+                              o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, n, us, ui, seed,
+                              ctr, lat, sidx, &o->ctl->flags));
+}
+
+template <int RNG>
+static void launch_sample_r(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t n,
+                            const uint64_t* us, const uint32_t* ui, uint64_t seed, uint64_t ctr, double* lat,
+                            int32_t* sidx, cudaStream_t s) {
+  int q, h;
+  sample_variant(RNG, &q, &h);
+  if (q == 1 && h) launch_sample_t<RNG, 1, true>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+  if (q == 1 && !h) launch_sample_t<RNG, 1, false>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+  if (q == 2 && h) launch_sample_t<RNG, 2, true>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+  if (q == 2 && !h) launch_sample_t<RNG, 2, false>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+  if (q == 4 && h) launch_sample_t<RNG, 4, true>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+  if (q == 4 && !h) launch_sample_t<RNG, 4, false>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+}
+
+static int launch_sample(emu_oracle_t o, int rng_mode, const int32_t* qt, const int32_t* qc, const uint8_t* qp,
+                         int64_t n, const uint64_t* us, const uint32_t* ui, uint64_t seed, uint64_t ctr, double* lat,
+                         int32_t* sidx, cudaStream_t s) {
+  if (rng_mode == EMU_RNG_EXPLICIT)
+    launch_sample_r<EMU_RNG_EXPLICIT>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+  else
+    launch_sample_r<EMU_RNG_PHILOX>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+  EMU_CUDA(cudaGetLastError());
+  return EMU_OK;
+}
+
 extern "C" {
 
 int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc, const uint8_t* q_phase, int64_t Q,
@@ -834,15 +992,10 @@ int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc
     const int64_t n = std::min(chunk, Q - done);
     int rc = build_missing(o, q_tt + done, q_conc + done, q_phase + done, n, s);
     if (rc) return rc;
-    const int grid = grid_for(n, kSampleThreads, kNumSMs * 16);
-    if (rng_mode == EMU_RNG_EXPLICIT)
-      EMU_LAUNCH("sample", s, k_sample<EMU_RNG_EXPLICIT><<<grid, kSampleThreads, 0, s>>>(
-          o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done, q_conc + done, q_phase + done, n,
-          u_sel + done, u_idx + done, seed, ctr_base + (uint64_t)done, out_lat + done, out_sidx + done, &o->ctl->flags));
-    else
-      EMU_LAUNCH("sample", s, k_sample<EMU_RNG_PHILOX><<<grid, kSampleThreads, 0, s>>>(
-          o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done, q_conc + done, q_phase + done, n,
-          nullptr, nullptr, seed, ctr_base + (uint64_t)done, out_lat + done, out_sidx + done, &o->ctl->flags));
+    rc = launch_sample(o, rng_mode, q_tt + done, q_conc + done, q_phase + done, n, u_sel ? u_sel + done : nullptr,
+                       u_idx ? u_idx + done : nullptr, seed, ctr_base + (uint64_t)done, out_lat + done,
+                       out_sidx + done, s);
+    if (rc) return rc;
     EMU_CUDA(cudaGetLastError());
     int flags = 0;
     if ((rc = read_flags(o, s, &flags))) return rc;
