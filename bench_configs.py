@@ -1,0 +1,260 @@
+#!/usr/bin/env python
+"""Secondary measurements for BASELINE.json configs 1, 3, 4, 5 (one JSON line each).
+
+The driver's headline is bench.py (config 2).  This script measures the
+other configs on one GPU so every SURVEY §8 row has a number:
+
+  c1  C1 pack (50k records) + the 10k-step reference-scheduler trace
+      (tests/golden/c1_trace.npz): PCG64 stream replay (bit-exact with the
+      reference LatencyOracle), batched Philox draws, and the per-step
+      LatencyOracle.__call__ latency.  CPU: the oracle port, same queries.
+  c3  sparse long-context profile (1M records, tt <= 131072), 10M queries,
+      M = 32 and M = 256, cold sweeps.
+  c4  offline table build from 100M synthetic records (device-resident
+      inputs), canonical order; records/s and the build's HBM bytes/s.
+  c5  what-if sweep: 512 scenarios (32 request rates x 16 burstiness
+      values) x 1M steps, keys generated on the GPU per scenario, Philox
+      draws; plus the synthetic token fill over 256M entries.
+
+    python bench_configs.py [c1 c3 c4 c5] [--steps K]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import torch  # noqa: E402
+
+import emu_oracle as O  # noqa: E402  (CPU baseline only)
+from paper_2605_00616_b200 import LatencyOracle, OracleConfig, _lib, token_fill  # noqa: E402
+from paper_2605_00616_b200.device import DeviceTables  # noqa: E402
+from paper_2605_00616_b200.profile import pack_from_device  # noqa: E402
+from paper_2605_00616_b200.workloads import (  # noqa: E402
+    explicit_uniforms,
+    queries_sparse,
+    records_llama,
+    records_sparse,
+)
+
+CORES = len(os.sched_getaffinity(0))
+
+
+def timed(fn, steps, warmup=2):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def oracle_for(rec, floor):
+    t = DeviceTables.build(*rec, canonical=True)
+    return t, LatencyOracle(pack_from_device(t, 1000, keep_host=False), OracleConfig(reliability_floor=floor),
+                            _validate=False)
+
+
+def c1(args):
+    tr = np.load(os.path.join(ROOT, "tests", "golden", "c1_trace.npz"))
+    qt, qc, qp = tr["tt"], tr["conc"], tr["phase"]
+    rec = records_llama(50_000, 0)
+    tables, orc = oracle_for(rec, 32)
+    golden = np.load(os.path.join(ROOT, "tests", "golden", "c1_golden.npz"))["lat_seq"]
+
+    def replay():
+        orc.flush()
+        orc.set_rng_state(np.random.default_rng(0).bit_generator.state)
+        return orc.sample_batch(qt, qc, qp, rng="pcg64")
+
+    lat, _ = replay()
+    exact = bool(np.array_equal(lat, golden))
+    ms_replay = timed(replay, args.steps)
+    dq = [torch.as_tensor(a, device="cuda") for a in (qt, qc, qp)]
+
+    def batched():
+        orc.flush()
+        orc.sample_batch(*dq, rng="philox", seed=1)
+
+    ms_batch = timed(batched, args.steps)
+    keys = list(zip(qt.tolist(), qc.tolist(), qp.tolist()))
+    for k in keys[:500]:
+        orc(*k)
+    us = []
+    for k in keys[500:3500]:
+        t0 = time.perf_counter()
+        orc(*k)
+        us.append((time.perf_counter() - t0) * 1e6)
+    us.sort()
+    tabs = O.build(*rec, canonical=True)
+    t0 = time.perf_counter()
+    O.sample_pcg64(tabs, qt, qc, qp, 32, state6=O.pcg64_state6(0))
+    cpu_s = time.perf_counter() - t0
+    return {"config": "c1", "workload": "50k-record pack, 10k reference-scheduler step keys (312 unique), M=32",
+            "pcg64_replay_ms": ms_replay, "pcg64_replay_queries_per_s": len(qt) / (ms_replay / 1e3),
+            "pcg64_bit_exact_vs_reference": exact, "batched_philox_ms": ms_batch,
+            "batched_queries_per_s": len(qt) / (ms_batch / 1e3), "p50_us_per_step_query": us[len(us) // 2],
+            "p99_us_per_step_query": us[int(0.99 * len(us))],
+            "cpu_baseline": {"value": len(qt) / cpu_s, "unit": "queries/s", "cores": 1, "kind": "port",
+                             "sample": "the same 10k trace, PCG64 stream, cold cache"}}
+
+
+def c3(args):
+    rec = records_sparse(1_000_000, 0)
+    Q = args.queries
+    qt, qc, qp = queries_sparse(Q, 1)
+    dq = [torch.as_tensor(a, device="cuda") for a in (qt, qc, qp)]
+    out = {"config": "c3", "workload": f"sparse long-context: 1M records (tt <= 131072), {Q} queries, cold sweep"}
+    tables = DeviceTables.build(*rec, canonical=True)
+    info = tables.info(1)
+    out["mixed_buckets"] = info["n_buckets"]
+    tabs = O.build(*rec, canonical=True)
+    for floor in (32, 256):
+        orc = LatencyOracle(pack_from_device(tables, 1000, keep_host=False), OracleConfig(reliability_floor=floor),
+                            _validate=False)
+
+        def sweep():
+            orc.flush()
+            orc.sample_batch(*dq, rng="philox", seed=1)
+
+        ms = timed(sweep, max(1, args.steps // 2), warmup=1)
+        _lib.profile_enable(True)
+        sweep()
+        kern = {k: round(_lib.profile_read(k)[0], 4) for k in ("mark", "pool_prep", "pool_warp", "pool_cta", "sample")}
+        _lib.profile_enable(False)
+        n = 2_000
+        t0 = time.perf_counter()
+        O.sample_batch(tabs, qt[:n], qc[:n], qp[:n], floor, mode="philox", seed=1, threads=CORES)
+        cpu = n / (time.perf_counter() - t0)
+        out[f"M{floor}"] = {"ms_per_sweep": ms, "queries_per_s": Q / (ms / 1e3), "kernels_ms": kern,
+                            "cpu_baseline": {"value": cpu, "unit": "queries/s", "cores": CORES, "kind": "port",
+                                             "sample": f"first {n} queries, cold cache per thread"}}
+        del orc
+    return out
+
+
+def c4(args):
+    n = args.records_c4
+    t0 = time.perf_counter()
+    parts = [records_llama(n // 10, 100 + k) for k in range(10)]
+    cols = [np.concatenate([p[i] for p in parts]) for i in range(4)]
+    gen_s = time.perf_counter() - t0
+    dev = [torch.as_tensor(c, device="cuda") for c in cols]
+
+    def build():
+        t = DeviceTables.build(*dev, canonical=True)
+        del t
+
+    ms = timed(build, max(1, args.steps // 3), warmup=1)
+    t = DeviceTables.build(*dev, canonical=True)
+    nb = sum(t.info(i)["n_buckets"] for i in range(3))
+    del t
+    algo_bytes = 33 * n + 48 * nb / 3
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    m = 2_000_000
+    t0 = time.perf_counter()
+    O.build(cols[0][:m], cols[1][:m], cols[2][:m], cols[3][:m], canonical=True)
+    cpu = m / (time.perf_counter() - t0)
+    return {"config": "c4", "workload": f"{n} synthetic records (generator G), canonical 3-table build",
+            "ms_per_build": ms, "records_per_s": n / (ms / 1e3), "buckets_total": nb,
+            "roofline": {"bound": "hbm", "achieved": algo_bytes / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": algo_bytes / (ms / 1e3) / 1e9 / peak,
+                         "bytes": "33 B/record + 48 B/bucket (SURVEY 8d); multi-pass sort moves more"},
+            "host_generation_s": gen_s,
+            "cpu_baseline": {"value": cpu, "unit": "records/s", "cores": 1, "kind": "port",
+                             "sample": f"oracle qsort build of the first {m} records"}}
+
+
+def scenario_keys(n, rate, gamma, gen):
+    """Synthetic step keys of one scenario (GPU): concurrency grows with the
+    request rate (Little's law with a ~3 s request lifetime) and its spread
+    with burstiness 1/gamma; 70 % decode steps."""
+    med = max(1.0, min(256.0, rate * 3.0))
+    sigma = 0.4 + 0.4 / math.sqrt(gamma)
+    conc = torch.clamp(torch.round(torch.exp(math.log(med) + sigma * torch.randn(n, device="cuda", generator=gen))),
+                       1, 256).to(torch.int32)
+    decode = torch.rand(n, device="cuda", generator=gen) < 0.7
+    chunk = torch.clamp(torch.round(torch.exp(math.log(180.0) + torch.randn(n, device="cuda", generator=gen))), 1,
+                        2048).to(torch.int32)
+    tt = torch.where(decode, conc, torch.clamp(conc - 1 + chunk, max=2048))
+    return tt, conc, (~decode).to(torch.uint8)
+
+
+def c5(args):
+    _, orc = oracle_for(records_llama(1_000_000, 0), 32)
+    rates = np.geomspace(1, 64, 32)
+    gammas = np.geomspace(0.125, 2, 16)
+    steps_per = args.steps_c5
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    lat = torch.empty(steps_per, dtype=torch.float64, device="cuda")
+    sidx = torch.empty(steps_per, dtype=torch.int32, device="cuda")
+    scen = [(r, g) for r in rates for g in gammas][: args.scenarios]
+    orc.flush()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = 0.0
+    for k, (r, g) in enumerate(scen):  # scenario keys are synthesised on the GPU outside the timed calls
+        tt, cc, ph = scenario_keys(steps_per, r, g, gen)
+        a.record()
+        orc.sample_batch(tt, cc, ph, rng="philox", seed=k, out_lat=lat, out_sidx=sidx)  # cache warm across scenarios
+        b.record()
+        b.synchronize()
+        ms += a.elapsed_time(b)
+    # token fill throughput (synthetic entries: 256M)
+    n = 256 << 20
+    g2 = torch.Generator(device="cuda")
+    g2.manual_seed(3)
+    pre = (torch.rand(n, device="cuda", generator=g2) < 0.1).to(torch.uint8)
+    plen = torch.randint(1, 2048, (n,), device="cuda", dtype=torch.int32, generator=g2)
+    prog = torch.remainder(torch.randint(0, 2048, (n,), device="cuda", dtype=torch.int32, generator=g2), plen)
+    chunk = torch.clamp(plen - prog, max=512).to(torch.int32)
+    gen_ = torch.randint(0, 512, (n,), device="cuda", dtype=torch.int32, generator=g2)
+    tgt = torch.randint(1, 512, (n,), device="cuda", dtype=torch.int32, generator=g2)
+    ids = torch.empty(n, dtype=torch.int32, device="cuda")
+    fin = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ms_fill = timed(lambda: token_fill(pre, chunk, prog, plen, gen_, tgt, out_ids=ids, out_finished=fin), 5)
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    fill_gbs = 26 * n / (ms_fill / 1e3) / 1e9
+    total_q = len(scen) * steps_per
+    return {"config": "c5", "workload": f"{len(scen)} scenarios x {steps_per} steps (rate x burstiness grid), "
+                                        "Philox draws, pool cache warm across scenarios",
+            "ms_total": ms, "queries_per_s": total_q / (ms / 1e3), "steps_total": total_q,
+            "token_fill": {"entries": n, "ms": ms_fill, "entries_per_s": n / (ms_fill / 1e3),
+                           "roofline": {"bound": "hbm", "achieved": fill_gbs, "peak": peak, "unit": "GB/s",
+                                        "frac": fill_gbs / peak, "bytes_per_entry": 26}}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["c1", "c3", "c4", "c5"])
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--queries", type=int, default=10_000_000)
+    ap.add_argument("--records-c4", type=int, default=100_000_000)
+    ap.add_argument("--scenarios", type=int, default=512)
+    ap.add_argument("--steps-c5", type=int, default=1_000_000)
+    args = ap.parse_args()
+    for c in args.configs:
+        res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5}[c](args)
+        print(json.dumps(res), flush=True)
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
