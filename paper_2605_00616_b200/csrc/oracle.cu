@@ -39,6 +39,10 @@ constexpr int kCtaThreads = 256;
 constexpr int kCtaCap = 8192;  // candidates in shared memory per CTA
 constexpr int kCtaSmem = kCtaCap * 12;
 constexpr int kCtaCache = 1024;  // cached counts/offsets per CTA workspace
+constexpr int kGrpThreads = 128;  // middle tier: one 4-warp group per key
+constexpr int kGrpCap = 2048;
+constexpr int kGrpSmem = kGrpCap * 12;
+constexpr int kGrpGrid = kNumSMs * 4;
 constexpr int kCtaGrid = kNumSMs;
 constexpr int kSampleThreads = 256;
 constexpr int kQPT = 4;  // queries per thread, interleaved for memory-level parallelism
@@ -50,7 +54,9 @@ struct BatchCtl {
   int esc_count;
   int esc_work;
   int flags;
-  int pad;
+  int esc2_count;  // keys too big for the 128-thread group tier -> CTA tier
+  int esc2_work;
+  int grp_pad;
 };
 
 struct Keys {
@@ -285,6 +291,36 @@ __global__ void __launch_bounds__(kWarpThreads, 7) k_pool_warp(DevTable P0, DevT
       int e = atomicAdd(esc_count, 1);
       esc_list[e] = (int)wk;
     }
+  }
+}
+
+// Middle tier: one 128-thread group (CTA) per key escalated by the warp tier
+// (windows of 257..2048 candidates, e.g. M = 256 on sparse tables); keys that
+// still overflow go on to the CTA tier.
+template <int MODE>
+__global__ void __launch_bounds__(kGrpThreads) k_pool_grp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
+                                                          int* work, const int* esc_list, const int* esc_count,
+                                                          int* esc2_list, int* esc2_count) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ long long scr[40];
+  __shared__ double dsh[10];
+  __shared__ int s_w;
+  __shared__ int32_t rows[3 * kGrpThreads];
+  __shared__ int32_t ncache[2 * kCtaCache];
+  PoolWS ws{(double*)smem, (int32_t*)(smem + kGrpCap * 8), kGrpCap, scr, dsh, rows, ncache, ncache + kCtaCache,
+            kCtaCache};
+  const int n = *esc_count;
+  for (;;) {
+    if (threadIdx.x == 0) s_w = atomicAdd(work, 1);
+    __syncthreads();
+    const int i = s_w;
+    __syncthreads();
+    if (i >= n) break;
+    const int w = esc_list[i];
+    const DevTable& T = keys.ph[w] ? P1 : P0;
+    const int64_t ent = keys.entry ? keys.entry[w] : 0;
+    const bool ok = process_key<kGrpThreads, MODE>(T, w, keys.tt[w], keys.conc[w], ent, cfg, ws, sk);
+    if (!ok && threadIdx.x == 0) esc2_list[atomicAdd(esc2_count, 1)] = w;
   }
 }
 
@@ -635,6 +671,8 @@ static int set_kernel_attrs() {
   if (g_attrs_set) return EMU_OK;
   EMU_CUDA(cudaFuncSetAttribute(k_pool_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpBytes * kWarpsPerCta));
   EMU_CUDA(cudaFuncSetAttribute(k_pool_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpBytes * kWarpsPerCta));
+  EMU_CUDA(cudaFuncSetAttribute(k_pool_grp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGrpSmem));
+  EMU_CUDA(cudaFuncSetAttribute(k_pool_grp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGrpSmem));
   EMU_CUDA(cudaFuncSetAttribute(k_pool_cta<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem));
   EMU_CUDA(cudaFuncSetAttribute(k_pool_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem));
   EMU_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem));
@@ -666,7 +704,9 @@ struct emu_oracle_s {
   uint8_t* nk_p = nullptr;
   int64_t* nk_e = nullptr;
   int* esc = nullptr;
+  int* esc2 = nullptr;
   int64_t chunk_cap = 0;
+  int64_t arena_max = 0;  // growth limit for the pool arena (slots)
   int64_t nk_cap = 0;  // allocated new-key capacity (lazy)
   KeyWin* kw = nullptr;
   long long* resv = nullptr;
@@ -765,6 +805,13 @@ int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, doubl
   o->map.dom_conc = (int32_t)dc;
   o->arena_cap = arena_slots > 0 ? arena_slots : (1LL << 26);
   if (o->arena_cap > 0x7fffffffLL) o->arena_cap = 0x7fffffffLL;
+  if (arena_slots > 0) {
+    o->arena_max = o->arena_cap;  // caller-fixed size: chunk instead of growing
+  } else {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    o->arena_max = std::max<int64_t>(o->arena_cap, std::min<int64_t>(0x7fffffffLL, (int64_t)(free_b / 4 / sizeof(Slot))));
+  }
   int64_t hcap = pow2_at_least(hash_slots > 0 ? hash_slots : (1LL << 16));
   o->chunk_cap = 1LL << 24;
   o->gcap = pow2_at_least(max_nb);
@@ -807,6 +854,7 @@ void emu_oracle_destroy(emu_oracle_t o) {
   cudaFree(o->nk_p);
   cudaFree(o->nk_e);
   cudaFree(o->esc);
+  cudaFree(o->esc2);
   cudaFree(o->kw);
   cudaFree(o->resv);
   cudaFree(o->cd);
@@ -847,6 +895,7 @@ static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
   cudaFree(o->nk_p);
   cudaFree(o->nk_e);
   cudaFree(o->esc);
+  cudaFree(o->esc2);
   cudaFree(o->kw);
   cudaFree(o->resv);
   cudaFree(o->cd);
@@ -863,7 +912,8 @@ static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
   o->nk_cap = 0;
   int rc;
   if ((rc = dalloc(&o->nk_tt, need)) || (rc = dalloc(&o->nk_c, need)) || (rc = dalloc(&o->nk_p, need)) ||
-      (rc = dalloc(&o->nk_e, need)) || (rc = dalloc(&o->esc, need)) || (rc = dalloc(&o->kw, need)) ||
+      (rc = dalloc(&o->nk_e, need)) || (rc = dalloc(&o->esc, need)) || (rc = dalloc(&o->esc2, need)) ||
+      (rc = dalloc(&o->kw, need)) ||
       (rc = dalloc(&o->resv, need)))
     return rc;
   o->nk_cap = need;
@@ -892,9 +942,14 @@ static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, c
   EMU_LAUNCH("pool_warp", s, k_pool_warp<0><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
                                  o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, &o->ctl->work, o->esc, &o->ctl->esc_count));
   EMU_CUDA(cudaGetLastError());
-  EMU_LAUNCH("pool_cta", s, k_pool_cta<0><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg,
+  EMU_LAUNCH("pool_grp", s, k_pool_grp<0><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg,
                                                                                   sk, &o->ctl->esc_work, o->esc,
-                                                                                  &o->ctl->esc_count, o->gd, o->gb,
+                                                                                  &o->ctl->esc_count, o->esc2,
+                                                                                  &o->ctl->esc2_count));
+  EMU_CUDA(cudaGetLastError());
+  EMU_LAUNCH("pool_cta", s, k_pool_cta<0><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg,
+                                                                                  sk, &o->ctl->esc2_work, o->esc2,
+                                                                                  &o->ctl->esc2_count, o->gd, o->gb,
                                                                                   o->gcap));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
@@ -913,6 +968,14 @@ static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s,
   *rc = EMU_OK;
   if (flags & FLAG_HASH) {
     if ((*rc = alloc_hash(o, o->map.hcap * 4))) return -1;
+  }
+  if ((flags & FLAG_ARENA) && o->arena_cap < o->arena_max) {  // grow the arena before resorting to chunking
+    cudaFree(o->arena);
+    o->arena = nullptr;
+    o->arena_cap = std::min(o->arena_max, o->arena_cap * 4);
+    if ((*rc = dalloc(&o->arena, o->arena_cap))) return -1;
+    if ((*rc = oracle_flush(o, s))) return -1;
+    return chunk;
   }
   if ((*rc = oracle_flush(o, s))) return -1;
   if (flags & FLAG_ARENA) {
@@ -1187,9 +1250,14 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
     EMU_LAUNCH("pool_warp", s, k_pool_warp<1><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
                                    o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, &o->ctl->work, o->esc, &o->ctl->esc_count));
     EMU_CUDA(cudaGetLastError());
-    EMU_LAUNCH("pool_cta", s, k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys,
+    EMU_LAUNCH("pool_grp", s, k_pool_grp<1><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(o->plane[0], o->plane[1], keys,
                                                                                     o->cfg, sk, &o->ctl->esc_work,
-                                                                                    o->esc, &o->ctl->esc_count, o->gd,
+                                                                                    o->esc, &o->ctl->esc_count, o->esc2,
+                                                                                    &o->ctl->esc2_count));
+    EMU_CUDA(cudaGetLastError());
+    EMU_LAUNCH("pool_cta", s, k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys,
+                                                                                    o->cfg, sk, &o->ctl->esc2_work,
+                                                                                    o->esc2, &o->ctl->esc2_count, o->gd,
                                                                                     o->gb, o->gcap));
     EMU_CUDA(cudaGetLastError());
     EMU_CUDA(cudaMemcpyAsync(hK.data(), xK, 8 * n, cudaMemcpyDeviceToHost, s));
