@@ -222,6 +222,16 @@ struct __align__(16) Slot {
   int32_t n;
 };
 
+// Pool layout in the arena (two-level inverse-CDF index):
+//   [header: the last cdf of every 8-slot group but the final one, as doubles,
+//    padded to whole slots][K slots]
+// A draw reads the header (binary search over ceil(K/8)-1 splits; one sector
+// for K <= 32), then the chosen group's <= 8 cdf values in parallel.
+constexpr int kGroupSlots = 8;
+__host__ __device__ __forceinline__ int64_t pool_groups(int64_t K) { return (K + kGroupSlots - 1) / kGroupSlots; }
+__host__ __device__ __forceinline__ int64_t pool_header_slots(int64_t K) { return pool_groups(K) / 2; }
+__host__ __device__ __forceinline__ int64_t pool_total_slots(int64_t K) { return K + pool_header_slots(K); }
+
 // Key-map entry: 0 empty, -1 claimed (being built), else (K << 32) | start.
 constexpr long long kEntryEmpty = 0;
 constexpr long long kEntryPending = -1;
@@ -238,6 +248,34 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x *= 0xc4ceb9fe1a85ec53ULL;
   x ^= x >> 33;
   return x;
+}
+
+// searchsorted(cdf, u, 'right') over the pool at arena[start] (K slots):
+// returns the chosen slot.  cdf[K-1] == 1.0 > u, so a hit always exists.
+__device__ __forceinline__ Slot pool_draw_slot(const Slot* __restrict__ arena, int64_t start, int64_t K, double u) {
+  const int64_t hs = pool_header_slots(K);
+  int64_t g = 0;
+  if (hs > 0) {
+    const double* sp = reinterpret_cast<const double*>(arena + start);
+    int64_t lo = 0, hi = pool_groups(K) - 1;  // number of splits <= u
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (sp[mid] <= u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    g = lo;
+  }
+  const Slot* P = arena + start + hs + g * kGroupSlots;
+  const int64_t n = min((int64_t)kGroupSlots, K - g * kGroupSlots);
+  double c[kGroupSlots];
+#pragma unroll
+  for (int q = 0; q < kGroupSlots; q++) c[q] = q < n ? P[q].cdf : 2.0;
+  int j = 0;
+#pragma unroll
+  for (int q = 0; q < kGroupSlots; q++) j += c[q] <= u ? 1 : 0;
+  return P[j];
 }
 
 // Oracle-side device state passed by value to kernels.

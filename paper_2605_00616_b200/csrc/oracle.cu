@@ -106,8 +106,9 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
     long long start = reserved;
     if (start == -1) {
       if (G::rank() == 0) {
-        unsigned long long st = atomicAdd(sk.arena_used, (unsigned long long)K);
-        long long s = (st + (unsigned long long)K <= (unsigned long long)sk.arena_cap) ? (long long)st : -2LL;
+        const unsigned long long tot = (unsigned long long)pool_total_slots(K);
+        unsigned long long st = atomicAdd(sk.arena_used, tot);
+        long long s = (st + tot <= (unsigned long long)sk.arena_cap) ? (long long)st : -2LL;
         if (s < 0) atomicOr(sk.flags, FLAG_ARENA);
         ws.scr[36] = s;
       }
@@ -117,13 +118,15 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
     }
     if (start < 0) return;
     EMU_PHASE_BEGIN();
-    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, sk.arena + start, nullptr, nullptr, nullptr, nullptr);
+    const int64_t hs = pool_header_slots(K);
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, sk.arena + start + hs,
+                    hs ? reinterpret_cast<double*>(sk.arena + start) : nullptr, nullptr, nullptr, nullptr, nullptr);
     // entries are consumed by a later kernel: stream order publishes them
     if (G::rank() == 0) *map_entry_ptr(sk.map, entry_idx) = make_entry(K, start);
     EMU_PHASE(6);
   } else {
     const int64_t base = w * sk.kmax;
-    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, nullptr, sk.x_bkt + base, sk.x_dist + base,
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, nullptr, nullptr, sk.x_bkt + base, sk.x_dist + base,
                     sk.x_prob + base, sk.x_cdf + base);
     if (G::rank() == 0) sk.x_K[w] = K;
   }
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Key
     if (!ready) k.flags = 0;
     long long r = -1;
     if (MODE == 0) {
-      const long long need = ready ? (k.cap < cfg.floor ? k.cap : cfg.floor) : 0;
+      const long long need = ready ? pool_total_slots(k.cap < cfg.floor ? k.cap : cfg.floor) : 0;
       const long long st = warp_alloc(sk.arena_used, need);
       if (ready) {
         r = (st + need <= sk.arena_cap) ? st : -2;
@@ -355,17 +358,6 @@ __global__ void __launch_bounds__(kCtaThreads) k_pool_cta(DevTable P0, DevTable 
   }
 }
 
-__device__ __forceinline__ int64_t upper_bound_cdf(const Slot* __restrict__ P, int64_t K, double u) {
-  int64_t lo = 0, hi = K;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (P[mid].cdf <= u)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
 
 // Lemire index for query qid after the first word w0 (EXPLICIT: hash32 chain;
 // PHILOX: the block-0 spare word, then blocks 1, 2, ... of Philox(qid)).
@@ -464,26 +456,11 @@ __global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 :
       lo[j] = 0;
       hi[j] = ok ? (int32_t)((unsigned long long)e[j] >> 32) : 0;
     }
-    // lockstep searchsorted(cdf, u, 'right') over the QPT pools
-    for (;;) {
-      bool any = false;
-#pragma unroll
-      for (int j = 0; j < QPT; j++) {
-        if (lo[j] < hi[j]) {
-          any = true;
-          const int32_t mid = (lo[j] + hi[j]) >> 1;
-          if (arena[start[j] + mid].cdf <= u[j])
-            lo[j] = mid + 1;
-          else
-            hi[j] = mid;
-        }
-      }
-      if (!any) break;
-    }
+    // two-level inverse-CDF lookup (header split, then one 8-slot group)
     Slot sl[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++)
-      if (v[j] && e[j] > 0) sl[j] = arena[start[j] + lo[j]];
+      if (v[j] && e[j] > 0) sl[j] = pool_draw_slot(arena, start[j], hi[j], u[j]);
     double lat[QPT];
     int32_t sidx[QPT];
 #pragma unroll
@@ -534,9 +511,9 @@ __device__ __forceinline__ void store_pcg(uint64_t* st6, const Pcg64& g) {
 
 // One draw of LatencyOracle.sample on the PCG64 stream: choice() draws one
 // double; integers(n) draws buffered u32 words only when n > 1.
-__device__ __forceinline__ int32_t pcg_draw(Pcg64& g, const Slot* P, int64_t K) {
+__device__ __forceinline__ int32_t pcg_draw(Pcg64& g, const Slot* arena, int64_t start, int64_t K) {
   const double u = unit_double(pcg64_next64(g));
-  const Slot s = P[upper_bound_cdf(P, K, u)];
+  const Slot s = pool_draw_slot(arena, start, K, u);
   uint32_t j = 0;
   if (s.n > 1) {
     uint32_t w0 = pcg64_next32(g);
@@ -561,7 +538,7 @@ __global__ void k_sample_pcg(MapView m, const Slot* __restrict__ arena, const do
     }
     const int64_t K = (int64_t)((unsigned long long)e >> 32);
     const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
-    const int32_t sidx = pcg_draw(g, arena + start, K);
+    const int32_t sidx = pcg_draw(g, arena, start, K);
     out_lat[i] = (ph ? s1 : s0)[sidx];
     out_sidx[i] = sidx;
   }
@@ -617,7 +594,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
     Pcg64 g = load_pcg(st6);
     const int64_t K = (int64_t)((unsigned long long)e >> 32);
     const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
-    const int32_t sidx = pcg_draw(g, sk.arena + start, K);
+    const int32_t sidx = pcg_draw(g, sk.arena, start, K);
     out->lat = T.samples[sidx];
     out->sidx = sidx;
     out->flags = 0;

@@ -850,7 +850,7 @@ __device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t 
 // Writes (optionally) bucket/dist/prob/cdf arrays and/or cache slots.
 template <int NT>
 __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, const PoolWS& ws_in,
-                            int64_t sorted_off, bool cached, Slot* slots,
+                            int64_t sorted_off, bool cached, Slot* slots, double* header,
                             int32_t* o_bkt, double* o_dist, double* o_prob, double* o_cdf) {
   using G = Grp<NT>;
   PoolWS ws = ws_in;
@@ -926,6 +926,7 @@ __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, 
         s.n = (int32_t)(T.bkt_off[bb + 1] - o0);
       }
       slots[j] = s;
+      if (header && (j % kGroupSlots) == kGroupSlots - 1 && j < K - 1) header[j / kGroupSlots] = cdf;
     }
   }
   G::sync();
