@@ -227,6 +227,9 @@ class LatencyOracle:
                                             _lib.stream_ptr(), ctypes.byref(h)))
         self._h = h
         self._host = host
+        self._step = _lib.lib().emu_oracle_step  # per-step hot path: no per-call lookups
+        self._step_out = ctypes.c_double()
+        self._step_out_ref = ctypes.byref(self._step_out)
         self.set_rng_state(np.random.default_rng(self.cfg.rng_seed).bit_generator.state)
 
     def _table_empty(self, i: int) -> bool:
@@ -259,10 +262,10 @@ class LatencyOracle:
     # -- reference surface ------------------------------------------------------------
     def sample(self, tt: int, conc: int, phase) -> float:
         """One draw on this oracle's stream (oracle.py:224-226)."""
-        out = ctypes.c_double()
-        _check(_lib.lib().emu_oracle_step(self._h, _i32(tt, "tt"), _i32(conc, "conc"), phase_code(phase),
-                                          ctypes.byref(out)))
-        return out.value
+        rc = self._step(self._h, _i32(tt, "tt"), _i32(conc, "conc"), phase_code(phase), self._step_out_ref)
+        if rc:
+            _check(rc)
+        return self._step_out.value
 
     __call__ = sample
 
