@@ -165,9 +165,12 @@ int emu_oracle_sample_pcg64(emu_oracle_t o, const int32_t* q_tt, const int32_t* 
                             const uint8_t* q_phase, int64_t Q, uint64_t* pcg_state,
                             double* out_lat, int32_t* out_sidx, void* stream);
 
-/* Convenience for host callers: same as emu_oracle_sample with HOST query and
- * result buffers (copies in, samples, copies out, synchronizes the stream).
- * This is the call the e2e measurement times. */
+/* Same as emu_oracle_sample with HOST query and result buffers: chunks of 1M
+ * queries are copied in on an internal stream, sampled on `stream` and copied
+ * out on a second internal stream, so the copies overlap the pool build and
+ * the draws (pinned buffers give full overlap).  Synchronizes before
+ * returning.  `out_sidx` may be NULL (latencies only).  This is the call the
+ * e2e measurement times. */
 int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc,
                            const uint8_t* q_phase, int64_t Q, int rng_mode, const uint64_t* u_sel,
                            const uint32_t* u_idx, uint64_t seed, uint64_t ctr_base,

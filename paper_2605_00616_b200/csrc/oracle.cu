@@ -48,6 +48,7 @@ constexpr int kGrpGrid = kNumSMs * 4;
 constexpr int kCtaGrid = kNumSMs;
 constexpr int kSampleThreads = 256;
 constexpr int kQPT = 4;  // queries per thread, interleaved for memory-level parallelism
+constexpr int64_t kHostChunk = 1 << 20;  // queries per pipelined chunk of emu_oracle_sample_host
 
 struct BatchCtl {
   unsigned long long cand_used;  // candidate scratch bump pointer
@@ -734,9 +735,16 @@ struct emu_oracle_s {
   StepOut* step_host = nullptr;  // pinned, mapped
   uint32_t step_seq = 0;
   int* flags_host = nullptr;
-  // host staging for emu_oracle_sample_host
+  // host staging for emu_oracle_sample_host (pipelined: copy-in stream,
+  // compute on the caller's stream, copy-out stream; one event pair per chunk)
   void* stage = nullptr;
   size_t stage_bytes = 0;
+  cudaStream_t cp_in = nullptr, cp_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_cmp;
+  cudaEvent_t ev_start = nullptr;
+  int* flag_log = nullptr;  // device: flags of each pipelined chunk
+  int* flag_log_host = nullptr;
+  int64_t flag_log_cap = 0;
 };
 
 static Sink make_sink(emu_oracle_t o) {
@@ -877,6 +885,13 @@ void emu_oracle_destroy(emu_oracle_t o) {
   cudaFree(o->gb);
   cudaFree(o->pcg);
   cudaFree(o->stage);
+  for (cudaEvent_t e : o->ev_in) cudaEventDestroy(e);
+  for (cudaEvent_t e : o->ev_cmp) cudaEventDestroy(e);
+  if (o->ev_start) cudaEventDestroy(o->ev_start);
+  if (o->cp_in) cudaStreamDestroy(o->cp_in);
+  if (o->cp_out) cudaStreamDestroy(o->cp_out);
+  cudaFree(o->flag_log);
+  if (o->flag_log_host) cudaFreeHost(o->flag_log_host);
   if (o->step_host) cudaFreeHost(o->step_host);
   if (o->flags_host) cudaFreeHost(o->flags_host);
   delete o;
@@ -1130,8 +1145,12 @@ int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q
                            double* out_lat, int32_t* out_sidx, void* stream) {
   if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
   if (Q <= 0) return Q == 0 ? EMU_OK : fail(EMU_ERR_INVALID, "negative query count");
-  cudaStream_t s = as_stream(stream);
+  if (!out_lat) return fail(EMU_ERR_INVALID, "NULL out_lat");
+  if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
+  if (rng_mode != EMU_RNG_EXPLICIT && rng_mode != EMU_RNG_PHILOX) return fail(EMU_ERR_INVALID, "unknown rng_mode");
   const bool ex = rng_mode == EMU_RNG_EXPLICIT;
+  if (ex && (!u_sel || !u_idx)) return fail(EMU_ERR_INVALID, "explicit mode needs u_sel/u_idx");
+  cudaStream_t s = as_stream(stream);
   size_t per = 4 + 4 + 1 + (ex ? 12 : 0) + 8 + 4;
   size_t need = per * (size_t)Q + 256;
   if (need > o->stage_bytes) {
@@ -1154,17 +1173,75 @@ int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q
   uint32_t* d_ui = ex ? (uint32_t*)carve(4 * Q) : nullptr;
   int32_t* d_si = (int32_t*)carve(4 * Q);
   uint8_t* d_qp = (uint8_t*)carve(Q);
-  EMU_CUDA(cudaMemcpyAsync(d_qt, q_tt, 4 * Q, cudaMemcpyDefault, s));
-  EMU_CUDA(cudaMemcpyAsync(d_qc, q_conc, 4 * Q, cudaMemcpyDefault, s));
-  EMU_CUDA(cudaMemcpyAsync(d_qp, q_phase, Q, cudaMemcpyDefault, s));
-  if (ex) {
-    EMU_CUDA(cudaMemcpyAsync(d_us, u_sel, 8 * Q, cudaMemcpyDefault, s));
-    EMU_CUDA(cudaMemcpyAsync(d_ui, u_idx, 4 * Q, cudaMemcpyDefault, s));
+  // Pipeline: chunk i's copy-in (cp_in) overlaps chunk i-1's pool build +
+  // draws (s) and chunk i-2's copy-out (cp_out).  Draws are pure functions of
+  // (query, uniforms / counter, pool), so chunking never changes a result.
+  // Staging covers all Q queries: no buffer is reused within a call.
+  const int64_t chunk = std::min<int64_t>(std::max<int64_t>(o->chunk_cap, 1), kHostChunk);
+  const int64_t nch = (Q + chunk - 1) / chunk;
+  if (!o->cp_in) {
+    EMU_CUDA(cudaStreamCreateWithFlags(&o->cp_in, cudaStreamNonBlocking));
+    EMU_CUDA(cudaStreamCreateWithFlags(&o->cp_out, cudaStreamNonBlocking));
+    EMU_CUDA(cudaEventCreateWithFlags(&o->ev_start, cudaEventDisableTiming));
   }
-  int rc = emu_oracle_sample(o, d_qt, d_qc, d_qp, Q, rng_mode, d_us, d_ui, seed, ctr_base, d_lat, d_si, stream);
+  while ((int64_t)o->ev_in.size() < nch) {
+    cudaEvent_t a, b;
+    EMU_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    EMU_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    o->ev_in.push_back(a);
+    o->ev_cmp.push_back(b);
+  }
+  if (nch > o->flag_log_cap) {
+    cudaFree(o->flag_log);
+    if (o->flag_log_host) cudaFreeHost(o->flag_log_host);
+    o->flag_log = nullptr;
+    o->flag_log_host = nullptr;
+    o->flag_log_cap = 0;
+    EMU_CUDA(cudaMalloc(&o->flag_log, sizeof(int) * nch));
+    EMU_CUDA(cudaHostAlloc((void**)&o->flag_log_host, sizeof(int) * nch, cudaHostAllocDefault));
+    o->flag_log_cap = nch;
+  }
+  EMU_CUDA(cudaEventRecord(o->ev_start, s));  // earlier work on s may still use the staging
+  EMU_CUDA(cudaStreamWaitEvent(o->cp_in, o->ev_start, 0));
+  for (int64_t i = 0; i < nch; i++) {
+    const int64_t a = i * chunk, n = std::min(chunk, Q - a);
+    EMU_CUDA(cudaMemcpyAsync(d_qt + a, q_tt + a, 4 * n, cudaMemcpyDefault, o->cp_in));
+    EMU_CUDA(cudaMemcpyAsync(d_qc + a, q_conc + a, 4 * n, cudaMemcpyDefault, o->cp_in));
+    EMU_CUDA(cudaMemcpyAsync(d_qp + a, q_phase + a, n, cudaMemcpyDefault, o->cp_in));
+    if (ex) {
+      EMU_CUDA(cudaMemcpyAsync(d_us + a, u_sel + a, 8 * n, cudaMemcpyDefault, o->cp_in));
+      EMU_CUDA(cudaMemcpyAsync(d_ui + a, u_idx + a, 4 * n, cudaMemcpyDefault, o->cp_in));
+    }
+    EMU_CUDA(cudaEventRecord(o->ev_in[i], o->cp_in));
+    EMU_CUDA(cudaStreamWaitEvent(s, o->ev_in[i], 0));
+    int rc = build_missing(o, d_qt + a, d_qc + a, d_qp + a, n, s);
+    if (rc) return rc;
+    rc = launch_sample(o, rng_mode, d_qt + a, d_qc + a, d_qp + a, n, ex ? d_us + a : nullptr, ex ? d_ui + a : nullptr,
+                       seed, ctr_base + (uint64_t)a, d_lat + a, d_si + a, s);
+    if (rc) return rc;
+    EMU_CUDA(cudaMemcpyAsync(o->flag_log + i, &o->ctl->flags, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    EMU_CUDA(cudaEventRecord(o->ev_cmp[i], s));
+    EMU_CUDA(cudaStreamWaitEvent(o->cp_out, o->ev_cmp[i], 0));
+    EMU_CUDA(cudaMemcpyAsync(out_lat + a, d_lat + a, 8 * n, cudaMemcpyDefault, o->cp_out));
+    if (out_sidx) EMU_CUDA(cudaMemcpyAsync(out_sidx + a, d_si + a, 4 * n, cudaMemcpyDefault, o->cp_out));
+  }
+  EMU_CUDA(cudaMemcpyAsync(o->flag_log_host, o->flag_log, sizeof(int) * nch, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  EMU_CUDA(cudaStreamSynchronize(o->cp_out));
+  int64_t bad = -1;
+  for (int64_t i = 0; i < nch && bad < 0; i++)
+    if (o->flag_log_host[i]) bad = i;
+  if (bad < 0) return EMU_OK;
+  // A chunk overflowed the arena / hash: redo it and everything after it with
+  // the serial path (flush + retry with smaller chunks); inputs are resident.
+  const int64_t a = bad * chunk, n = Q - a;
+  int rc = oracle_flush(o, s);  // drop entries left claimed by the failed chunk
   if (rc) return rc;
-  EMU_CUDA(cudaMemcpyAsync(out_lat, d_lat, 8 * Q, cudaMemcpyDefault, s));
-  if (out_sidx) EMU_CUDA(cudaMemcpyAsync(out_sidx, d_si, 4 * Q, cudaMemcpyDefault, s));
+  rc = emu_oracle_sample(o, d_qt + a, d_qc + a, d_qp + a, n, rng_mode, ex ? d_us + a : nullptr,
+                             ex ? d_ui + a : nullptr, seed, ctr_base + (uint64_t)a, d_lat + a, d_si + a, stream);
+  if (rc) return rc;
+  EMU_CUDA(cudaMemcpyAsync(out_lat + a, d_lat + a, 8 * n, cudaMemcpyDefault, s));
+  if (out_sidx) EMU_CUDA(cudaMemcpyAsync(out_sidx + a, d_si + a, 4 * n, cudaMemcpyDefault, s));
   EMU_CUDA(cudaStreamSynchronize(s));
   return EMU_OK;
 }

@@ -320,8 +320,9 @@ class LatencyOracle:
         rng="pcg64"   : continues this oracle's numpy PCG64 stream -- identical to
                         calling sample() Q times in order.
         Inputs may be CUDA tensors (results stay on the device: (lat f64, sidx i32)
-        tensors) or host arrays (results come back as numpy arrays).  sidx indexes the
-        samples of the table each query resolved to.
+        tensors) or host arrays (results come back as numpy arrays; copies are
+        pipelined with the device work; out_sidx=False skips the index copy-out and
+        returns sidx=None).  sidx indexes the samples of the table each query resolved to.
         """
         torch = _lib.require_cuda()
         on_dev = hasattr(tt, "is_cuda") and tt.is_cuda
@@ -353,7 +354,10 @@ class LatencyOracle:
         us = np.ascontiguousarray(u_sel, dtype=np.uint64) if u_sel is not None else None
         ui = np.ascontiguousarray(u_idx, dtype=np.uint32) if u_idx is not None else None
         lat = np.empty(Q, dtype=np.float64) if out_lat is None else out_lat
-        sidx = np.empty(Q, dtype=np.int32) if out_sidx is None else out_sidx
+        if out_sidx is False:  # latencies only: no index copy-out
+            sidx = None
+        else:
+            sidx = np.empty(Q, dtype=np.int32) if out_sidx is None else out_sidx
         _check(_lib.lib().emu_oracle_sample_host(self._h, _lib.ptr(qt), _lib.ptr(qc), _lib.ptr(qp), Q, mode,
                                                  _lib.ptr(us), _lib.ptr(ui), seed & (2**64 - 1), int(ctr_base),
                                                  _lib.ptr(lat), _lib.ptr(sidx), _lib.stream_ptr()))

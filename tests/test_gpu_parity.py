@@ -146,7 +146,7 @@ def test_pools_match_oracle_random_keys(c1_pack, floor, power):
         np.testing.assert_allclose(got[4], want[4], rtol=1e-6, atol=0)
 
 
-def test_sparse_long_context_pools(tmp_path):
+def test_sparse_long_context_pools():
     rec = records_sparse(200_000, 0)
     pack = build_pack_arrays(*rec, num_gpu_blocks=1000, canonical=True)
     tabs = to_oracle_tables(pack)
@@ -247,6 +247,44 @@ def test_full_scale_properties(c1_pack):
                                    mode="philox", seed=1, ctr_base=k0, threads=8)
     assert np.array_equal(s[k0:k0 + 20_000], sidx_o)
     assert np.array_equal(lt[k0:k0 + 20_000], lat_o)
+
+
+@pytest.mark.parametrize("arena", [0, 1 << 20])
+def test_pipelined_host_path_matches_device_path(c1_pack, arena):
+    """emu_oracle_sample_host (1M-query chunks on three streams) returns exactly
+    what the device-resident call returns; a small arena makes a middle chunk
+    overflow, which is redone by the serial flush-and-retry path."""
+    Q = 2_600_000
+    qt, qc, qp = queries_llama(Q, 5)
+    us, ui = explicit_uniforms(Q, 6)
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32), arena_slots=arena)
+    lat_h, sidx_h = orc.sample_batch(qt, qc, qp, rng="explicit", u_sel=us, u_idx=ui)
+    lat_l, none = orc.sample_batch(qt, qc, qp, rng="explicit", u_sel=us, u_idx=ui, out_sidx=False)
+    assert none is None
+    orc.flush()
+    lat_d, sidx_d = orc.sample_batch(dev(qt), dev(qc), dev(qp), rng="explicit", u_sel=dev(us.view(np.int64)),
+                                     u_idx=dev(ui.view(np.int32)))
+    assert np.array_equal(sidx_h, sidx_d.cpu().numpy())
+    assert np.array_equal(lat_h, lat_d.cpu().numpy())
+    assert np.array_equal(lat_l, lat_h)
+    k0 = 2_000_000  # inside the third chunk
+    tabs = to_oracle_tables(c1_pack)
+    lat_o, sidx_o = O.sample_batch(tabs, qt[k0:k0 + 20_000], qc[k0:k0 + 20_000], qp[k0:k0 + 20_000], 32,
+                                   mode="explicit", u_sel=us[k0:k0 + 20_000], u_idx=ui[k0:k0 + 20_000], threads=8)
+    assert np.array_equal(sidx_h[k0:k0 + 20_000], sidx_o)
+    assert np.array_equal(lat_h[k0:k0 + 20_000], lat_o)
+
+
+def test_config2_pools_match_oracle():
+    """Pools of 3,000 config-2 keys (1M-record table) vs the oracle."""
+    pack = build_pack_arrays(*records_llama(1_000_000, 0), num_gpu_blocks=1000, canonical=True)
+    tabs = to_oracle_tables(pack)
+    qt, qc, qp = queries_llama(3_000, 9)
+    orc = LatencyOracle(pack, OracleConfig(reliability_floor=32))
+    got = orc.pools(qt, qc, qp)
+    want = O.pools(tabs, qt, qc, qp, 32)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
 
 
 def test_small_arena_forces_flush_and_retry(c1_pack):

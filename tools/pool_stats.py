@@ -18,6 +18,7 @@ orc.flush(); orc.sample_batch(qt, qc, qp, rng="philox"); torch.cuda.synchronize(
 lib.emu_stats_read(buf.ctypes.data)
 keys = int(buf[11])
 names = ["radius", "refine", "window", "enumerate", "sort", "prefix", "finish"]
+print("exact-resort", int(buf[12]), "wide->slow", int(buf[13]))
 print("keys", keys, "avg C_sat %.1f  avg pos %.1f  avg K %.1f" % (buf[8] / keys, buf[9] / keys, buf[10] / keys))
 tot = sum(int(buf[i]) for i in range(7))
 for i, n in enumerate(names):
