@@ -214,29 +214,69 @@ __device__ __forceinline__ uint32_t lemire_index(uint32_t n, uint32_t first_word
 }
 
 // ---------------------------------------------------------------- pool slots
-// One cached pool slot (16 B): inverse-CDF value, the bucket's first sample
-// and its sample count.  A pool is K consecutive slots.
+// The pool arena is allocated in 16-byte units; pools start on even units
+// (32 B, one L2 sector).
 struct __align__(16) Slot {
   double cdf;
   int32_t soff;
   int32_t n;
 };
 
-// Pool layout in the arena (two-level inverse-CDF index):
-//   [header: the last cdf of every 8-slot group but the final one, as doubles,
-//    padded to whole slots][K slots]
-// A draw reads the header (binary search over ceil(K/8)-1 splits; one sector
-// for K <= 32), then the chosen group's <= 8 cdf values in parallel.
+// A drawn bucket: its first sample and sample count.
+struct PoolPick {
+  int32_t soff;
+  int32_t n;
+};
+
+// Pool layout in the arena (two-level inverse-CDF index), for K buckets in
+// G = ceil(K/8) groups of 8:
+//   [header: G-1 split cdfs (the last cdf of every group but the final one),
+//    padded to an even unit count]
+//   [cdf: K doubles -- each 8-bucket group is 64 B on a sector boundary]
+//   [data: K x {int32 first sample, int32 count}]
+// A draw reads the header (<= 3 splits for K <= 32: one 32-B sector), the
+// chosen group's cdfs with <= 4 16-byte loads, then one 8-byte data word:
+// 5-6 load instructions per query instead of one per cdf.
 constexpr int kGroupSlots = 8;
 __host__ __device__ __forceinline__ int64_t pool_groups(int64_t K) { return (K + kGroupSlots - 1) / kGroupSlots; }
-__host__ __device__ __forceinline__ int64_t pool_header_slots(int64_t K) { return pool_groups(K) / 2; }
-__host__ __device__ __forceinline__ int64_t pool_total_slots(int64_t K) { return K + pool_header_slots(K); }
+__host__ __device__ __forceinline__ int64_t pool_header_slots(int64_t K) {
+  const int64_t h = pool_groups(K) / 2;  // ceil((G - 1) / 2) units
+  return (h + 1) & ~(int64_t)1;
+}
+__host__ __device__ __forceinline__ int64_t pool_cdf_units(int64_t K) { return (K + 1) / 2; }
+__host__ __device__ __forceinline__ int64_t pool_total_slots(int64_t K) {
+  return (pool_header_slots(K) + 2 * pool_cdf_units(K) + 1) & ~(int64_t)1;
+}
 
-// Key-map entry: 0 empty, -1 claimed (being built), else (K << 32) | start.
+// Arena pointers of a pool at unit `start`.
+struct PoolPtrs {
+  double* header;  // nullptr when G == 1
+  double* cdf;
+  int2* data;
+};
+__device__ __forceinline__ PoolPtrs pool_ptrs(Slot* arena, int64_t start, int64_t K) {
+  const int64_t hs = pool_header_slots(K);
+  PoolPtrs p;
+  p.header = hs ? reinterpret_cast<double*>(arena + start) : nullptr;
+  p.cdf = reinterpret_cast<double*>(arena + start + hs);
+  p.data = reinterpret_cast<int2*>(arena + start + hs + pool_cdf_units(K));
+  return p;
+}
+
+// Key-map entry: 0 empty, -1 claimed (being built); a built pool is either
+//   (K << 32) | start                        K >= 2 buckets at arena unit start
+//   kEntryDirect | soff << 31 | n            K == 1: the bucket itself, no arena
+// (bit 62 tags a direct entry; K < 2^30, soff, n < 2^31).  Single-bucket pools
+// (e.g. every decode key whose own bucket holds >= floor samples) then draw
+// with map entry -> sample: two dependent loads instead of four.
 constexpr long long kEntryEmpty = 0;
 constexpr long long kEntryPending = -1;
+constexpr unsigned long long kEntryDirect = 1ULL << 62;
 __device__ __forceinline__ long long make_entry(int64_t K, int64_t start) {
   return (long long)(((uint64_t)K << 32) | (uint64_t)start);
+}
+__device__ __forceinline__ long long make_entry_direct(int64_t soff, int64_t n) {
+  return (long long)(kEntryDirect | ((uint64_t)soff << 31) | (uint64_t)n);
 }
 
 constexpr unsigned long long kHashEmpty = 0x8000000080000000ULL;
@@ -250,32 +290,59 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
-// searchsorted(cdf, u, 'right') over the pool at arena[start] (K slots):
-// returns the chosen slot.  cdf[K-1] == 1.0 > u, so a hit always exists.
-__device__ __forceinline__ Slot pool_draw_slot(const Slot* __restrict__ arena, int64_t start, int64_t K, double u) {
-  const int64_t hs = pool_header_slots(K);
-  int64_t g = 0;
-  if (hs > 0) {
-    const double* sp = reinterpret_cast<const double*>(arena + start);
-    int64_t lo = 0, hi = pool_groups(K) - 1;  // number of splits <= u
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (sp[mid] <= u)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    g = lo;
+__device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ arena, int64_t start, int64_t K, double u);
+
+// The bucket a draw u selects from a built entry e (> 0).
+__device__ __forceinline__ PoolPick pool_pick(const Slot* __restrict__ arena, long long e, double u) {
+  const unsigned long long v = (unsigned long long)e;
+  if (v & kEntryDirect) {
+    PoolPick pk;
+    pk.soff = (int32_t)((v >> 31) & 0x7fffffffULL);
+    pk.n = (int32_t)(v & 0x7fffffffULL);
+    return pk;
   }
-  const Slot* P = arena + start + hs + g * kGroupSlots;
-  const int64_t n = min((int64_t)kGroupSlots, K - g * kGroupSlots);
-  double c[kGroupSlots];
-#pragma unroll
-  for (int q = 0; q < kGroupSlots; q++) c[q] = q < n ? P[q].cdf : 2.0;
+  return pool_draw_slot(arena, (int64_t)(v & 0xffffffffULL), (int64_t)(v >> 32), u);
+}
+
+// searchsorted(cdf, u, 'right') over the pool at arena[start] (K buckets):
+// returns the chosen bucket.  cdf[K-1] == 1.0 > u, so a hit always exists.
+__device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ arena, int64_t start, int64_t K, double u) {
+  const int64_t hs = pool_header_slots(K);
+  const int64_t G = pool_groups(K);
+  int64_t g = 0;
+  if (G > 1) {
+    const double* sp = reinterpret_cast<const double*>(arena + start);
+    if (G <= 5) {  // <= 4 splits: two 16-byte loads, count splits <= u
+      const double2 a = *reinterpret_cast<const double2*>(sp);
+      const double2 b = G > 3 ? reinterpret_cast<const double2*>(sp)[1] : make_double2(2.0, 2.0);
+      g = (a.x <= u) + (G > 2 && a.y <= u) + (G > 3 && b.x <= u) + (G > 4 && b.y <= u);
+    } else {
+      int64_t lo = 0, hi = G - 1;  // number of splits <= u
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (sp[mid] <= u)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      g = lo;
+    }
+  }
+  const double2* C = reinterpret_cast<const double2*>(arena + start + hs) + g * (kGroupSlots / 2);
+  const int n = (int)min((int64_t)kGroupSlots, K - g * kGroupSlots);
   int j = 0;
 #pragma unroll
-  for (int q = 0; q < kGroupSlots; q++) j += c[q] <= u ? 1 : 0;
-  return P[j];
+  for (int q = 0; q < kGroupSlots / 2; q++) {
+    if (2 * q < n) {
+      const double2 c = C[q];
+      j += (c.x <= u) + (2 * q + 1 < n && c.y <= u);
+    }
+  }
+  const int2 d = reinterpret_cast<const int2*>(arena + start + hs + pool_cdf_units(K))[g * kGroupSlots + j];
+  PoolPick pk;
+  pk.soff = d.x;
+  pk.n = d.y;
+  return pk;
 }
 
 // Oracle-side device state passed by value to kernels.

@@ -119,6 +119,15 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
                           long long reserved, const Cfg& cfg, const PoolWS& ws, const Sink& sk) {
   using G = Grp<NT>;
   if (MODE == 0) {
+    if (K == 1 && reserved != -2) {  // direct entry: the bucket itself (cdf == [1.0]), no arena slots
+      if (G::rank() == 0) {
+        const int32_t bb = ws.b[soff];
+        const int64_t o0 = T.bkt_off[bb];
+        *map_entry_ptr(sk.map, entry_idx) = make_entry_direct(o0, T.bkt_off[bb + 1] - o0);
+      }
+      G::sync();
+      return;
+    }
     long long start = reserved;
     if (start == -1) {
       if (G::rank() == 0) {
@@ -134,15 +143,14 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
     }
     if (start < 0) return;
     EMU_PHASE_BEGIN();
-    const int64_t hs = pool_header_slots(K);
-    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, sk.arena + start + hs,
-                    hs ? reinterpret_cast<double*>(sk.arena + start) : nullptr, nullptr, nullptr, nullptr, nullptr);
+    const PoolPtrs pp = pool_ptrs(sk.arena, start, K);
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, &pp, nullptr, nullptr, nullptr, nullptr);
     // entries are consumed by a later kernel: stream order publishes them
     if (G::rank() == 0) *map_entry_ptr(sk.map, entry_idx) = make_entry(K, start);
     EMU_PHASE(6);
   } else {
     const int64_t base = w * sk.kmax;
-    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, nullptr, nullptr, sk.x_bkt + base, sk.x_dist + base,
+    pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, nullptr, sk.x_bkt + base, sk.x_dist + base,
                     sk.x_prob + base, sk.x_cdf + base);
     if (G::rank() == 0) sk.x_K[w] = K;
   }
@@ -452,7 +460,6 @@ __global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 :
     uint64_t us[QPT];
     uint32_t w0[QPT];
     uint4 px[QPT];
-    int32_t lo[QPT], hi[QPT], start[QPT];
     double u[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
@@ -467,16 +474,12 @@ __global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 :
         w0[j] = px[j].z;
       }
       u[j] = unit_double(us[j]);
-      const bool ok = v[j] && e[j] > 0;
-      start[j] = ok ? (int32_t)((unsigned long long)e[j] & 0xffffffffULL) : 0;
-      lo[j] = 0;
-      hi[j] = ok ? (int32_t)((unsigned long long)e[j] >> 32) : 0;
     }
     // two-level inverse-CDF lookup (header split, then one 8-slot group)
-    Slot sl[QPT];
+    PoolPick sl[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++)
-      if (v[j] && e[j] > 0) sl[j] = pool_draw_slot(arena, start[j], hi[j], u[j]);
+      if (v[j] && e[j] > 0) sl[j] = pool_pick(arena, e[j], u[j]);
     double lat[QPT];
     int32_t sidx[QPT];
 #pragma unroll
@@ -527,9 +530,9 @@ __device__ __forceinline__ void store_pcg(uint64_t* st6, const Pcg64& g) {
 
 // One draw of LatencyOracle.sample on the PCG64 stream: choice() draws one
 // double; integers(n) draws buffered u32 words only when n > 1.
-__device__ __forceinline__ int32_t pcg_draw(Pcg64& g, const Slot* arena, int64_t start, int64_t K) {
+__device__ __forceinline__ int32_t pcg_draw(Pcg64& g, const Slot* arena, long long e) {
   const double u = unit_double(pcg64_next64(g));
-  const Slot s = pool_draw_slot(arena, start, K, u);
+  const PoolPick s = pool_pick(arena, e, u);
   uint32_t j = 0;
   if (s.n > 1) {
     uint32_t w0 = pcg64_next32(g);
@@ -552,9 +555,7 @@ __global__ void k_sample_pcg(MapView m, const Slot* __restrict__ arena, const do
       atomicOr(flags, FLAG_MISSING);
       return;  // stream state left untouched: the host retries the whole batch
     }
-    const int64_t K = (int64_t)((unsigned long long)e >> 32);
-    const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
-    const int32_t sidx = pcg_draw(g, arena, start, K);
+    const int32_t sidx = pcg_draw(g, arena, e);
     out_lat[i] = (ph ? s1 : s0)[sidx];
     out_sidx[i] = sidx;
   }
@@ -608,9 +609,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
       return;
     }
     Pcg64 g = load_pcg(st6);
-    const int64_t K = (int64_t)((unsigned long long)e >> 32);
-    const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
-    const int32_t sidx = pcg_draw(g, sk.arena, start, K);
+    const int32_t sidx = pcg_draw(g, sk.arena, e);
     store_pcg(st6, g);
     publish_step(out, T.samples[sidx], sidx, 0, seq);
   }
@@ -630,9 +629,7 @@ __global__ void k_step_hit(MapView m, const Slot* __restrict__ arena, const doub
     return;
   }
   Pcg64 g = load_pcg(st6);
-  const int64_t K = (int64_t)((unsigned long long)e >> 32);
-  const int64_t start = (int64_t)((unsigned long long)e & 0xffffffffULL);
-  const int32_t sidx = pcg_draw(g, arena, start, K);
+  const int32_t sidx = pcg_draw(g, arena, e);
   store_pcg(st6, g);
   publish_step(out, (ph ? s1 : s0)[sidx], sidx, 0, seq);
 }

@@ -850,7 +850,7 @@ __device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t 
 // Writes (optionally) bucket/dist/prob/cdf arrays and/or cache slots.
 template <int NT>
 __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, const PoolWS& ws_in,
-                            int64_t sorted_off, bool cached, Slot* slots, double* header,
+                            int64_t sorted_off, bool cached, const PoolPtrs* slots,
                             int32_t* o_bkt, double* o_dist, double* o_prob, double* o_cdf) {
   using G = Grp<NT>;
   PoolWS ws = ws_in;
@@ -914,19 +914,19 @@ __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, 
     double cdf = __ddiv_rn(ws.d[j], last);
     if (o_cdf) o_cdf[j] = cdf;
     if (slots) {
-      Slot s;
-      s.cdf = cdf;
+      int2 dv;
       if (use_cache) {
-        s.soff = ws.o[j];
-        s.n = ws.n[j];
+        dv.x = ws.o[j];
+        dv.y = ws.n[j];
       } else {
         const int32_t bb = ws.b[j];
         const int64_t o0 = T.bkt_off[bb];
-        s.soff = (int32_t)o0;
-        s.n = (int32_t)(T.bkt_off[bb + 1] - o0);
+        dv.x = (int32_t)o0;
+        dv.y = (int32_t)(T.bkt_off[bb + 1] - o0);
       }
-      slots[j] = s;
-      if (header && (j % kGroupSlots) == kGroupSlots - 1 && j < K - 1) header[j / kGroupSlots] = cdf;
+      slots->cdf[j] = cdf;
+      slots->data[j] = dv;
+      if (slots->header && (j % kGroupSlots) == kGroupSlots - 1 && j < K - 1) slots->header[j / kGroupSlots] = cdf;
     }
   }
   G::sync();
