@@ -306,20 +306,24 @@ __device__ __forceinline__ PoolPick pool_pick(const Slot* __restrict__ arena, lo
 
 // searchsorted(cdf, u, 'right') over the pool at arena[start] (K buckets):
 // returns the chosen bucket.  cdf[K-1] == 1.0 > u, so a hit always exists.
-__device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ arena, int64_t start, int64_t K, double u) {
-  const int64_t hs = pool_header_slots(K);
-  const int64_t G = pool_groups(K);
-  int64_t g = 0;
+// 32-bit offset arithmetic (K, start < 2^31 units).
+__device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ arena, int64_t start64, int64_t K64,
+                                                   double u) {
+  const int32_t K = (int32_t)K64;
+  const Slot* P = arena + start64;
+  const int32_t G = (K + kGroupSlots - 1) >> 3;
+  const int32_t hs = ((G >> 1) + 1) & ~1;
+  int32_t g = 0;
   if (G > 1) {
-    const double* sp = reinterpret_cast<const double*>(arena + start);
+    const double* sp = reinterpret_cast<const double*>(P);
     if (G <= 5) {  // <= 4 splits: two 16-byte loads, count splits <= u
       const double2 a = *reinterpret_cast<const double2*>(sp);
       const double2 b = G > 3 ? reinterpret_cast<const double2*>(sp)[1] : make_double2(2.0, 2.0);
-      g = (a.x <= u) + (G > 2 && a.y <= u) + (G > 3 && b.x <= u) + (G > 4 && b.y <= u);
+      g = (a.x <= u) + (G > 2 && a.y <= u) + (b.x <= u) + (G > 4 && b.y <= u);
     } else {
-      int64_t lo = 0, hi = G - 1;  // number of splits <= u
+      int32_t lo = 0, hi = G - 1;  // number of splits <= u
       while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
+        const int32_t mid = (lo + hi) >> 1;
         if (sp[mid] <= u)
           lo = mid + 1;
         else
@@ -328,9 +332,9 @@ __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ aren
       g = lo;
     }
   }
-  const double2* C = reinterpret_cast<const double2*>(arena + start + hs) + g * (kGroupSlots / 2);
-  const int n = (int)min((int64_t)kGroupSlots, K - g * kGroupSlots);
-  int j = 0;
+  const double2* C = reinterpret_cast<const double2*>(P + hs) + g * (kGroupSlots / 2);
+  const int32_t n = min(kGroupSlots, K - g * kGroupSlots);
+  int32_t j = 0;
 #pragma unroll
   for (int q = 0; q < kGroupSlots / 2; q++) {
     if (2 * q < n) {
@@ -338,7 +342,7 @@ __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ aren
       j += (c.x <= u) + (2 * q + 1 < n && c.y <= u);
     }
   }
-  const int2 d = reinterpret_cast<const int2*>(arena + start + hs + pool_cdf_units(K))[g * kGroupSlots + j];
+  const int2 d = reinterpret_cast<const int2*>(P + hs + ((K + 1) >> 1))[g * kGroupSlots + j];
   PoolPick pk;
   pk.soff = d.x;
   pk.n = d.y;
@@ -367,8 +371,8 @@ __device__ __forceinline__ long long* map_entry_ptr(const MapView& m, int64_t id
 
 template <bool kInsert>
 __device__ __forceinline__ int64_t map_find(const MapView& m, int plane, int32_t tt, int32_t conc) {
-  if (tt >= 1 && tt <= m.dom_tt && conc >= 1 && conc <= m.dom_conc)
-    return ((int64_t)plane * m.dom_tt + (tt - 1)) * (int64_t)m.dom_conc + (conc - 1);
+  if (tt >= 1 && tt <= m.dom_tt && conc >= 1 && conc <= m.dom_conc)  // dense map < 2^27 entries: 32-bit math
+    return (int64_t)((plane * m.dom_tt + (tt - 1)) * m.dom_conc + (conc - 1));
   unsigned long long key = ((unsigned long long)(uint32_t)tt << 32) | (uint32_t)conc;
   uint64_t mask = (uint64_t)m.hcap - 1;
   uint64_t h = mix64(key) & mask;

@@ -240,7 +240,8 @@ __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t*
         c[j] = qc[i];
         idx[j] = map_find<true>(m, ph[j], t[j], c[j]);
       }
-      cur[j] = idx[j] >= 0 ? *(volatile long long*)map_entry_ptr(m, idx[j]) : -1;
+      // a hint only (the CAS decides): an L2 load, not a volatile (system-scope) one
+      cur[j] = idx[j] >= 0 ? __ldcg(map_entry_ptr(m, idx[j])) : -1;
     }
 #pragma unroll
     for (int j = 0; j < kQPT; j++)
@@ -248,8 +249,14 @@ __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t*
     // claim empty entries; winners append their key (one atomic per warp)
 #pragma unroll
     for (int j = 0; j < kQPT; j++) {
+      const bool cand = idx[j] >= 0 && cur[j] == kEntryEmpty;
+      if (!__any_sync(kFull, cand)) continue;
+      // one CAS per distinct key per warp (the cold sweep's first wave hits a
+      // few hot entries from every warp at once)
+      const unsigned peers = __match_any_sync(kFull, cand ? (unsigned long long)idx[j]
+                                                          : (0xffffffff00000000ULL | (threadIdx.x & 31)));
       bool won = false;
-      if (idx[j] >= 0 && cur[j] == kEntryEmpty)
+      if (cand && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
         won = atomicCAS((unsigned long long*)map_entry_ptr(m, idx[j]), 0ULL, (unsigned long long)kEntryPending) == 0ULL;
       const unsigned ballot = __ballot_sync(kFull, won);
       if (!ballot) continue;
@@ -505,6 +512,100 @@ __global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 :
         st_stream(out_sidx + i[j], sidx[j], HINT);
       }
     }
+  }
+}
+
+// Compacting sampler: a warp takes 32*CQ queries (CQ per lane, coalesced),
+// finishes the direct-entry ones (single-bucket pools: entry -> sample) at
+// once and queues the rest in shared memory; the queue is then drained with
+// every lane busy (header -> cdf group -> bucket data -> sample).  ~71 % of
+// the config-2 queries are direct, so the pool path runs on dense warps
+// instead of on every warp with a third of its lanes.
+struct PendingDraw {
+  long long e;
+  uint64_t us;
+  uint32_t w0, pw;
+  int32_t rel;
+  int32_t pad;
+};
+
+template <int RNG, int CQ>
+__global__ void __launch_bounds__(256) k_sample_c(MapView m, const Slot* __restrict__ arena,
+                                                  const double* __restrict__ s0, const double* __restrict__ s1,
+                                                  const int32_t* __restrict__ qt, const int32_t* __restrict__ qc,
+                                                  const uint8_t* __restrict__ qp, int64_t Q,
+                                                  const uint64_t* __restrict__ usel, const uint32_t* __restrict__ uidx,
+                                                  uint64_t seed, uint64_t ctr_base, double* __restrict__ out_lat,
+                                                  int32_t* __restrict__ out_sidx, int* flags) {
+  __shared__ PendingDraw qs[8][32 * CQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  PendingDraw* wq = qs[warp];
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t tb = ((int64_t)blockIdx.x * 8 + warp) * (32 * CQ); tb < Q; tb += nwarps * (32 * CQ)) {
+    int np = 0;
+#pragma unroll
+    for (int j = 0; j < CQ; j++) {
+      const int rel = j * 32 + lane;
+      const int64_t i = tb + rel;
+      const bool v = i < Q;
+      int ph = 0;
+      long long e = 0;
+      uint64_t us = 0;
+      uint32_t w0 = 0, pw = 0;
+      if (v) {
+        ph = __ldcs(qp + i) ? 1 : 0;
+        const int64_t idx = map_find<false>(m, ph, __ldcs(qt + i), __ldcs(qc + i));
+        e = idx >= 0 ? *map_entry_ptr(m, idx) : 0;
+        if (RNG == EMU_RNG_EXPLICIT) {
+          us = __ldcs(usel + i);
+          w0 = __ldcs(uidx + i);
+        } else {
+          const uint64_t qid = ctr_base + (uint64_t)i;
+          const uint4 px = philox4x32_10(make_uint4((uint32_t)qid, (uint32_t)(qid >> 32), 0u, 0u), key);
+          us = (uint64_t)px.x | ((uint64_t)px.y << 32);
+          w0 = px.z;
+          pw = px.w;
+        }
+      }
+      const bool direct = v && e > 0 && ((unsigned long long)e & kEntryDirect);
+      const bool pend = v && e > 0 && !direct;
+      if (direct) {
+        const unsigned long long ev = (unsigned long long)e;
+        const int32_t soff = (int32_t)((ev >> 31) & 0x7fffffffULL), n = (int32_t)(ev & 0x7fffffffULL);
+        const uint32_t k = draw_index<RNG>((uint32_t)n, w0, make_uint4(0, 0, 0, pw), ctr_base + (uint64_t)i, key);
+        const int32_t sidx = soff + (int32_t)k;
+        __stcs(out_lat + i, (ph ? s1 : s0)[sidx]);
+        __stcs(out_sidx + i, sidx);
+      } else if (v && e <= 0) {
+        __stcs(out_lat + i, __longlong_as_double(0x7ff8000000000000LL));
+        __stcs(out_sidx + i, -1);
+        atomicOr(flags, FLAG_MISSING);
+      }
+      const unsigned bal = __ballot_sync(kFull, pend);
+      if (pend) {
+        PendingDraw& P = wq[np + __popc(bal & lt)];
+        P.e = e;
+        P.us = us;
+        P.w0 = w0;
+        P.pw = pw;
+        P.rel = rel | (ph << 30);
+      }
+      np += __popc(bal);
+    }
+    __syncwarp();
+    for (int k = lane; k < np; k += 32) {
+      const PendingDraw P = wq[k];
+      const int64_t i = tb + (P.rel & 0x3fffffff);
+      const int ph = P.rel >> 30;
+      const PoolPick pk = pool_pick(arena, P.e, unit_double(P.us));
+      const uint32_t kk = draw_index<RNG>((uint32_t)pk.n, P.w0, make_uint4(0, 0, 0, P.pw), ctr_base + (uint64_t)i, key);
+      const int32_t sidx = pk.soff + (int32_t)kk;
+      __stcs(out_lat + i, (ph ? s1 : s0)[sidx]);
+      __stcs(out_sidx + i, sidx);
+    }
+    __syncwarp();
   }
 }
 
@@ -1011,18 +1112,21 @@ static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s,
   return chunk;
 }
 
-// Sampler variant: queries per thread and streaming-cache hints.  Default
-// (1, hints); EMU_SAMPLE_VARIANT="qpt,hint" overrides for tuning runs.
+// Sampler variant: queries per thread and streaming-cache hints; 0 = the
+// compacting sampler (k_sample_c).  Defaults (measured, config 2): EXPLICIT
+// one query per thread with streaming hints; PHILOX the compacting sampler
+// (its Philox rounds are ALU work the dense drain amortises).
+// EMU_SAMPLE_VARIANT="qpt,hint" overrides for tuning runs.
 static void sample_variant(int rng_mode, int* qpt, int* hint) {
-  static int q = -1, h = -1;
-  if (q < 0) {
-    q = 1;
-    h = -1;  // default: hints for EXPLICIT (streams 21 B/query), none for PHILOX (measured)
+  static int q = -2, h = -1;
+  if (q == -2) {
+    q = -1;
+    h = -1;
     const char* v = getenv("EMU_SAMPLE_VARIANT");
     if (v) sscanf(v, "%d,%d", &q, &h);
-    if (q != 1 && q != 2 && q != 4) q = 1;
+    if (q != -1 && q != 0 && q != 1 && q != 2 && q != 4 && q != 8) q = -1;
   }
-  *qpt = q;
+  *qpt = q >= 0 ? q : (rng_mode == EMU_RNG_EXPLICIT ? 1 : 0);
   *hint = h < 0 ? (rng_mode == EMU_RNG_EXPLICIT ? 1 : 0) : (h ? 1 : 0);
 }
 
@@ -1042,6 +1146,19 @@ static void launch_sample_r(emu_oracle_t o, const int32_t* qt, const int32_t* qc
                             int32_t* sidx, cudaStream_t s) {
   int q, h;
   sample_variant(RNG, &q, &h);
+  if (q == 0 || q == 8) {
+    const int per = q == 0 ? 64 : 128;
+    const int grid = grid_for((n + per - 1) / per, 8, kNumSMs * 64);
+    if (q == 0)
+      EMU_LAUNCH("sample", s, k_sample_c<RNG, 2><<<grid, 256, 0, s>>>(o->map, o->arena, o->plane[0].samples,
+                                                                      o->plane[1].samples, qt, qc, qp, n, us, ui, seed,
+                                                                      ctr, lat, sidx, &o->ctl->flags));
+    else
+      EMU_LAUNCH("sample", s, k_sample_c<RNG, 4><<<grid, 256, 0, s>>>(o->map, o->arena, o->plane[0].samples,
+                                                                      o->plane[1].samples, qt, qc, qp, n, us, ui, seed,
+                                                                      ctr, lat, sidx, &o->ctl->flags));
+    return;
+  }
   if (q == 1 && h) launch_sample_t<RNG, 1, true>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
   if (q == 1 && !h) launch_sample_t<RNG, 1, false>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
   if (q == 2 && h) launch_sample_t<RNG, 2, true>(o, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
