@@ -111,12 +111,12 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu summary, if any."""
+def ncu_metric(kernel: str, key: str = "dram_bytes"):
+    """Per-launch metric of `kernel` from the committed ncu summary (profiles/), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            return json.load(f).get(kernel, {}).get("dram_bytes")
+            return json.load(f).get(kernel, {}).get(key)
     except (OSError, ValueError):
         return None
 
@@ -254,10 +254,23 @@ def run_b200(args):
         step_ms = sum(v["ms_per_launch"] * v["launches"] for v in kern.values()) / 2
         line["roofline"] = {"bound": "hbm", "kernel": "k_sample", "achieved": achieved, "peak": peak,
                             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                            "traffic": ncu_traffic("k_sample"), "bytes_per_query": bpq,
+                            "traffic": ncu_metric("k_sample"), "bytes_per_query": bpq,
                             "share_of_step": kern["sample"]["ms_per_launch"] / max(step_ms, 1e-9),
                             "kernels_ms": {k: round(v["ms_per_launch"], 4) for k, v in kern.items()},
                             "step_roofline_frac": bpq * Q / (ms / 1e3) / 1e9 / peak}
+        # the pool build is per unique key and bound by instruction issue, not HBM:
+        # its roofline is warp instructions (ncu count per launch) / time vs the
+        # SMs' issue rate (148 SMs x 4 schedulers x SM clock)
+        inst = ncu_metric("k_pool_warp", "inst_executed")
+        t_pw = kern["pool_warp"]["ms_per_launch"] * 1e-3
+        sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
+        line["roofline_pool_build"] = {
+            "bound": "issue", "kernel": "k_pool_warp", "unit": "warp-inst/s",
+            "achieved": (inst / t_pw) if inst and t_pw > 0 else None, "peak": 148 * 4 * sm_hz,
+            "frac": (inst / t_pw / (148 * 4 * sm_hz)) if inst and t_pw > 0 else None,
+            "inst_per_launch": inst, "share_of_step": kern["pool_warp"]["ms_per_launch"] / max(step_ms, 1e-9),
+            "note": "one pool per unique key (189k keys per 10M-query cold sweep); no dense contraction, "
+                    "no streaming: issue- and L2-latency-bound (DESIGN.md section 6)"}
         # ---- e2e through the public API with pinned host buffers
         pin = lambda a: torch.as_tensor(a).pin_memory().numpy()  # noqa: E731
         hq = [pin(a) for a in (qt_h, qc_h, qp_h)]
