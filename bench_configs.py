@@ -12,6 +12,7 @@ other configs on one GPU so every SURVEY §8 row has a number:
       M = 32 and M = 256, cold sweeps.
   c4  offline table build from 100M synthetic records (device-resident
       inputs), canonical order; records/s and the build's HBM bytes/s.
+  codec  pack JSON load and trace JSONL ingest, native vs the reference's json path
   c5  what-if sweep: 512 scenarios (32 request rates x 16 burstiness
       values) x 1M steps, keys generated on the GPU per scenario, Philox
       draws; plus the synthetic token fill over 256M entries.
@@ -241,6 +242,72 @@ def c5(args):
                                         "frac": fill_gbs / peak, "bytes_per_entry": 26}}}
 
 
+def codec(args):
+    """pack JSON -> SoA and trace JSONL -> records -> GPU tables.
+    Reference-algorithm times use this package's json path (the reference's
+    json.loads + per-bucket / per-record objects, profile.py:299-404); the
+    native path is csrc/codec.cpp (+ the GPU build for traces)."""
+    from paper_2605_00616_b200.profile import (build_pack_arrays, load_pack, parse_trace_arrays,
+                                               read_trace_file, save_pack, trace_record_to_line, StepTraceRecord,
+                                               StepPhase)
+    import tempfile
+
+    n = args.records_codec
+    rec = records_llama(n, 0)
+    pack = build_pack_arrays(*rec, num_gpu_blocks=1000, canonical=True)
+    data = save_pack(pack)
+    os.environ["EMU_PACK_CODEC"] = "json"
+    t0 = time.perf_counter()
+    ref_pack = load_pack(data)
+    json_s = time.perf_counter() - t0
+    del os.environ["EMU_PACK_CODEC"]
+    native_s = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        fast = load_pack(data)
+        native_s.append(time.perf_counter() - t0)
+    same = all(np.array_equal(a.samples.view(np.uint64), b.samples.view(np.uint64)) and np.array_equal(a.off, b.off)
+               and np.array_equal(a.tt, b.tt) and np.array_equal(a.conc, b.conc)
+               for a, b in zip(fast.soas(), ref_pack.soas()))
+    # trace ingest: JSONL text of n records
+    tt, cc, ph, lat = rec
+    ph_names = (StepPhase.DECODE_ONLY, StepPhase.PREFILL_OR_MIXED)
+    lines = [trace_record_to_line(StepTraceRecord(i, int(a), int(b), ph_names[int(c)], float(d)))
+             for i, (a, b, c, d) in enumerate(zip(tt, cc, ph, lat))]
+    text = ("\n".join(lines) + "\n").encode()
+    with tempfile.NamedTemporaryFile("wb", suffix=".jsonl", delete=False) as f:
+        f.write(text)
+        path = f.name
+    t0 = time.perf_counter()
+    recs = read_trace_file(path)
+    read_py_s = time.perf_counter() - t0
+    parse_s = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        cols = parse_trace_arrays(text)
+        parse_s.append(time.perf_counter() - t0)
+    exact = (np.array_equal(cols[4].view(np.uint64), np.array([r.latency_s for r in recs]).view(np.uint64))
+             and np.array_equal(cols[1], tt) and np.array_equal(cols[2], cc))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    p2 = build_pack_arrays(cols[1], cols[2], cols[3], cols[4], 1000, step=cols[0], canonical=True, keep_host=False)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    os.unlink(path)
+    t0 = time.perf_counter()
+    O.build(tt, cc, ph, lat, canonical=True)
+    cpu_build_s = time.perf_counter() - t0
+    return {"config": "codec", "workload": f"{n}-record Llama-shaped profile: pack JSON ({len(data) / 1e6:.1f} MB) "
+                                           f"and trace JSONL ({len(text) / 1e6:.1f} MB)",
+            "pack_load": {"json_path_s": json_s, "native_s": min(native_s), "speedup": json_s / min(native_s),
+                          "bit_exact_vs_json_path": bool(same), "MB_per_s": len(data) / 1e6 / min(native_s)},
+            "trace_ingest": {"read_trace_file_s": read_py_s, "native_parse_s": min(parse_s),
+                             "records_per_s": n / min(parse_s), "speedup": read_py_s / min(parse_s),
+                             "bit_exact_vs_parse_trace_line": bool(exact), "threads": min(32, CORES),
+                             "gpu_build_s": build_s, "cpu_port_build_s": cpu_build_s,
+                             "end_to_end_records_per_s": n / (min(parse_s) + build_s)}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["c1", "c3", "c4", "c5"])
@@ -249,9 +316,10 @@ def main():
     ap.add_argument("--records-c4", type=int, default=100_000_000)
     ap.add_argument("--scenarios", type=int, default=512)
     ap.add_argument("--steps-c5", type=int, default=1_000_000)
+    ap.add_argument("--records-codec", type=int, default=1_000_000)
     args = ap.parse_args()
     for c in args.configs:
-        res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5}[c](args)
+        res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5, "codec": codec}[c](args)
         print(json.dumps(res), flush=True)
         torch.cuda.empty_cache()
 

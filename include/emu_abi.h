@@ -17,6 +17,8 @@
  *                                                               profile.py:248-250)
  *   EMU_ERR_CUDA       3  -> RuntimeError (any CUDA failure; message from emu_last_error)
  *   EMU_ERR_CAPACITY   4  -> internal: pool arena / key map full; caller flushes and retries
+ *   EMU_ERR_UNSUPPORTED 5 -> internal: a document outside the native codec's subset; the
+ *                            Python mirror re-reads it with the reference's json path
  * emu_last_error() returns a thread-local, NUL-terminated message for the last
  * non-zero status on the calling thread.
  *
@@ -39,6 +41,7 @@ extern "C" {
 #define EMU_ERR_INVALID 2
 #define EMU_ERR_CUDA 3
 #define EMU_ERR_CAPACITY 4
+#define EMU_ERR_UNSUPPORTED 5
 
 /* RNG modes for emu_oracle_sample. */
 #define EMU_RNG_EXPLICIT 0 /* caller supplies u_sel[Q] (u64) and u_idx[Q] (u32)           */
@@ -46,6 +49,7 @@ extern "C" {
 
 typedef struct emu_tables_s* emu_tables_t;
 typedef struct emu_oracle_s* emu_oracle_t;
+typedef struct emu_pack_parsed_s* emu_pack_parsed_t;
 
 /* One phase table in canonical SoA form: buckets sorted by (tt, conc),
  * bkt_off[n_buckets+1] are offsets into samples[n_samples] (bucket b owns
@@ -206,6 +210,41 @@ int emu_distance(const int32_t* q_tt, const int32_t* q_conc, const int32_t* b_tt
 int emu_token_fill(const uint8_t* is_prefill, const int32_t* chunk, const int32_t* prefill_progress,
                    const int32_t* prompt_len, const int32_t* generated, const int32_t* target_len,
                    int64_t n, int32_t* out_ids, uint8_t* out_finished, void* stream);
+
+/* --------------------------------------------------------------- codecs --
+ * Native readers of the reference's on-disk formats (host-only; no CUDA).
+ *
+ * emu_pack_parse_json: a pack document as written by save_pack
+ *   (profile.py:275-296) -> three tables in canonical SoA form, buckets stably
+ *   sorted by (tt, conc) (PhaseTable.from_buckets, profile.py:122-129), samples
+ *   in file order, numbers parsed correctly rounded (== Python float()).
+ *   Replaces load_pack's json.loads + per-bucket objects (profile.py:299-347);
+ *   validation stays with the caller (ProfilePack.validate).  Returns
+ *   EMU_ERR_UNSUPPORTED for documents outside the subset the reference writes
+ *   (syntax errors, escaped strings, non-integer keys, NaN, duplicate keys,
+ *   schema_version != 1): the caller re-reads those with json.loads, which
+ *   raises the reference's own PackFormatError / PackVersionError. */
+int emu_pack_parse_json(const char* text, int64_t len, emu_pack_parsed_t* out);
+/* sizes[6] = {B, N} of decode, mixed, combined; metadata_len = bytes of the
+ * metadata object as canonical JSON (sorted keys, no spaces). */
+int emu_pack_parsed_info(emu_pack_parsed_t p, int64_t* schema_version, int64_t* num_gpu_blocks,
+                         int64_t* sizes, int64_t* metadata_len);
+int emu_pack_parsed_copy(emu_pack_parsed_t p, int table, int32_t* tt, int32_t* conc, int64_t* off,
+                         double* samples);
+int emu_pack_parsed_metadata(emu_pack_parsed_t p, char* buf, int64_t cap);
+void emu_pack_parsed_free(emu_pack_parsed_t p);
+
+/* emu_trace_parse_jsonl: step-trace JSON lines (trace_record_to_line /
+ *   parse_trace_line, profile.py:350-380) -> record columns in file order,
+ *   blank lines skipped, parsed on n_threads host threads.  *n_out = records;
+ *   EMU_ERR_CAPACITY if more than `cap`; EMU_ERR_UNSUPPORTED (with *bad_line =
+ *   the record index) for a line outside the subset -- the caller re-reads
+ *   the file with parse_trace_line for the reference's exact error.
+ *   emu_trace_count_lines counts the non-blank lines. */
+int64_t emu_trace_count_lines(const char* text, int64_t len);
+int emu_trace_parse_jsonl(const char* text, int64_t len, int n_threads, int64_t cap, int64_t* step,
+                          int32_t* tt, int32_t* conc, uint8_t* phase, double* lat, int64_t* n_out,
+                          int64_t* bad_line);
 
 /* ------------------------------------------------------------ profiling --
  * Every kernel the library launches goes through one launch macro that counts

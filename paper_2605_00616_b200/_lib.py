@@ -14,7 +14,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EMU_LIB_PATH") or os.path.join(_PKG, "libemu_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 
-EMU_OK, EMU_ERR_NO_DATA, EMU_ERR_INVALID, EMU_ERR_CUDA, EMU_ERR_CAPACITY = 0, 1, 2, 3, 4
+EMU_OK, EMU_ERR_NO_DATA, EMU_ERR_INVALID, EMU_ERR_CUDA, EMU_ERR_CAPACITY, EMU_ERR_UNSUPPORTED = 0, 1, 2, 3, 4, 5
 EMU_RNG_EXPLICIT, EMU_RNG_PHILOX = 0, 1
 
 c_int, c_i32, c_i64, c_u64, c_dbl, c_vp = (ctypes.c_int, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
@@ -62,6 +62,15 @@ SIGNATURES = {
     "emu_oracle_stats": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "emu_distance": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "emu_token_fill": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "emu_pack_parse_json": (c_int, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
+    "emu_pack_parsed_info": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_vp,
+                                     ctypes.POINTER(c_i64)]),
+    "emu_pack_parsed_copy": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),
+    "emu_pack_parsed_metadata": (c_int, [c_vp, c_vp, c_i64]),
+    "emu_pack_parsed_free": (None, [c_vp]),
+    "emu_trace_count_lines": (c_i64, [c_vp, c_i64]),
+    "emu_trace_parse_jsonl": (c_int, [c_vp, c_i64, c_int, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                      ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "emu_launch_count": (c_i64, []),
     "emu_profile_enable": (c_int, [c_int]),
     "emu_profile_read": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),

@@ -16,6 +16,7 @@ match the reference; what changes is where the work happens:
 from __future__ import annotations
 
 import json
+import os
 from dataclasses import dataclass, field
 from enum import Enum
 from pathlib import Path
@@ -434,9 +435,9 @@ def _parse_table(tables_obj: dict, kind: TableKind) -> PhaseTable:
     return PhaseTable.from_buckets(kind, out)
 
 
-def load_pack(data: bytes | str) -> ProfilePack:
-    """Parse and validate pack bytes; ranges are derived from the buckets."""
-    text = data.decode("utf-8") if isinstance(data, (bytes, bytearray)) else data
+def _load_pack_json(text: str) -> ProfilePack:
+    """The reference's json.loads path (profile.py:299-347): the fallback of
+    load_pack and the source of its exact error messages."""
     try:
         doc = json.loads(text)
     except json.JSONDecodeError as exc:
@@ -459,6 +460,92 @@ def load_pack(data: bytes | str) -> ProfilePack:
         raise PackFormatError("num_gpu_blocks must be an integer")
     pack = ProfilePack(blocks, decode, mixed, combined, {str(k): str(v) for k, v in metadata.items()}, version)
     pack.validate()
+    return pack
+
+
+def _load_pack_native(raw: bytes):
+    """emu_pack_parse_json (csrc/codec.cpp): the pack as three TableSoA, or None
+    when the document is outside the native subset (-> the json path)."""
+    import ctypes
+
+    from . import _lib
+
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(raw, len(raw))
+    rc = L.emu_pack_parse_json(buf, len(raw), ctypes.byref(h))
+    if rc == _lib.EMU_ERR_UNSUPPORTED:
+        return None
+    _lib.check(rc, invalid_exc=PackFormatError)
+    try:
+        ver, blocks, mlen = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        sizes = np.zeros(6, dtype=np.int64)
+        _lib.check(L.emu_pack_parsed_info(h, ctypes.byref(ver), ctypes.byref(blocks), _lib.ptr(sizes),
+                                          ctypes.byref(mlen)))
+        soas = []
+        for t in range(3):
+            B, N = int(sizes[2 * t]), int(sizes[2 * t + 1])
+            s = TableSoA(np.empty(B, np.int32), np.empty(B, np.int32), np.empty(B + 1, np.int64),
+                         np.empty(N, np.float64))
+            _lib.check(L.emu_pack_parsed_copy(h, t, _lib.ptr(s.tt), _lib.ptr(s.conc), _lib.ptr(s.off),
+                                              _lib.ptr(s.samples)))
+            soas.append(s)
+        mbuf = ctypes.create_string_buffer(max(1, mlen.value))
+        _lib.check(L.emu_pack_parsed_metadata(h, mbuf, mlen.value))
+        metadata = json.loads(mbuf.raw[:mlen.value].decode("utf-8"))
+    finally:
+        L.emu_pack_parsed_free(h)
+    return int(ver.value), int(blocks.value), metadata, soas
+
+
+def _validate_soa_table(kind: TableKind, s: TableSoA) -> None:
+    """PhaseTable.validate for a SoA table without materialising buckets: the
+    first bucket (in (tt, conc) order) that fails Bucket.validate or repeats a
+    key raises exactly the message the bucket walk would raise."""
+    B = len(s.tt)
+    if B == 0:
+        return
+    counts = np.diff(s.off)
+    bad = (s.tt < 1) | (s.conc < 1) | (counts == 0)
+    nonpos = ~(s.samples > 0)
+    if nonpos.any():
+        seg = np.searchsorted(s.off, np.flatnonzero(nonpos), side="right") - 1
+        bad[seg] = True
+    dup = np.zeros(B, dtype=bool)
+    dup[1:] = (s.tt[1:] == s.tt[:-1]) & (s.conc[1:] == s.conc[:-1])
+    hit = np.flatnonzero(bad | dup)
+    if len(hit) == 0:
+        return
+    i = int(hit[0])
+    Bucket(int(s.tt[i]), int(s.conc[i]), s.samples[s.off[i]:s.off[i + 1]].tolist()).validate()
+    raise PackValidationError(f"{kind.value} table has duplicate bucket {(int(s.tt[i]), int(s.conc[i]))}")
+
+
+def load_pack(data: bytes | str) -> ProfilePack:
+    """Parse and validate pack bytes; ranges are derived from the buckets.
+
+    Well-formed documents go through the native codec (csrc/codec.cpp) into
+    SoA tables -- bit-identical to the reference's parse -- and are validated
+    vectorised; anything else takes the reference's json.loads path, which
+    raises its exact errors."""
+    raw = data.encode("utf-8") if isinstance(data, str) else bytes(data)
+    parsed = None
+    if os.environ.get("EMU_PACK_CODEC", "native") != "json":
+        parsed = _load_pack_native(raw)
+    if parsed is None:
+        return _load_pack_json(raw.decode("utf-8"))
+    version, blocks, metadata, soas = parsed
+    kinds = (TableKind.DECODE, TableKind.MIXED, TableKind.COMBINED)
+    tables = [PhaseTable.from_soa(k, s) for k, s in zip(kinds, soas)]
+    pack = ProfilePack(blocks, *tables, {str(k): str(v) for k, v in metadata.items()}, version)
+    if pack.num_gpu_blocks < 1:
+        raise PackValidationError(f"num_gpu_blocks must be >= 1, got {pack.num_gpu_blocks}")
+    for k, s in zip(kinds, soas):
+        _validate_soa_table(k, s)
+    phase_total = int(soas[0].off[-1]) + int(soas[1].off[-1])
+    if int(soas[2].off[-1]) != phase_total:
+        raise PackValidationError(
+            f"combined table inconsistent: {int(soas[2].off[-1])} samples != decode+mixed {phase_total}")
     return pack
 
 
@@ -497,3 +584,55 @@ def read_trace_file(path: str | Path) -> list[StepTraceRecord]:
 def iter_trace_dir(path: str | Path) -> Iterator[StepTraceRecord]:
     for file in sorted(Path(path).glob("*.jsonl")):
         yield from read_trace_file(file)
+
+
+def parse_trace_arrays(text: bytes | str, threads: int = 0):
+    """JSONL trace text -> record columns (step i64, tt i32, conc i32, phase u8,
+    latency_s f64) in file order, via emu_trace_parse_jsonl (csrc/codec.cpp,
+    multithreaded).  Same records as [parse_trace_line(l) for l in lines]; a
+    line outside the native subset re-reads the text line by line with
+    parse_trace_line (the reference's errors and coercions)."""
+    import ctypes
+
+    from . import _lib
+
+    raw = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    L = _lib.lib()
+    buf = ctypes.create_string_buffer(raw, len(raw))
+    n = int(L.emu_trace_count_lines(buf, len(raw)))
+    cols = (np.empty(n, np.int64), np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.uint8),
+            np.empty(n, np.float64))
+    n_out, bad = ctypes.c_int64(), ctypes.c_int64()
+    threads = threads or min(32, len(os.sched_getaffinity(0)))
+    rc = L.emu_trace_parse_jsonl(buf, len(raw), int(threads), n, *(_lib.ptr(c) for c in cols),
+                                 ctypes.byref(n_out), ctypes.byref(bad))
+    if rc == _lib.EMU_ERR_UNSUPPORTED:
+        recs = [parse_trace_line(s) for s in (ln.strip() for ln in raw.decode("utf-8").splitlines()) if s]
+        return records_to_arrays_with_step(recs)
+    _lib.check(rc, invalid_exc=PackFormatError)
+    return cols
+
+
+def records_to_arrays_with_step(recs: Sequence[StepTraceRecord]):
+    n = len(recs)
+    return (np.fromiter((r.step_index for r in recs), np.int64, n),
+            np.fromiter((r.total_tokens for r in recs), np.int64, n).astype(np.int32),
+            np.fromiter((r.concurrency for r in recs), np.int64, n).astype(np.int32),
+            np.fromiter((phase_code(r.phase) for r in recs), np.uint8, n),
+            np.fromiter((r.latency_s for r in recs), np.float64, n))
+
+
+def read_trace_arrays(path: str | Path, threads: int = 0):
+    """read_trace_file's records as columns (native parse of the whole file)."""
+    return parse_trace_arrays(Path(path).read_bytes(), threads)
+
+
+def build_pack_from_traces(paths, num_gpu_blocks: int, metadata: dict[str, str] | None = None, *,
+                           canonical: bool = True) -> ProfilePack:
+    """Trace JSONL files -> GPU-built pack: the native ingest feeding
+    emu_tables_build (cli.py:202-208 reads the files with read_trace_file and
+    calls build_pack).  Records are concatenated in the given path order."""
+    parts = [read_trace_arrays(p) for p in paths]
+    step, tt, conc, ph, lat = (np.concatenate([c[i] for c in parts]) if parts else np.zeros(0)
+                               for i in range(5))
+    return build_pack_arrays(tt, conc, ph, lat, num_gpu_blocks, metadata, step=step, canonical=canonical)
