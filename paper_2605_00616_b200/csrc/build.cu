@@ -7,7 +7,9 @@
 //                     smallest failing index wins (build_pack reports the first).
 //   2. k_make_keys  : hi = (tt-1) << cbits | (conc-1), lo = lat_bits << 1 | phase
 //                     (positive doubles order like their IEEE bit patterns).
-//   3. LSD radix sort, 8-bit digits, stable (warp match_any ranking):
+//   3. LSD radix sort, 8-bit digits, stable: per 4096-record tile, warp
+//      match_any ranking into shared memory in digit order, then coalesced
+//      digit runs out (k_radix_scatter); scratch from a stream-ordered pool:
 //        canonical -> digits of lo then hi   (bucket key, then latency value)
 //        capture   -> digits of hi only      (stable = build_pack's dict appends)
 //      digit positions whose histogram is a single bin are skipped.
@@ -18,6 +20,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -119,27 +125,62 @@ __global__ void __launch_bounds__(kRThreads) k_radix_up(const uint64_t* __restri
   counts[(int64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
 }
 
-// Stable scatter of (hi, lo) pairs by one digit of `key` (== hi or lo).
-__global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __restrict__ key, int shift,
+// Stable scatter of (hi, lo) pairs by one digit of `key` (== hi or lo).  The
+// tile is first ranked into shared memory in digit order (warp match_any per
+// round of 256, stable), then written out with consecutive threads on
+// consecutive output positions: every digit's run of the tile is a coalesced
+// segment instead of 256 interleaved 8-byte streams.
+constexpr int kRSmem = kRTile * 16;
+__global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __restrict__ key, int shift, int key_is_hi,
                                                             const uint64_t* __restrict__ a_hi,
                                                             const uint64_t* __restrict__ a_lo, uint64_t* __restrict__ b_hi,
                                                             uint64_t* __restrict__ b_lo, int64_t n, int64_t nblk,
                                                             const unsigned int* __restrict__ offs) {
+  extern __shared__ uint64_t tile[];  // [kRTile] hi, then [kRTile] lo
+  uint64_t* s_hi = tile;
+  uint64_t* s_lo = tile + kRTile;
   __shared__ unsigned int gofs[256];
+  __shared__ unsigned int tstart[256];
   __shared__ unsigned int run[256];
   __shared__ unsigned short wh[kRWarps][256];
+  __shared__ unsigned int wsum[kRWarps];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  gofs[t] = offs[(int64_t)t * nblk + blockIdx.x];
+  const int64_t blk = blockIdx.x;
+  const int64_t base = blk * kRTile;
+  const int cnt_tile = (int)min((int64_t)kRTile, n - base);
+  // this tile's digit counts from the scanned (digit-major) offsets
+  const int64_t flat = (int64_t)t * nblk + blk;
+  const unsigned int o0 = offs[flat];
+  const unsigned int o1 = (t == 255 && blk == nblk - 1) ? (unsigned int)n : offs[flat + 1];
+  gofs[t] = o0;
+  const unsigned int c = o1 - o0;
+  // exclusive scan of the 256 counts -> tile-local digit starts
+  unsigned int x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
   run[t] = 0;
+  __syncthreads();
+  unsigned int wb = 0;
+  for (int q = 0; q < w; q++) wb += wsum[q];
+  tstart[t] = wb + x - c;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t base = (int64_t)blockIdx.x * kRTile;
   for (int k = 0; k < kRRounds; k++) {
-    const int64_t i = base + (int64_t)k * kRThreads + t;
-    const bool valid = i < n;
+    const int li = k * kRThreads + t;
+    const int64_t i = base + li;
+    const bool valid = li < cnt_tile;
 #pragma unroll
     for (int q = 0; q < kRWarps; q++) wh[q][t] = 0;
     __syncthreads();
-    const unsigned d = valid ? (unsigned)((key[i] >> shift) & 255u) : 256u + (unsigned)lane;
+    uint64_t h = 0, l = 0;
+    if (valid) {
+      h = a_hi[i];
+      l = a_lo[i];
+    }
+    const unsigned d = valid ? (unsigned)(((key_is_hi ? h : l) >> shift) & 255u) : 256u + (unsigned)lane;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const unsigned rank = __popc(peers & lt_mask);
     if (valid && rank == 0) wh[w][d] = (unsigned short)__popc(peers);
@@ -148,19 +189,26 @@ __global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __r
       unsigned r = run[t];
 #pragma unroll
       for (int q = 0; q < kRWarps; q++) {
-        unsigned c = wh[q][t];
+        unsigned cc = wh[q][t];
         wh[q][t] = (unsigned short)r;
-        r += c;
+        r += cc;
       }
       run[t] = r;
     }
     __syncthreads();
     if (valid) {
-      const unsigned pos = gofs[d] + wh[w][d] + rank;
-      b_hi[pos] = a_hi[i];
-      b_lo[pos] = a_lo[i];
+      const unsigned lp = tstart[d] + wh[w][d] + rank;
+      s_hi[lp] = h;
+      s_lo[lp] = l;
     }
-    __syncthreads();
+    __syncthreads();  // wh is rewritten by the next round
+  }
+  for (int j = t; j < cnt_tile; j += kRThreads) {
+    const uint64_t h = s_hi[j], l = s_lo[j];
+    const unsigned d = (unsigned)(((key_is_hi ? h : l) >> shift) & 255u);
+    const unsigned pos = gofs[d] + (unsigned)j - tstart[d];
+    b_hi[pos] = h;
+    b_lo[pos] = l;
   }
 }
 
@@ -245,10 +293,29 @@ __global__ void k_conc_range(const int32_t* c, int64_t n, int* mm) {
   }
 }
 
+
+// Build scratch comes from the device's stream-ordered memory pool, kept
+// reserved between builds (release threshold = max): repeated builds reuse it
+// instead of mapping and unmapping GBs with cudaMalloc / cudaFree.
+static cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static bool pool_set = false;
+  if (!pool_set) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set = true;
+  }
+  return cudaMallocAsync(p, bytes > 0 ? bytes : 1, s);
+}
+
+// Table outputs from the same pool (TableBuf::release frees them with cudaFree).
 template <typename T>
-static int balloc(T** p, int64_t n) {
+static int palloc(cudaStream_t s, T** p, int64_t n) {
   *p = nullptr;
-  EMU_CUDA(cudaMalloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1)));
+  EMU_CUDA(scratch_alloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), s));
   return EMU_OK;
 }
 
@@ -269,8 +336,8 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
   tb = TableBuf();
   int rc;
   if (m == 0) {
-    if ((rc = balloc(&tb.bkt_tt, 0)) || (rc = balloc(&tb.bkt_conc, 0)) || (rc = balloc(&tb.bkt_off, 1)) ||
-        (rc = balloc(&tb.samples, 0)) || (rc = balloc(&tb.row_tt, 0)) || (rc = balloc(&tb.row_start, 1)))
+    if ((rc = palloc(s, &tb.bkt_tt, 0)) || (rc = palloc(s, &tb.bkt_conc, 0)) || (rc = palloc(s, &tb.bkt_off, 1)) ||
+        (rc = palloc(s, &tb.samples, 0)) || (rc = palloc(s, &tb.row_tt, 0)) || (rc = palloc(s, &tb.row_start, 1)))
       return rc;
     EMU_CUDA(cudaMemsetAsync(tb.bkt_off, 0, 8, s));
     EMU_CUDA(cudaMemsetAsync(tb.row_start, 0, 8, s));
@@ -282,8 +349,8 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
   EMU_CUDA(cudaMemcpyAsync(&nb_u, total_dev, 4, cudaMemcpyDeviceToHost, s));
   EMU_CUDA(cudaStreamSynchronize(s));
   const int64_t nb = nb_u;
-  if ((rc = balloc(&tb.bkt_tt, nb)) || (rc = balloc(&tb.bkt_conc, nb)) || (rc = balloc(&tb.bkt_off, nb + 1)) ||
-      (rc = balloc(&tb.samples, m)))
+  if ((rc = palloc(s, &tb.bkt_tt, nb)) || (rc = palloc(s, &tb.bkt_conc, nb)) || (rc = palloc(s, &tb.bkt_off, nb + 1)) ||
+      (rc = palloc(s, &tb.samples, m)))
     return rc;
   HeadOut ho{hi, lo, cbits, tb.bkt_tt, tb.bkt_conc, tb.bkt_off, tb.samples};
   EMU_CUDA(device_excl_scan<unsigned int>(HeadIn{hi}, ho, m, partial, total_dev, s));
@@ -295,7 +362,7 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
   EMU_CUDA(cudaMemcpyAsync(&nr_u, total_dev, 4, cudaMemcpyDeviceToHost, s));
   EMU_CUDA(cudaStreamSynchronize(s));
   const int64_t nr = nr_u;
-  if ((rc = balloc(&tb.row_tt, nr)) || (rc = balloc(&tb.row_start, nr + 1))) return rc;
+  if ((rc = palloc(s, &tb.row_tt, nr)) || (rc = palloc(s, &tb.row_start, nr + 1))) return rc;
   EMU_CUDA(device_excl_scan<unsigned int>(RowIn{tb.bkt_tt}, RowOut{tb.bkt_tt, tb.row_tt, tb.row_start}, nb, partial,
                                           total_dev, s));
   EMU_CUDA(cudaMemcpyAsync(tb.row_start + nr, &nb, 8, cudaMemcpyHostToDevice, s));
@@ -350,6 +417,14 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   if (n < 0) return fail(EMU_ERR_INVALID, "negative record count");
   if (n >= (1LL << 31)) return fail(EMU_ERR_INVALID, "record count must be < 2^31 per build");
   cudaStream_t s = as_stream(stream);
+  static const bool trace = getenv("EMU_BUILD_TRACE") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    fprintf(stderr, "[emu build] %-24s %8.3f ms\n", what, ms);
+  };
   // Stage host inputs on the device (device inputs are used in place).
   std::vector<void*> owned;
   auto stage = [&](const void* src, size_t bytes, const void** dst) -> int {
@@ -358,15 +433,25 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
       return EMU_OK;
     }
     void* d = nullptr;
-    EMU_CUDA(cudaMalloc(&d, bytes));
+    EMU_CUDA(scratch_alloc(&d, bytes, s));
     owned.push_back(d);
     EMU_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
     *dst = d;
     return EMU_OK;
   };
   auto free_owned = [&]() {
-    for (void* p : owned) cudaFree(p);
+    for (void* p : owned) cudaFreeAsync(p, s);
     owned.clear();
+  };
+  auto salloc = [&](auto** p, int64_t count) -> int {
+    using T = std::remove_pointer_t<std::remove_reference_t<decltype(p)>>;
+    *p = nullptr;
+    void* q = nullptr;
+    EMU_CUDA(scratch_alloc(&q, sizeof(**p) * (size_t)(count > 0 ? count : 1), s));
+    *p = (decltype(*p))q;
+    owned.push_back(q);
+    (void)sizeof(T);
+    return EMU_OK;
   };
   RecIn r{};
   r.n = n;
@@ -380,13 +465,10 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   unsigned long long* first_bad = nullptr;
   int* small = nullptr;  // maxv[2], mm[2]
   unsigned int* total_dev = nullptr;
-  if ((rc = balloc(&first_bad, 1)) || (rc = balloc(&small, 4)) || (rc = balloc(&total_dev, 2))) {
+  if ((rc = salloc(&first_bad, 1)) || (rc = salloc(&small, 4)) || (rc = salloc(&total_dev, 2))) {
     free_owned();
     return rc;
   }
-  owned.push_back(first_bad);
-  owned.push_back(small);
-  owned.push_back(total_dev);
   auto* t = new emu_tables_s();
   auto bail = [&](int code) {
     for (int j = 0; j < 3; j++) t->tab[j].release();
@@ -421,6 +503,7 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
     return fail(EMU_ERR_INVALID, "trace record " + std::to_string(fb >> 3) + " failed validation check " +
                                      std::to_string(fb & 7));
   }
+  mark("validate");
   const int cbits = bits_for((int64_t)mv[1] - 1);
   const int tbits = bits_for((int64_t)mv[0] - 1);
   // 2. keys (double buffered)
@@ -429,11 +512,9 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   const int64_t nblk = (n + kRTile - 1) / kRTile;
   const int64_t ncount = 256 * nblk;
   const int64_t npart = std::max<int64_t>((ncount + kScanTile - 1) / kScanTile, (n + kScanTile - 1) / kScanTile) + 1;
-  if ((rc = balloc(&hi0, n)) || (rc = balloc(&lo0, n)) || (rc = balloc(&hi1, n)) || (rc = balloc(&lo1, n)) ||
-      (rc = balloc(&counts, ncount)) || (rc = balloc(&hist, 16 * 256)) || (rc = balloc(&partial, npart)))
+  if ((rc = salloc(&hi0, n)) || (rc = salloc(&lo0, n)) || (rc = salloc(&hi1, n)) || (rc = salloc(&lo1, n)) ||
+      (rc = salloc(&counts, ncount)) || (rc = salloc(&hist, 16 * 256)) || (rc = salloc(&partial, npart)))
     return bail(rc);
-  for (void* p : {(void*)hi0, (void*)lo0, (void*)hi1, (void*)lo1, (void*)counts, (void*)hist, (void*)partial})
-    owned.push_back(p);
   EMU_LAUNCH("make_keys", s, k_make_keys<<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, cbits, hi0, lo0));
   // 3. which digit positions actually vary
   PassSet ps{};
@@ -452,7 +533,10 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   if (cudaMemcpyAsync(hh.data(), hist, 4 * 16 * 256, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess)
     return bail(cuda_fail(cudaGetLastError(), "k_digit_hist"));
+  mark("keys+hist");
   // 4. LSD passes
+  if (cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "radix smem attribute"));
   for (int p = 0; p < ps.n; p++) {
     unsigned int mx = *std::max_element(hh.begin() + p * 256, hh.begin() + (p + 1) * 256);
     if ((int64_t)mx == n) continue;  // all records share this digit: pass is the identity
@@ -462,13 +546,16 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
         [counts] __device__(int64_t i) { return counts[i]; },
         [counts] __device__(int64_t i, unsigned int ex) { counts[i] = ex; }, ncount, partial, total_dev, s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "radix scan"));
-    EMU_LAUNCH("radix_scatter", s, k_radix_scatter<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], hi0, lo0, hi1, lo1, n, nblk, counts));
+    EMU_LAUNCH("radix_scatter", s, k_radix_scatter<<<(unsigned)nblk, kRThreads, kRSmem, s>>>(
+                                       key, ps.shift[p], ps.word[p], hi0, lo0, hi1, lo1, n, nblk, counts));
     std::swap(hi0, hi1);
     std::swap(lo0, lo1);
   }
   if (cudaGetLastError() != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "radix sort"));
+  mark("radix sort");
   // 5. combined table = sorted run; decode/mixed = stable partition by phase
   if ((rc = segment(hi0, lo0, n, cbits, partial, total_dev, small + 2, s, t->tab[2]))) return bail(rc);
+  mark("segment combined");
   cudaError_t e = device_excl_scan<unsigned int>(PhaseIn{lo0}, [] __device__(int64_t, unsigned int) {}, n, partial,
                                                  total_dev, s);
   if (e != cudaSuccess) return bail(cuda_fail(e, "phase partition count"));
@@ -479,11 +566,15 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   e = device_excl_scan<unsigned int>(PhaseIn{lo0}, PhaseOut{hi0, lo0, hi1, lo1, hi1 + n_dec, lo1 + n_dec}, n, partial,
                                      total_dev, s);
   if (e != cudaSuccess) return bail(cuda_fail(e, "phase partition"));
+  mark("phase partition");
   if ((rc = segment(hi1, lo1, n_dec, cbits, partial, total_dev, small + 2, s, t->tab[0]))) return bail(rc);
+  mark("segment decode");
   if ((rc = segment(hi1 + n_dec, lo1 + n_dec, n - n_dec, cbits, partial, total_dev, small + 2, s, t->tab[1])))
     return bail(rc);
   if (cudaStreamSynchronize(s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "build"));
+  mark("segment mixed");
   free_owned();
+  mark("free");
   *out = t;
   return EMU_OK;
 }

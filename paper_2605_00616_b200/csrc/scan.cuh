@@ -68,28 +68,40 @@ __global__ void k_scan_partials(T* partial, int64_t nb, T* total_out) {
   if (threadIdx.x == 0 && total_out) *total_out = carry;
 }
 
-// out(i, excl) receives each element's exclusive prefix.
+// out(i, excl) receives each element's exclusive prefix.  Warp w of a tile
+// owns 512 consecutive elements, read and emitted in 16 coalesced rounds of 32
+// (loads and the out() stores stay coalesced); one block scan combines the
+// warp totals.
 template <typename T, typename In, typename Out>
-__global__ void k_scan_down(In in, Out out, int64_t n, const T* partial) {
-  __shared__ T sm[33];
-  const int64_t base = (int64_t)blockIdx.x * kScanTile;
-  // thread t owns kScanItems consecutive elements
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(In in, Out out, int64_t n, const T* partial) {
+  __shared__ T wsum[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t wbase = (int64_t)blockIdx.x * kScanTile + (int64_t)w * (32 * kScanItems);
   T v[kScanItems];
   T acc = 0;
-  const int64_t my = base + (int64_t)threadIdx.x * kScanItems;
 #pragma unroll
   for (int k = 0; k < kScanItems; k++) {
-    int64_t i = my + k;
+    const int64_t i = wbase + k * 32 + lane;
     v[k] = i < n ? in(i) : T(0);
     acc += v[k];
   }
-  T tot;
-  T ex = block_excl_scan<T>(acc, tot, sm) + partial[blockIdx.x];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) wsum[w] = acc;
+  __syncthreads();
+  T carry = partial[blockIdx.x];
+  for (int q = 0; q < w; q++) carry += wsum[q];
 #pragma unroll
   for (int k = 0; k < kScanItems; k++) {
-    int64_t i = my + k;
-    if (i < n) out(i, ex);
-    ex += v[k];
+    T x = v[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const int64_t i = wbase + k * 32 + lane;
+    if (i < n) out(i, carry + x - v[k]);
+    carry += __shfl_sync(0xffffffffu, x, 31);
   }
 }
 

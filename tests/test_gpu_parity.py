@@ -60,6 +60,17 @@ def test_gpu_build_matches_oracle(c1_records, canonical):
     assert pack.decode_table.total_samples + pack.mixed_table.total_samples == len(c1_records[0])
 
 
+@pytest.mark.parametrize("canonical", [True, False])
+def test_gpu_build_large_matches_oracle(canonical):
+    """3M records: ~730 radix tiles per pass, multi-tile digit runs, scans over
+    many tiles -- the GPU build vs the C restatement of build_pack."""
+    rec = records_llama(3_000_000, 5)
+    got = DeviceTables.build(*rec, canonical=canonical).to_host()
+    want = O.build(*rec, canonical=canonical)
+    for g, w in zip(got, want):
+        assert soa_equal(g, w)
+
+
 def test_gpu_build_edge_cases():
     # empty input
     pack = build_pack_arrays(np.zeros(0), np.zeros(0), np.zeros(0), np.zeros(0), 5)
