@@ -56,6 +56,10 @@ struct DevTable {
   const int32_t* wpre;
   const int32_t* rowbase;
   int32_t wpr;
+  // Column index of the same grid: buckets ordered by (conc, tt).
+  const int32_t* col_start;
+  const int32_t* col_tt;
+  const int32_t* col_b;
   // sq_t[k] = (k / span_t)^2 rounded exactly like norm_dist, k < lt (same for conc).
   const double* sq_t;
   const double* sq_c;

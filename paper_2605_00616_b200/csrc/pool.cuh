@@ -538,7 +538,50 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
   if (C > 0) {
     const int32_t nri = w.i1 - w.i0 + 1;
     const int32_t b0 = T.bsat[w.i0 * st + (st - 1)], b1 = T.bsat[(w.i1 + 1) * st + (st - 1)];
-    if (b1 - b0 <= 2 * nri || C == b1 - b0) {  // scan the tt slab
+    const int32_t ncj = w.j1 - w.j0 + 1;
+    if (ncj * 16 < nri && ncj <= NT) {  // tall, narrow window: column index (see warp_enumerate)
+      const int32_t tlo = T.tt_lo + w.i0, thi = T.tt_lo + w.i1;
+      const int r = G::rank();
+      int32_t lo = 0, cnt = 0;
+      if (r < ncj) {
+        const int32_t s0 = T.col_start[w.j0 + r], s1 = T.col_start[w.j0 + r + 1];
+        lo = (int32_t)lower_bound_i32(T.col_tt, s0, s1, tlo);
+        cnt = (int32_t)upper_bound_i32(T.col_tt, lo, s1, thi) - lo;
+      }
+      long long tot;
+      const int ex = (int)G::excl_scan(cnt, tot, ws.scr);
+      ws.rows[r] = lo;
+      ws.rows[NT + r] = ex;
+      G::sync();
+      for (int kb = 0; kb < (int)tot; kb += NT) {
+        const int k = kb + r;
+        bool in = false;
+        double d = 0.0;
+        int32_t bb = 0;
+        if (k < (int)tot) {
+          int l0 = 0, h0 = ncj;  // last column whose prefix <= k
+          while (h0 - l0 > 1) {
+            const int mid = (l0 + h0) >> 1;
+            if (ws.rows[NT + mid] <= k)
+              l0 = mid;
+            else
+              h0 = mid;
+          }
+          const int32_t idx = ws.rows[l0] + (k - ws.rows[NT + l0]);
+          bb = T.col_b[idx];
+          d = dist_tab(T, (int64_t)t - T.col_tt[idx], (int64_t)c - (T.c_lo + w.j0 + l0), span_t, span_c);
+          in = d <= dmax;
+        }
+        long long kt;
+        const int ex2 = (int)G::excl_scan(in ? 1 : 0, kt, ws.scr);
+        if (in) {
+          ws.d[pos + ex2] = d;
+          ws.b[pos + ex2] = bb;
+        }
+        pos += (int)kt;
+      }
+      G::sync();
+    } else if (b1 - b0 <= 2 * nri || C == b1 - b0) {  // scan the tt slab
       const int32_t clo = T.c_lo + w.j0, chi = T.c_lo + w.j1;
       for (int32_t base = b0; base < b1; base += NT) {
         const int32_t b = base + G::rank();
@@ -608,6 +651,67 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
     }
   }
   G::sync();
+  // ---- 3b. (group / CTA tiers) drop candidates beyond the pool radius bound.
+  // d_K lies in [~r1, sqrt(2) r1]: of 8 pivots r1 * (1 + (sqrt(2)-1)(l+1)/8) the
+  // smallest whose disc already holds >= floor samples bounds d_K, and every
+  // candidate beyond it sorts after the pool.  Typical M = 256 windows shrink
+  // from ~1.8 K to ~1.1 K candidates, halving the shared-memory sort.
+  if (NT > 32 && pos > 64 && dmax < 1e300) {
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ws.scr) + 16;
+    if (G::rank() < 8) cnt[G::rank()] = 0;
+    G::sync();
+    double pv[8];
+    unsigned long long acc[8];
+#pragma unroll
+    for (int l = 0; l < 8; l++) {
+      pv[l] = r1 * (1.0 + 0.41421356237309515 * (double)(l + 1) * 0.125);
+      acc[l] = 0;
+    }
+    for (int i = G::rank(); i < pos; i += NT) {
+      const double d = ws.d[i];
+      const int32_t bb = ws.b[i];
+      const unsigned long long n =
+          (unsigned long long)min((int64_t)(T.bkt_off[bb + 1] - T.bkt_off[bb]), mfloor);
+#pragma unroll
+      for (int l = 0; l < 8; l++) acc[l] += d <= pv[l] ? n : 0ULL;
+    }
+#pragma unroll
+    for (int l = 0; l < 8; l++) {
+      unsigned long long v = acc[l];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      if ((G::rank() & 31) == 0 && v) atomicAdd(&cnt[l], v);
+    }
+    G::sync();
+    int l = 0;
+    while (l < 7 && cnt[l] < (unsigned long long)mfloor) l++;
+    const bool use = cnt[l] >= (unsigned long long)mfloor;
+    const double piv = r1 * (1.0 + 0.41421356237309515 * (double)(l + 1) * 0.125);
+    G::sync();
+    if (use) {
+      int out = 0;
+      for (int base = 0; base < pos; base += NT) {
+        const int i = base + G::rank();
+        double d = 0.0;
+        int32_t bb = 0;
+        bool keep = false;
+        if (i < pos) {
+          d = ws.d[i];
+          bb = ws.b[i];
+          keep = d <= piv;
+        }
+        long long kt;
+        const int ex = (int)G::excl_scan(keep ? 1 : 0, kt, ws.scr);
+        if (keep) {
+          ws.d[out + ex] = d;
+          ws.b[out + ex] = bb;
+        }
+        out += (int)kt;
+      }
+      G::sync();
+      pos = out;
+    }
+  }
   EMU_PHASE(3);
   EMU_STAT(9, pos);
   // ---- 4. order
@@ -719,6 +823,94 @@ __device__ int warp_enumerate(const DevTable& T, int32_t t, int32_t c, const Key
   const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
   if (kw.cap <= 0) return 0;
   if (kw.cap > ws.cap) return -1;
+  const int32_t nrows = kw.i1 - kw.i0 + 1, ncols = kw.j1 - kw.j0 + 1;
+  if (ncols * 16 < nrows) {
+    // Tall, narrow windows (sparse long-context tables: windows thousands of
+    // tt rows tall, a few conc columns wide): per column, binary-search the
+    // window's tt range in the column index, then take the candidates
+    // lane-parallel.  Candidate order is irrelevant: the sort breaks distance
+    // ties on the bucket index.
+    const int32_t tlo = T.tt_lo + kw.i0, thi = T.tt_lo + kw.i1;
+    int pos = 0;
+    for (int32_t cbase = kw.j0; cbase <= kw.j1; cbase += 32) {
+      const int32_t j = cbase + lane;
+      int32_t lo = 0, cnt = 0;
+      if (j <= kw.j1) {
+        const int32_t s0 = T.col_start[j], s1 = T.col_start[j + 1];
+        lo = (int32_t)lower_bound_i32(T.col_tt, s0, s1, tlo);
+        cnt = (int32_t)upper_bound_i32(T.col_tt, lo, s1, thi) - lo;
+      }
+      int x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      const int tot = __shfl_sync(kFull, x, 31);
+      ws.rows[lane] = lo;
+      ws.rows[32 + lane] = x - cnt;
+      __syncwarp();
+      const int ncol = min(32, kw.j1 - cbase + 1);
+      for (int kb = 0; kb < tot; kb += 32) {
+        const int k = kb + lane;
+        bool in = false;
+        double d = 0.0;
+        int32_t b = 0;
+        if (k < tot) {
+          int l0 = 0, h0 = ncol;  // last column whose prefix <= k
+          while (h0 - l0 > 1) {
+            const int mid = (l0 + h0) >> 1;
+            if (ws.rows[32 + mid] <= k)
+              l0 = mid;
+            else
+              h0 = mid;
+          }
+          const int32_t idx = ws.rows[l0] + (k - ws.rows[32 + l0]);
+          b = T.col_b[idx];
+          d = __dsqrt_rn(__dadd_rn(sq_delta((int64_t)t - T.col_tt[idx], span_t, T.sq_t, T.lt),
+                                   sq_delta((int64_t)c - (T.c_lo + cbase + l0), span_c, T.sq_c, T.lc)));
+          in = d <= kw.dmax;
+        }
+        const unsigned m = __ballot_sync(kFull, in);
+        if (in) {
+          ws.d[pos + __popc(m & lt)] = d;
+          ws.b[pos + __popc(m & lt)] = b;
+        }
+        pos += __popc(m);
+      }
+      __syncwarp();
+    }
+    return pos;
+  }
+  {
+    // Sparse rows: scan the window's tt slab -- contiguous in bucket order --
+    // when it holds fewer buckets than the window has rows.
+    const int32_t b0 = T.rowbase[kw.i0], b1 = T.rowbase[kw.i1 + 1];
+    if (b1 - b0 <= nrows) {
+      const int32_t clo = T.c_lo + kw.j0, chi = T.c_lo + kw.j1;
+      int pos = 0;
+      for (int32_t base = b0; base < b1; base += 32) {
+        const int32_t b = base + lane;
+        bool in = false;
+        double d = 0.0;
+        if (b < b1) {
+          const int32_t bc = T.bkt_conc[b];
+          if (bc >= clo && bc <= chi) {
+            d = dist_tab(T, (int64_t)t - T.bkt_tt[b], (int64_t)c - bc, span_t, span_c);
+            in = d <= kw.dmax;
+          }
+        }
+        const unsigned m = __ballot_sync(kFull, in);
+        if (in) {
+          ws.d[pos + __popc(m & lt)] = d;
+          ws.b[pos + __popc(m & lt)] = b;
+        }
+        pos += __popc(m);
+      }
+      __syncwarp();
+      return pos;
+    }
+  }
   const int32_t w0 = kw.j0 >> 5, w1 = kw.j1 >> 5;
   int pos = 0;
   for (int32_t rbase = kw.i0; rbase <= kw.i1; rbase += 32) {

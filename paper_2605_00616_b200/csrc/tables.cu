@@ -44,6 +44,9 @@ void TableBuf::release() {
   cudaFree(bmap);
   cudaFree(wpre);
   cudaFree(rowbase);
+  cudaFree(col_start);
+  cudaFree(col_tt);
+  cudaFree(col_b);
   cudaFree(sq_t);
   cudaFree(sq_c);
   *this = TableBuf();
@@ -72,6 +75,9 @@ DevTable TableBuf::view() const {
   t.wpre = wpre;
   t.rowbase = rowbase;
   t.wpr = wpr;
+  t.col_start = col_start;
+  t.col_tt = col_tt;
+  t.col_b = col_b;
   t.sq_t = sq_t;
   t.sq_c = sq_c;
   t.lt = lt;
@@ -135,6 +141,25 @@ int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, c
       acc += __builtin_popcount(bm[(size_t)(i * wpr + k)]);
     }
   }
+  // column index: buckets by (conc, tt) (counting sort on conc; tt ascending
+  // within a column because buckets are already in (tt, conc) order)
+  std::vector<int32_t> cstart((size_t)gnc + 1, 0), ctt((size_t)tb.nb), cb((size_t)tb.nb);
+  for (int64_t b = 0; b < tb.nb; b++) cstart[(size_t)(h_cc[b] - tb.c_lo) + 1]++;
+  for (int64_t j = 0; j < gnc; j++) cstart[(size_t)j + 1] += cstart[(size_t)j];
+  {
+    std::vector<int32_t> fill(cstart.begin(), cstart.end() - 1);
+    for (int64_t b = 0; b < tb.nb; b++) {
+      const int32_t k = fill[(size_t)(h_cc[b] - tb.c_lo)]++;
+      ctt[(size_t)k] = h_tt[b];
+      cb[(size_t)k] = (int32_t)b;
+    }
+  }
+  EMU_CUDA(cudaMalloc((void**)&tb.col_start, 4 * (gnc + 1)));
+  EMU_CUDA(cudaMalloc((void**)&tb.col_tt, 4 * std::max<int64_t>(1, tb.nb)));
+  EMU_CUDA(cudaMalloc((void**)&tb.col_b, 4 * std::max<int64_t>(1, tb.nb)));
+  EMU_CUDA(cudaMemcpyAsync(tb.col_start, cstart.data(), 4 * (gnc + 1), cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.col_tt, ctt.data(), 4 * tb.nb, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemcpyAsync(tb.col_b, cb.data(), 4 * tb.nb, cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMalloc((void**)&tb.bsat, 4 * cells));
   EMU_CUDA(cudaMalloc((void**)&tb.ssat, 4 * cells));
   EMU_CUDA(cudaMalloc((void**)&tb.bmap, 4 * gnt * wpr));

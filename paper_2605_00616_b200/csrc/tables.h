@@ -20,6 +20,9 @@ struct TableBuf {
   int32_t* wpre = nullptr;
   int32_t* rowbase = nullptr;
   int32_t wpr = 0;
+  int32_t* col_start = nullptr;  // [gnc+1]: buckets of conc index j are col_*[col_start[j] .. col_start[j+1])
+  int32_t* col_tt = nullptr;     // [nb] tt of those buckets, ascending
+  int32_t* col_b = nullptr;      // [nb] their bucket index
   double* sq_t = nullptr;
   double* sq_c = nullptr;
   int64_t lt = 0, lc = 0;

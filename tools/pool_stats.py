@@ -7,11 +7,12 @@ import numpy as np, torch
 from paper_2605_00616_b200 import LatencyOracle, OracleConfig, _lib
 from paper_2605_00616_b200.device import DeviceTables
 from paper_2605_00616_b200.profile import pack_from_device
-from paper_2605_00616_b200.workloads import queries_llama, records_llama
+from paper_2605_00616_b200.workloads import queries_llama, records_llama, queries_sparse, records_sparse
 floor = int(os.environ.get("FLOOR", 32))
-tables = DeviceTables.build(*records_llama(1_000_000, 0), canonical=True)
+sparse = os.environ.get('WORK') == 'sparse'
+tables = DeviceTables.build(*(records_sparse if sparse else records_llama)(1_000_000, 0), canonical=True)
 orc = LatencyOracle(pack_from_device(tables, 1000, keep_host=False), OracleConfig(reliability_floor=floor), _validate=False)
-qt, qc, qp = (torch.as_tensor(a, device="cuda") for a in queries_llama(10_000_000, 1))
+qt, qc, qp = (torch.as_tensor(a, device="cuda") for a in (queries_sparse if sparse else queries_llama)(int(os.environ.get('Q', 10_000_000)), 1))
 lib = _lib.lib(); lib.emu_stats_read.argtypes = [ctypes.c_void_p]
 buf = np.zeros(32, np.uint64)
 orc.flush(); orc.sample_batch(qt, qc, qp, rng="philox"); torch.cuda.synchronize()
