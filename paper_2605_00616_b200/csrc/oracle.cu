@@ -35,7 +35,10 @@ enum : int { FLAG_ARENA = 1, FLAG_HASH = 2, FLAG_MISSING = 4 };
 constexpr int kWarpCap = 256;  // candidates per warp workspace
 constexpr int kWarpsPerCta = 4;
 constexpr int kWarpThreads = 32 * kWarpsPerCta;
-constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 128 * 4 + kWarpCap * 4;  // d,b,scr,dsh,rows,n,o
+constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 32 * 4 + kWarpCap * 4;  // d,b,scr,dsh,rows,n,o
+#ifndef EMU_WARP_MINB
+#define EMU_WARP_MINB 8  // 64 registers: 8 CTAs x 4 warps per SM (smem 4.9 KB per warp)
+#endif
 constexpr int kWarpGrid = kNumSMs * 8;
 constexpr int kCtaThreads = 256;
 constexpr int kCtaCap = 8192;  // candidates in shared memory per CTA
@@ -279,7 +282,7 @@ __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t*
 // Shepard CDF; keys without a fast-path window run the full in-warp search,
 // and windows too large for a warp are escalated to k_pool_cta.
 template <int MODE>
-__global__ void __launch_bounds__(kWarpThreads, 7) k_pool_warp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
+__global__ void __launch_bounds__(kWarpThreads, EMU_WARP_MINB) k_pool_warp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
                                                             const KeyWin* kw, const long long* resv, int* work,
                                                             int* esc_list, int* esc_count) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(kWarpThreads, 7) k_pool_warp(DevTable P0, DevT
   ws.scr = (long long*)(base + kWarpCap * 12);
   ws.dsh = (double*)(base + kWarpCap * 12 + 40 * 8);
   ws.rows = (int32_t*)(base + kWarpCap * 12 + 40 * 8 + 10 * 8);
-  ws.n = (int32_t*)(base + kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 128 * 4);
+  ws.n = (int32_t*)(base + kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 32 * 4);
   ws.o = ws.n + kWarpCap / 2;
   ws.ncache = kWarpCap / 2;
   ws.cap = kWarpCap;
