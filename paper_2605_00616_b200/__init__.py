@@ -27,10 +27,13 @@ from .profile import (
     TableKind,
     build_pack,
     build_pack_arrays,
+    build_pack_from_traces,
     iter_trace_dir,
     load_pack,
     load_pack_file,
+    parse_trace_arrays,
     parse_trace_line,
+    read_trace_arrays,
     read_trace_file,
     save_pack,
     save_pack_file,
@@ -54,12 +57,15 @@ __all__ = [
     "TableKind",
     "build_pack",
     "build_pack_arrays",
+    "build_pack_from_traces",
     "iter_trace_dir",
     "load_pack",
     "load_pack_file",
     "normalized_distance",
+    "parse_trace_arrays",
     "parse_trace_line",
     "pool_neighbors",
+    "read_trace_arrays",
     "read_trace_file",
     "sample_latency",
     "save_pack",

@@ -71,6 +71,30 @@ def test_gpu_build_large_matches_oracle(canonical):
         assert soa_equal(g, w)
 
 
+def test_trace_files_to_gpu_pack(tmp_path):
+    """Reference-written JSONL (tests/golden/codec_trace.jsonl) -> native ingest ->
+    GPU build == the C restatement of build_pack over the same records."""
+    import json as _json
+    import os as _os
+
+    from conftest import ROOT
+    from paper_2605_00616_b200.profile import build_pack_from_traces
+
+    src = _os.path.join(ROOT, "tests", "golden", "codec_trace.jsonl")
+    lines = open(src).read().splitlines()
+    half = len(lines) // 2
+    (tmp_path / "a.jsonl").write_text("\n".join(lines[:half]) + "\n")
+    (tmp_path / "b.jsonl").write_text("\n\n".join(lines[half:]) + "\n")
+    pack = build_pack_from_traces([tmp_path / "a.jsonl", tmp_path / "b.jsonl"], 77)
+    want = _json.load(open(_os.path.join(ROOT, "tests", "golden", "codec_expect.json")))["trace"]
+    lat = np.frombuffer(bytes.fromhex(want["latency_hex"]), dtype="<f8")
+    ph = np.array([0 if p == "decode" else 1 for p in want["phase"]], np.uint8)
+    tabs = O.build(np.array(want["tt"], np.int32), np.array(want["conc"], np.int32), ph, lat, canonical=True)
+    for g, w in zip(pack.soas(), tabs):
+        assert soa_equal(g, w)
+    assert pack.num_gpu_blocks == 77
+
+
 def test_gpu_build_edge_cases():
     # empty input
     pack = build_pack_arrays(np.zeros(0), np.zeros(0), np.zeros(0), np.zeros(0), 5)
