@@ -149,34 +149,45 @@ def c3(args):
 
 
 def c4(args):
+    from paper_2605_00616_b200.capture import records_device
+
     n = args.records_c4
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    parts = [records_llama(n // 10, 100 + k) for k in range(10)]
-    cols = [np.concatenate([p[i] for p in parts]) for i in range(4)]
+    dev = list(records_device(n, seed=100))  # generator G + ground-truth latencies on the device
+    torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
-    dev = [torch.as_tensor(c, device="cuda") for c in cols]
+    m = 2_000_000
+    cols = [d[:m].cpu().numpy() for d in dev]
 
     def build():
         t = DeviceTables.build(*dev, canonical=True)
         del t
 
     ms = timed(build, max(1, args.steps // 3), warmup=1)
+    _lib.profile_enable(True)
     t = DeviceTables.build(*dev, canonical=True)
     nb = sum(t.info(i)["n_buckets"] for i in range(3))
+    sc_ms, passes = _lib.profile_read("radix_scatter")
+    up_ms, _ = _lib.profile_read("radix_up")
+    scan_ms, _ = _lib.profile_read("scan")
+    _lib.profile_enable(False)
     del t
     algo_bytes = 33 * n + 48 * nb / 3
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-    m = 2_000_000
     t0 = time.perf_counter()
-    O.build(cols[0][:m], cols[1][:m], cols[2][:m], cols[3][:m], canonical=True)
+    O.build(cols[0], cols[1], cols[2], cols[3], canonical=True)
     cpu = m / (time.perf_counter() - t0)
     return {"config": "c4", "workload": f"{n} synthetic records (generator G), canonical 3-table build",
             "ms_per_build": ms, "records_per_s": n / (ms / 1e3), "buckets_total": nb,
             "roofline": {"bound": "hbm", "achieved": algo_bytes / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": algo_bytes / (ms / 1e3) / 1e9 / peak,
                          "bytes": "33 B/record + 48 B/bucket (SURVEY 8d); multi-pass sort moves more"},
-            "host_generation_s": gen_s,
+            "device_generation_s": gen_s,
+            "radix_sort": {"passes": passes, "scatter_ms": sc_ms, "upsweep_ms": up_ms, "scan_ms": scan_ms,
+                           "scatter_GBps": 40 * n * passes / (sc_ms / 1e3) / 1e9,
+                           "note": "each pass reads key 8 B + (hi, lo) 16 B and writes 16 B per record"},
             "cpu_baseline": {"value": cpu, "unit": "records/s", "cores": 1, "kind": "port",
                              "sample": f"oracle qsort build of the first {m} records"}}
 

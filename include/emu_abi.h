@@ -211,6 +211,26 @@ int emu_token_fill(const uint8_t* is_prefill, const int32_t* chunk, const int32_
                    const int32_t* prompt_len, const int32_t* generated, const int32_t* target_len,
                    int64_t n, int32_t* out_ids, uint8_t* out_finished, void* stream);
 
+/* ------------------------------------------------------ capture stand-ins --
+ * emu_ground_truth: ground_truth_latency (engine.py:128-147) for n step keys
+ *   ([dev] columns): m * (base + per_token*tt + per_seq*conc) * (1 + g) with
+ *   m = prefill_multiplier for mixed steps and g ~ N(0, noise_cv) redrawn while
+ *   the factor is nonpositive; noise_cv == 0 consumes no randomness.  The
+ *   deterministic part is bit-identical to the reference's expression; the
+ *   deviates are Box-Muller on Philox4x32-10 keyed by (seed, i) (CPython's
+ *   random.gauss stream is not reproduced).  GroundTruthParams.validate's
+ *   checks and messages (engine.py:116-125) -> EMU_ERR_INVALID.
+ * emu_gen_step_keys: n step keys ([dev] outputs) of the synthetic generator G
+ *    from Philox(seed, i): conc = clip(rint(exp(conc_mu +
+ *   conc_sigma z0)), 1, conc_max); decode with probability p_decode (tt = conc);
+ *   else tt = min(tt_max, conc - 1 + clip(rint(exp(chunk_mu + chunk_sigma z1)), 1, tt_max)). */
+int emu_ground_truth(const int32_t* tt, const int32_t* conc, const uint8_t* phase, int64_t n,
+                     double base_s, double per_token_s, double per_seq_s, double prefill_multiplier,
+                     double noise_cv, uint64_t seed, double* out_lat, void* stream);
+int emu_gen_step_keys(int64_t n, uint64_t seed, double conc_mu, double conc_sigma, int32_t conc_max,
+                      double p_decode, double chunk_mu, double chunk_sigma, int32_t tt_max, int32_t* tt,
+                      int32_t* conc, uint8_t* phase, void* stream);
+
 /* --------------------------------------------------------------- codecs --
  * Native readers of the reference's on-disk formats (host-only; no CUDA).
  *

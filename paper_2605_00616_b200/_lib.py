@@ -62,6 +62,9 @@ SIGNATURES = {
     "emu_oracle_stats": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "emu_distance": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "emu_token_fill": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "emu_ground_truth": (c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_u64, c_vp, c_vp]),
+    "emu_gen_step_keys": (c_int, [c_i64, c_u64, c_dbl, c_dbl, c_i32, c_dbl, c_dbl, c_dbl, c_i32, c_vp, c_vp, c_vp,
+                                  c_vp]),
     "emu_pack_parse_json": (c_int, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
     "emu_pack_parsed_info": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_vp,
                                      ctypes.POINTER(c_i64)]),
