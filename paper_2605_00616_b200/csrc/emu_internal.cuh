@@ -294,9 +294,19 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
+// Loads of the draw path; CG = true reads through L2 only (a long-running
+// kernel must not see L1 lines older than the pools other kernels rebuilt).
+template <bool CG, typename T>
+__device__ __forceinline__ T ldp(const T* p) {
+  if (CG) return __ldcg(p);
+  return *p;
+}
+
+template <bool CG = false>
 __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ arena, int64_t start, int64_t K, double u);
 
 // The bucket a draw u selects from a built entry e (> 0).
+template <bool CG = false>
 __device__ __forceinline__ PoolPick pool_pick(const Slot* __restrict__ arena, long long e, double u) {
   const unsigned long long v = (unsigned long long)e;
   if (v & kEntryDirect) {
@@ -305,12 +315,13 @@ __device__ __forceinline__ PoolPick pool_pick(const Slot* __restrict__ arena, lo
     pk.n = (int32_t)(v & 0x7fffffffULL);
     return pk;
   }
-  return pool_draw_slot(arena, (int64_t)(v & 0xffffffffULL), (int64_t)(v >> 32), u);
+  return pool_draw_slot<CG>(arena, (int64_t)(v & 0xffffffffULL), (int64_t)(v >> 32), u);
 }
 
 // searchsorted(cdf, u, 'right') over the pool at arena[start] (K buckets):
 // returns the chosen bucket.  cdf[K-1] == 1.0 > u, so a hit always exists.
 // 32-bit offset arithmetic (K, start < 2^31 units).
+template <bool CG>
 __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ arena, int64_t start64, int64_t K64,
                                                    double u) {
   const int32_t K = (int32_t)K64;
@@ -321,14 +332,14 @@ __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ aren
   if (G > 1) {
     const double* sp = reinterpret_cast<const double*>(P);
     if (G <= 5) {  // <= 4 splits: two 16-byte loads, count splits <= u
-      const double2 a = *reinterpret_cast<const double2*>(sp);
-      const double2 b = G > 3 ? reinterpret_cast<const double2*>(sp)[1] : make_double2(2.0, 2.0);
+      const double2 a = ldp<CG>(reinterpret_cast<const double2*>(sp));
+      const double2 b = G > 3 ? ldp<CG>(reinterpret_cast<const double2*>(sp) + 1) : make_double2(2.0, 2.0);
       g = (a.x <= u) + (G > 2 && a.y <= u) + (b.x <= u) + (G > 4 && b.y <= u);
     } else {
       int32_t lo = 0, hi = G - 1;  // number of splits <= u
       while (lo < hi) {
         const int32_t mid = (lo + hi) >> 1;
-        if (sp[mid] <= u)
+        if (ldp<CG>(sp + mid) <= u)
           lo = mid + 1;
         else
           hi = mid;
@@ -342,11 +353,11 @@ __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ aren
 #pragma unroll
   for (int q = 0; q < kGroupSlots / 2; q++) {
     if (2 * q < n) {
-      const double2 c = C[q];
+      const double2 c = ldp<CG>(C + q);
       j += (c.x <= u) + (2 * q + 1 < n && c.y <= u);
     }
   }
-  const int2 d = reinterpret_cast<const int2*>(P + hs + ((K + 1) >> 1))[g * kGroupSlots + j];
+  const int2 d = ldp<CG>(reinterpret_cast<const int2*>(P + hs + ((K + 1) >> 1)) + g * kGroupSlots + j);
   PoolPick pk;
   pk.soff = d.x;
   pk.n = d.y;

@@ -813,6 +813,86 @@ __global__ void k_step_hit(MapView m, const Slot* __restrict__ arena, const doub
   publish_step(out, (ph ? s1 : s0)[sidx], sidx, 0, seq);
 }
 
+// ------------------------------------------------------------ step server
+// The engine calls the oracle once per step, synchronously (engine.py:555-557),
+// so a kernel launch per call dominates its latency.  The step server is a
+// one-warp kernel that stays resident while steps keep coming: the host writes
+// a request into mapped pinned memory, lane 0 sees it over PCIe, serves it
+// exactly like k_step_hit (cached keys; misses go back to the host, which
+// launches k_step) and writes the result back into mapped memory.  It exits
+// after `idle_ns` without a request (device-wide syncs then wait at most that
+// long) or after `max_ns`; the host relaunches it on demand.  Requests carry a
+// sequence number; a (re)started server first serves any request it has not
+// served yet, so a request written while the server was exiting is never lost.
+struct __align__(16) StepReq {
+  uint32_t seq;
+  int32_t tt, conc, phase;
+};
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_step_server(MapView m, const Slot* __restrict__ arena, const double* __restrict__ s0,
+                              const double* __restrict__ s1, uint64_t* st6, const StepReq* req, StepOut* out,
+                              uint32_t* served_dev, volatile int* alive, uint64_t idle_ns, uint64_t max_ns) {
+  if (threadIdx.x != 0) return;
+  uint32_t served = *(volatile uint32_t*)served_dev;
+  const uint64_t t0 = global_ns();
+  uint64_t t_last = t0;
+  for (;;) {
+    // one 16-byte read over PCIe: the host writes the fields before the
+    // sequence number (x86 store order), so a snapshot with a new seq has them
+    uint32_t sq, ut, uc, up;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(sq), "=r"(ut), "=r"(uc), "=r"(up)
+                 : "l"(req));
+    if (sq != served) {
+      const int32_t t = (int32_t)ut, c = (int32_t)uc, ph = up ? 1 : 0;
+      const int64_t idx = map_find<false>(m, ph, t, c);
+      const long long e = idx >= 0 ? __ldcg(map_entry_ptr(m, idx)) : 0;
+      if (e <= 0) {
+        publish_step(out, 0.0, -1, 8 /* kStepMiss */, sq);
+      } else {
+        Pcg64 g;
+        g.s_hi = __ldcg(st6 + 0);
+        g.s_lo = __ldcg(st6 + 1);
+        g.i_hi = __ldcg(st6 + 2);
+        g.i_lo = __ldcg(st6 + 3);
+        g.has_u32 = (uint32_t)__ldcg(st6 + 4);
+        g.u32 = (uint32_t)__ldcg(st6 + 5);
+        const double u = unit_double(pcg64_next64(g));
+        const PoolPick pk = pool_pick<true>(arena, e, u);
+        uint32_t j = 0;
+        if (pk.n > 1) {
+          const uint32_t w0 = pcg64_next32(g);
+          j = lemire_index((uint32_t)pk.n, w0, [&]() { return pcg64_next32(g); });
+        }
+        const int32_t sidx = pk.soff + (int32_t)j;
+        __stcg(st6 + 0, g.s_hi);
+        __stcg(st6 + 1, g.s_lo);
+        __stcg(st6 + 2, g.i_hi);
+        __stcg(st6 + 3, g.i_lo);
+        __stcg(st6 + 4, (uint64_t)g.has_u32);
+        __stcg(st6 + 5, (uint64_t)g.u32);
+        __threadfence();
+        publish_step(out, __ldcg((ph ? s1 : s0) + sidx), sidx, 0, sq);
+      }
+      served = sq;
+      *(volatile uint32_t*)served_dev = served;
+      t_last = global_ns();
+      continue;
+    }
+    const uint64_t now = global_ns();
+    if (now - t_last > idle_ns || now - t0 > max_ns) break;
+  }
+  __threadfence();
+  *alive = 0;
+  __threadfence_system();
+}
+
 __global__ void k_fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -908,6 +988,17 @@ struct emu_oracle_s {
   // rng / step
   uint64_t* pcg = nullptr;
   StepOut* step_dev = nullptr;   // device alias of step_host (mapped)
+  // step server (k_step_server): mapped request mailbox + liveness flag
+  StepReq* req_host = nullptr;
+  StepReq* req_dev = nullptr;
+  int* alive_host = nullptr;
+  int* alive_dev = nullptr;
+  uint32_t* served_dev = nullptr;
+  cudaStream_t srv_stream = nullptr;
+  cudaEvent_t async_done = nullptr;  // recorded after asynchronous calls (flush)
+  cudaEvent_t srv_done = nullptr;    // recorded after each server launch: completed = not running
+  bool async_pending = false;
+  bool server = true;                // EMU_STEP_SERVER=0 disables
   StepOut* step_host = nullptr;  // pinned, mapped
   uint32_t step_seq = 0;
   int* flags_host = nullptr;
@@ -944,7 +1035,14 @@ static int oracle_flush(emu_oracle_t o, cudaStream_t s) {
   return EMU_OK;
 }
 
+// Wait for the step server to exit (<= its idle timeout) before the arrays it
+// was launched with are reallocated.
+static void quiesce_server(emu_oracle_t o) {
+  if (o->srv_stream) cudaStreamSynchronize(o->srv_stream);
+}
+
 static int alloc_hash(emu_oracle_t o, int64_t hcap) {
+  quiesce_server(o);
   cudaFree(o->map.hkeys);
   cudaFree(o->map.hvals);
   o->map.hkeys = nullptr;
@@ -1026,6 +1124,24 @@ int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, doubl
     return fail(EMU_ERR_CUDA, "cudaHostAlloc failed");
   }
   memset((void*)o->step_host, 0, sizeof(StepOut));
+  {
+    const char* sv = getenv("EMU_STEP_SERVER");
+    o->server = !(sv && sv[0] == '0');
+    if (cudaHostAlloc((void**)&o->req_host, sizeof(StepReq), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&o->req_dev, o->req_host, 0) != cudaSuccess ||
+        cudaHostAlloc((void**)&o->alive_host, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&o->alive_dev, o->alive_host, 0) != cudaSuccess ||
+        cudaMalloc((void**)&o->served_dev, sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(o->served_dev, 0, sizeof(uint32_t)) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&o->srv_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&o->srv_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&o->async_done, cudaEventDisableTiming) != cudaSuccess) {
+      emu_oracle_destroy(o);
+      return fail(EMU_ERR_CUDA, "step server setup failed");
+    }
+    memset((void*)o->req_host, 0, sizeof(StepReq));
+    *o->alive_host = 0;
+  }
   if ((rc = oracle_flush(o, s))) {
     emu_oracle_destroy(o);
     return rc;
@@ -1068,6 +1184,13 @@ void emu_oracle_destroy(emu_oracle_t o) {
   if (o->cp_out) cudaStreamDestroy(o->cp_out);
   cudaFree(o->flag_log);
   if (o->flag_log_host) cudaFreeHost(o->flag_log_host);
+  if (o->srv_stream) cudaStreamSynchronize(o->srv_stream);  // the server exits after its idle timeout
+  if (o->srv_stream) cudaStreamDestroy(o->srv_stream);
+  if (o->srv_done) cudaEventDestroy(o->srv_done);
+  if (o->async_done) cudaEventDestroy(o->async_done);
+  cudaFree(o->served_dev);
+  if (o->req_host) cudaFreeHost(o->req_host);
+  if (o->alive_host) cudaFreeHost(o->alive_host);
   if (o->step_host) cudaFreeHost(o->step_host);
   if (o->flags_host) cudaFreeHost(o->flags_host);
   delete o;
@@ -1075,7 +1198,11 @@ void emu_oracle_destroy(emu_oracle_t o) {
 
 int emu_oracle_flush(emu_oracle_t o, void* stream) {
   if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
-  return oracle_flush(o, as_stream(stream));
+  const int rc = oracle_flush(o, as_stream(stream));
+  if (rc) return rc;
+  EMU_CUDA(cudaEventRecord(o->async_done, as_stream(stream)));  // the step server waits for it
+  o->async_pending = true;
+  return EMU_OK;
 }
 
 int emu_oracle_stats(emu_oracle_t o, int64_t* n_pools, int64_t* n_slots) {
@@ -1174,6 +1301,7 @@ static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s,
     if ((*rc = alloc_hash(o, o->map.hcap * 4))) return -1;
   }
   if ((flags & FLAG_ARENA) && o->arena_cap < o->arena_max) {  // grow the arena before resorting to chunking
+    quiesce_server(o);
     cudaFree(o->arena);
     o->arena = nullptr;
     o->arena_cap = std::min(o->arena_max, o->arena_cap * 4);
@@ -1449,6 +1577,9 @@ int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q
 int emu_oracle_seed_pcg64(emu_oracle_t o, const uint64_t* st6) {
   if (!o || !st6) return fail(EMU_ERR_INVALID, "NULL oracle/state");
   EMU_CUDA(cudaMemcpy(o->pcg, st6, 6 * sizeof(uint64_t), cudaMemcpyDefault));
+  // a pageable-source copy may return before its DMA lands; the step server
+  // (another stream) must see the new state on its next request
+  EMU_CUDA(cudaStreamSynchronize(0));
   return EMU_OK;
 }
 
@@ -1458,13 +1589,67 @@ int emu_oracle_get_pcg64(emu_oracle_t o, uint64_t* st6) {
   return EMU_OK;
 }
 
+static constexpr uint64_t kServerIdleNs = 200000;      // exit after 200 us without a step
+static constexpr uint64_t kServerMaxNs = 2000000000ULL;  // and after 2 s in any case
+
+static int launch_server(emu_oracle_t o) {
+  *(volatile int*)o->alive_host = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  EMU_LAUNCH("step_server", o->srv_stream,
+             k_step_server<<<1, 32, 0, o->srv_stream>>>(o->map, o->arena, o->plane[0].samples, o->plane[1].samples,
+                                                        o->pcg, o->req_dev, o->step_dev, o->served_dev,
+                                                        o->alive_dev, kServerIdleNs, kServerMaxNs));
+  EMU_CUDA(cudaGetLastError());
+  EMU_CUDA(cudaEventRecord(o->srv_done, o->srv_stream));
+  return EMU_OK;
+}
+
+// One step through the resident server: returns the result flags (0 = done,
+// kStepMiss = key not cached), or -1 with an error set.
+static int step_via_server(emu_oracle_t o, int32_t tt, int32_t conc, int ph, double* out_lat) {
+  if (o->async_pending) {  // stream order: pools the server reads must be settled
+    if (cudaEventSynchronize(o->async_done) != cudaSuccess) return -1 + 0 * cuda_fail(cudaGetLastError(), "flush");
+    o->async_pending = false;
+  }
+  volatile StepReq* rq = o->req_host;
+  volatile StepOut* h = o->step_host;
+  const uint32_t seq = ++o->step_seq;
+  rq->tt = tt;
+  rq->conc = conc;
+  rq->phase = ph;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  rq->seq = seq;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  if (!*(volatile int*)o->alive_host && cudaEventQuery(o->srv_done) != cudaErrorNotReady) {
+    if (launch_server(o)) return -1;
+  }
+  for (uint64_t spin = 1; h->seq != seq; spin++) {
+    if ((spin & 1023) == 0) {
+      const cudaError_t e = cudaEventQuery(o->srv_done);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return -1 + 0 * cuda_fail(e, "k_step_server");
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      if (e == cudaSuccess && h->seq != seq && launch_server(o)) return -1;  // exited before our request
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  const int f = h->flags;
+  if (f == 0) *out_lat = h->lat;
+  return f;
+}
+
 int emu_oracle_step(emu_oracle_t o, int32_t tt, int32_t conc, int32_t phase, double* out_lat) {
   if (!o || !out_lat) return fail(EMU_ERR_INVALID, "NULL oracle/out");
   if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
   const int ph = phase ? 1 : 0;
   cudaStream_t s = 0;
   volatile StepOut* h = o->step_host;
-  bool full = false;  // first try the cached-key kernel
+  bool full = false;  // first try the cached-key path (resident server, else k_step_hit)
+  if (o->server) {
+    const int f = step_via_server(o, tt, conc, ph, out_lat);
+    if (f < 0) return EMU_ERR_CUDA;
+    if (f == 0) return EMU_OK;
+    full = true;  // kStepMiss: build the pool with k_step below
+  }
   for (int attempt = 0; attempt < 5; attempt++) {
     const uint32_t seq = ++o->step_seq;
     if (!full) {

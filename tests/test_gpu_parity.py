@@ -322,6 +322,32 @@ def test_config2_pools_match_oracle():
         assert np.array_equal(g, w)
 
 
+def test_step_server_matches_launch_path(c1_pack, c1_trace, monkeypatch):
+    """The resident step server (k_step_server) continues the same PCG64 stream
+    as the per-call kernel path across idle-timeout exits and relaunches,
+    flushes, batched PCG64 draws and re-seeding in between."""
+    import time as _time
+
+    keys = list(zip(c1_trace["tt"][:600].tolist(), c1_trace["conc"][:600].tolist(), c1_trace["phase"][:600].tolist()))
+    seqs = []
+    for server in ("1", "0"):
+        monkeypatch.setenv("EMU_STEP_SERVER", server)
+        orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32, rng_seed=5))
+        out = [orc(*k) for k in keys[:200]]
+        _time.sleep(0.002)  # > idle timeout: the server exits, the next call relaunches it
+        out += [orc(*k) for k in keys[200:300]]
+        orc.flush()
+        out += [orc(*k) for k in keys[300:400]]
+        lat, _ = orc.sample_batch(c1_trace["tt"][:500], c1_trace["conc"][:500], c1_trace["phase"][:500],
+                                  rng="pcg64")
+        out += lat.tolist()
+        orc.set_rng_state(np.random.default_rng(77).bit_generator.state)
+        out += [orc(*k) for k in keys[400:600]]
+        seqs.append(np.array(out))
+        del orc
+    assert np.array_equal(seqs[0], seqs[1])
+
+
 def test_small_arena_forces_flush_and_retry(c1_pack):
     tabs = to_oracle_tables(c1_pack)
     qt, qc, qp = queries_llama(50_000, 21)
