@@ -65,6 +65,9 @@ def _check(rc: int) -> None:
     _lib.check(rc, no_data_exc=NoProfileDataError)
 
 
+_PHASE_MEMO: dict = {}  # phase object -> code, for the per-step call
+
+
 def _i32(v: int, what: str) -> int:
     v = int(v)
     if not _I32_MIN < v <= _I32_MAX:
@@ -262,7 +265,14 @@ class LatencyOracle:
     # -- reference surface ------------------------------------------------------------
     def sample(self, tt: int, conc: int, phase) -> float:
         """One draw on this oracle's stream (oracle.py:224-226)."""
-        rc = self._step(self._h, _i32(tt, "tt"), _i32(conc, "conc"), phase_code(phase), self._step_out_ref)
+        ph = _PHASE_MEMO.get(phase) if phase.__hash__ is not None else None
+        if ph is None:
+            ph = phase_code(phase)
+            if phase.__hash__ is not None and len(_PHASE_MEMO) < 64:
+                _PHASE_MEMO[phase] = ph
+        if not (type(tt) is int and type(conc) is int and _I32_MIN < tt <= _I32_MAX and _I32_MIN < conc <= _I32_MAX):
+            tt, conc = _i32(tt, "tt"), _i32(conc, "conc")
+        rc = self._step(self._h, tt, conc, ph, self._step_out_ref)
         if rc:
             _check(rc)
         return self._step_out.value
