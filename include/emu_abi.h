@@ -50,6 +50,7 @@ extern "C" {
 typedef struct emu_tables_s* emu_tables_t;
 typedef struct emu_oracle_s* emu_oracle_t;
 typedef struct emu_pack_parsed_s* emu_pack_parsed_t;
+typedef struct emu_sched_s* emu_sched_t;
 
 /* One phase table in canonical SoA form: buckets sorted by (tt, conc),
  * bkt_off[n_buckets+1] are offsets into samples[n_samples] (bucket b owns
@@ -188,6 +189,11 @@ int emu_oracle_seed_pcg64(emu_oracle_t o, const uint64_t* pcg_state6);
 int emu_oracle_get_pcg64(emu_oracle_t o, uint64_t* pcg_state6);
 int emu_oracle_step(emu_oracle_t o, int32_t tt, int32_t conc, int32_t phase, double* out_lat);
 
+/* Build (without drawing) the pools of n keys [dev] not cached yet -- the
+ * warm-up half of emu_oracle_sample (the lazy cache of _pooled, oracle.py:200-222). */
+int emu_oracle_prefetch(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc,
+                        const uint8_t* q_phase, int64_t n, void* stream);
+
 /* Cache statistics: number of cached pools and arena slots in use. */
 int emu_oracle_stats(emu_oracle_t o, int64_t* n_pools, int64_t* n_slots);
 
@@ -230,6 +236,39 @@ int emu_ground_truth(const int32_t* tt, const int32_t* conc, const uint8_t* phas
 int emu_gen_step_keys(int64_t n, uint64_t seed, double conc_mu, double conc_sigma, int32_t conc_max,
                       double p_decode, double chunk_mu, double chunk_sigma, int32_t tt_max, int32_t* tt,
                       int32_t* conc, uint8_t* phase, void* stream);
+
+/* ------------------------------------------------------------ scheduler --
+ * The reference scheduler in virtual time for S independent scenarios, one
+ * GPU thread each (EmulatorEngine.admit / _schedule_step / _apply_outcome /
+ * release_blocks, engine.py:323-483, driven like the reference's virtual-time
+ * runs: admit arrivals <= t, schedule, latency, apply, t += latency).
+ * emu_sched_create: scenario s owns requests [req_off[s], req_off[s+1]) of the
+ *   concatenated host arrays prompt/target (int32) and arrival offsets (f64,
+ *   ascending); one EngineConfig for all; at most max_steps steps each.
+ *   EngineConfig.validate and admit's checks -> EMU_ERR_INVALID with the
+ *   reference's messages.
+ * emu_sched_run_replay      : step latencies from lat[S * max_steps] (parity replay);
+ * emu_sched_run_ground_truth: ground_truth_latency with Philox(seed, s, step) noise;
+ * emu_sched_run_oracle      : the oracle in the closed loop: scenario s draws from
+ *   its own numpy PCG64 stream (pcg_states[6 s .. 6 s + 5], as in
+ *   emu_oracle_sample_pcg64) exactly like LatencyOracle.sample; a step whose key
+ *   has no pool pauses the scenario, the host builds the pools of all paused
+ *   scenarios (emu_oracle_prefetch) and relaunches (*rounds = launches).
+ * emu_sched_results: per scenario n_steps and status (1 done, 3 invariant
+ *   error), per step [S * max_steps]: tt, conc, phase, latency, tokens emitted,
+ *   requests finished, cumulative preemptions (host outputs; NULL skips). */
+int emu_sched_create(int32_t S, const int64_t* req_off, const int32_t* prompt, const int32_t* target,
+                     const double* arrival, int32_t num_gpu_blocks, int32_t block_size,
+                     int32_t max_model_len, int32_t max_num_batched_tokens, int32_t max_num_seqs,
+                     int64_t max_steps, emu_sched_t* out);
+int emu_sched_run_replay(emu_sched_t sc, const double* lat, void* stream);
+int emu_sched_run_ground_truth(emu_sched_t sc, double base_s, double per_token_s, double per_seq_s,
+                               double prefill_multiplier, double noise_cv, uint64_t seed, void* stream);
+int emu_sched_run_oracle(emu_sched_t sc, emu_oracle_t o, const uint64_t* pcg_states, int64_t* rounds,
+                         void* stream);
+int emu_sched_results(emu_sched_t sc, int64_t* n_steps, int32_t* status, int32_t* tt, int32_t* conc,
+                      uint8_t* phase, double* lat, int32_t* tokens, int32_t* finished, int64_t* preempt);
+void emu_sched_destroy(emu_sched_t sc);
 
 /* --------------------------------------------------------------- codecs --
  * Native readers of the reference's on-disk formats (host-only; no CUDA).

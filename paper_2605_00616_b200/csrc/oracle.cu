@@ -1035,6 +1035,18 @@ static int oracle_flush(emu_oracle_t o, cudaStream_t s) {
   return EMU_OK;
 }
 
+namespace emu {
+int oracle_views(emu_oracle_t o, MapView* m, const Slot** arena, const double** s0, const double** s1) {
+  if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
+  if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
+  *m = o->map;
+  *arena = o->arena;
+  *s0 = o->plane[0].samples;
+  *s1 = o->plane[1].samples;
+  return EMU_OK;
+}
+}  // namespace emu
+
 // Wait for the step server to exit (<= its idle timeout) before the arrays it
 // was launched with are reallocated.
 static void quiesce_server(emu_oracle_t o) {
@@ -1572,6 +1584,27 @@ int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q
   if (out_sidx) EMU_CUDA(cudaMemcpyAsync(out_sidx + a, d_si + a, 4 * n, cudaMemcpyDefault, s));
   EMU_CUDA(cudaStreamSynchronize(s));
   return EMU_OK;
+}
+
+// Build (without drawing) the pools of n keys [dev] that are not cached yet:
+// the warm-up half of emu_oracle_sample, used by the closed-loop scheduler.
+int emu_oracle_prefetch(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc, const uint8_t* q_phase, int64_t n,
+                        void* stream) {
+  if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
+  if (n < 0) return fail(EMU_ERR_INVALID, "negative key count");
+  if (n == 0) return EMU_OK;
+  if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
+  cudaStream_t s = as_stream(stream);
+  for (int attempt = 0; attempt < 16; attempt++) {
+    int rc = build_missing(o, q_tt, q_conc, q_phase, n, s);
+    if (rc) return rc;
+    int flags = 0;
+    if ((rc = read_flags(o, s, &flags))) return rc;
+    if (!(flags & (FLAG_ARENA | FLAG_HASH))) return EMU_OK;
+    recover(o, flags, n, s, &rc);
+    if (rc) return rc;
+  }
+  return fail(EMU_ERR_CAPACITY, "oracle could not place the pools of the pending keys");
 }
 
 int emu_oracle_seed_pcg64(emu_oracle_t o, const uint64_t* st6) {

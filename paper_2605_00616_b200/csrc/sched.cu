@@ -1,0 +1,669 @@
+// sched.cu -- the reference scheduler in virtual time, one scenario per thread
+// (the caller of the oracle that turns what-if scenarios
+// into step-key streams).
+//
+// Restates EmulatorEngine._schedule_step / _apply_outcome / admit /
+// release_blocks (engine.py:310-483) and the virtual-time driver of the
+// reference's capture / acceptance runs: admit every request whose arrival
+// offset is <= t, schedule a step, take its latency, apply the outcome,
+// t += latency; an empty schedule jumps t to the next arrival.  Exact
+// semantics kept: decode entries first over a snapshot of the running list,
+// then prefills (running partial prefills, then the waiting queue in id order,
+// both snapshotted before the pass), KV blocks reserved per step, make_room
+// preempting the newest running request (which drops its entry and refunds its
+// budget), FIFO admission that never preempts and stops at the first request
+// that does not fit, and the completing prefill reserving its first output
+// token.
+//
+// Latency sources: MODE 0 replays recorded latencies (parity with a recorded
+// reference run); MODE 1 is ground_truth_latency with Philox noise (a capture
+// stand-in); MODE 2 is the oracle itself in the closed loop -- each scenario
+// owns a numpy PCG64 stream and draws exactly like LatencyOracle.sample; a step
+// whose key has no pool yet pauses the scenario (the host builds the pools of
+// all paused scenarios with the batched pool path and relaunches).
+//
+// The waiting queue is a bitmap over request ids (ids are arrival order, the
+// queue is id-ordered); requests preempted after the candidate snapshot carry
+// a later event stamp and are skipped, as the reference's list snapshot does.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "emu_internal.cuh"
+#include "prof.h"
+
+namespace emu {
+
+enum : uint8_t { RQ_WAITING = 0, RQ_PREFILLING = 1, RQ_DECODING = 2, RQ_PREEMPTED = 3, RQ_FINISHED = 4 };
+enum : int32_t { SC_RUNNING = 0, SC_DONE = 1, SC_PAUSED = 2, SC_ERROR = 3 };
+
+struct SchedArgs {
+  int32_t num_blocks, block_size, max_batched, max_seqs;
+  int64_t max_steps;
+  int32_t S;
+  // requests (per scenario slice [roff[s], roff[s+1]))
+  const int64_t* roff;
+  const int32_t* prompt;
+  const int32_t* target;
+  const double* arrival;
+  int32_t* progress;
+  int32_t* generated;
+  int32_t* alloc;
+  uint8_t* rphase;
+  int32_t* eidx;
+  int32_t* pevt;
+  int32_t* running;  // slice of R_s
+  int32_t* snap;     // slice of R_s
+  uint32_t* wbits;   // slice [woff[s], woff[s+1])
+  const int64_t* woff;
+  // per-step entries [S * max_seqs]
+  int32_t* ent_id;
+  int32_t* ent_chunk;
+  uint8_t* ent_pre;
+  // scalar state [S]
+  double* t;
+  int32_t* next_arr;
+  int32_t* nrun;
+  int32_t* wfront;
+  int32_t* free_blocks;
+  int64_t* nsteps;
+  int32_t* evt;
+  int64_t* preempt;
+  int32_t* status;
+  int32_t* n_ent;
+  int32_t* resume;
+  int32_t* key;  // [S * 3] pending / current key (tt, conc, phase)
+  uint64_t* pcg;  // [S * 6]
+  // outputs [S * max_steps]
+  int32_t* o_tt;
+  int32_t* o_conc;
+  uint8_t* o_ph;
+  double* o_lat;
+  int32_t* o_tok;
+  int32_t* o_fin;
+  int64_t* o_pre;
+  // latency sources
+  const double* lat_in;  // MODE 0: [S * max_steps]
+  double gt_base, gt_tok, gt_seq, gt_mult, gt_cv;
+  uint64_t seed;
+  MapView map;  // MODE 2
+  const Slot* arena;
+  const double* s0;
+  const double* s1;
+};
+
+struct Scen {
+  const SchedArgs& A;
+  int32_t s;
+  int64_t r0;  // first request (global index)
+  int32_t R;
+  int32_t* run;
+  int32_t* snp;
+  uint32_t* wb;
+  int32_t* eid;
+  int32_t* ech;
+  uint8_t* epr;
+  int32_t nrun, wfront, freeb, evt, ne, budget;
+  int64_t npre;
+  bool err;
+
+  __device__ int32_t blocks_needed(int64_t tokens) const {
+    return (int32_t)((tokens + A.block_size - 1) / A.block_size);
+  }
+  __device__ void wait_insert(int32_t r) {
+    wb[r >> 5] |= 1u << (r & 31);
+    if (r < wfront) wfront = r;
+  }
+  __device__ void wait_remove(int32_t r) { wb[r >> 5] &= ~(1u << (r & 31)); }
+  // next waiting id >= r (or R)
+  __device__ int32_t wait_next(int32_t r) const {
+    int32_t w = r >> 5;
+    const int32_t nw = (R + 31) >> 5;
+    if (w >= nw) return R;
+    uint32_t m = wb[w] & (0xffffffffu << (r & 31));
+    while (!m) {
+      if (++w >= nw) return R;
+      m = wb[w];
+    }
+    return w * 32 + __ffs(m) - 1;
+  }
+  __device__ void release(int32_t r) {
+    const int64_t g = r0 + r;
+    if (A.alloc[g] == 0) err = true;  // EngineInvariantError: double free
+    freeb += A.alloc[g];
+    A.alloc[g] = 0;
+  }
+  __device__ void add_entry(int32_t r, int32_t chunk, bool pre) {
+    eid[ne] = r;
+    ech[ne] = chunk;
+    epr[ne] = pre ? 1 : 0;
+    A.eidx[r0 + r] = ne;
+    ne++;
+  }
+  __device__ int32_t preempt_newest() {
+    const int32_t v = run[--nrun];
+    const int64_t g = r0 + v;
+    A.rphase[g] = RQ_PREEMPTED;
+    release(v);
+    A.progress[g] = 0;
+    wait_insert(v);
+    A.pevt[g] = ++evt;
+    npre++;
+    const int32_t k = A.eidx[g];
+    if (k >= 0) {  // drop its entry (order kept) and refund its budget
+      budget += ech[k];
+      for (int32_t q = k + 1; q < ne; q++) {
+        eid[q - 1] = eid[q];
+        ech[q - 1] = ech[q];
+        epr[q - 1] = epr[q];
+        A.eidx[r0 + eid[q - 1]] = q - 1;
+      }
+      ne--;
+      A.eidx[g] = -1;
+    }
+    return v;
+  }
+  __device__ bool make_room(int32_t demand, int32_t requester) {
+    while (freeb < demand)
+      if (preempt_newest() == requester) return false;
+    return true;
+  }
+  // one prefill candidate; returns false to stop the pass (reference `break`)
+  __device__ bool prefill_candidate(int32_t r) {
+    if (budget < 1 || ne >= A.max_seqs) return false;
+    const int64_t g = r0 + r;
+    const uint8_t ph = A.rphase[g];
+    if (ph != RQ_PREFILLING && ph != RQ_WAITING && ph != RQ_PREEMPTED) return true;
+    const int32_t prog = A.progress[g], pl = A.prompt[g];
+    const int32_t chunk = min(pl - prog, budget);
+    const bool completing = prog + chunk == pl;
+    const int64_t new_total = (int64_t)prog + chunk + A.generated[g] + (completing ? 1 : 0);
+    const int32_t demand = blocks_needed(new_total) - A.alloc[g];
+    if (ph == RQ_PREFILLING) {
+      if (demand > 0 && !make_room(demand, r)) return true;
+    } else {
+      if (demand > freeb) return false;
+      wait_remove(r);
+      run[nrun++] = r;
+      A.rphase[g] = RQ_PREFILLING;
+    }
+    if (demand > 0) {
+      freeb -= demand;
+      A.alloc[g] += demand;
+    }
+    add_entry(r, chunk, true);
+    budget -= chunk;
+    return true;
+  }
+  // _schedule_step; returns the number of entries (0 = nothing to run)
+  __device__ int32_t schedule() {
+    budget = A.max_batched;
+    ne = 0;
+    const int32_t ns = nrun;
+    for (int32_t k = 0; k < ns; k++) snp[k] = run[k];
+    for (int32_t k = 0; k < ns; k++) {  // decoding requests first, one token each
+      const int32_t r = snp[k];
+      const int64_t g = r0 + r;
+      if (A.rphase[g] != RQ_DECODING) continue;
+      if (budget < 1 || ne >= A.max_seqs) break;
+      const int32_t demand = blocks_needed((int64_t)A.progress[g] + A.generated[g] + 1) - A.alloc[g];
+      if (demand > 0) {
+        if (!make_room(demand, r)) continue;
+        freeb -= demand;
+        A.alloc[g] += demand;
+      }
+      add_entry(r, 1, false);
+      budget -= 1;
+    }
+    // prefills: running partial prefills, then the waiting queue (both as of now)
+    int32_t nc = 0;
+    for (int32_t k = 0; k < nrun; k++)
+      if (A.rphase[r0 + run[k]] == RQ_PREFILLING) snp[nc++] = run[k];
+    const int32_t snap_evt = evt;
+    const int32_t wstart = wfront;
+    bool go = true;
+    for (int32_t k = 0; k < nc && go; k++) go = prefill_candidate(snp[k]);
+    for (int32_t r = wait_next(wstart); go && r < R; r = wait_next(r + 1)) {
+      if (A.pevt[r0 + r] > snap_evt) continue;  // preempted after the snapshot
+      go = prefill_candidate(r);
+    }
+    // keep wfront a lower bound of the waiting ids
+    wfront = wait_next(wfront);
+    return ne;
+  }
+};
+
+template <int MODE>
+__global__ void k_sched(SchedArgs A) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= A.S) return;
+  if (A.status[s] == SC_DONE || A.status[s] == SC_ERROR) return;
+  const int64_t r0 = A.roff[s];
+  Scen c{A, s, r0, (int32_t)(A.roff[s + 1] - r0), A.running + r0, A.snap + r0, A.wbits + A.woff[s],
+         A.ent_id + (int64_t)s * A.max_seqs, A.ent_chunk + (int64_t)s * A.max_seqs, A.ent_pre + (int64_t)s * A.max_seqs,
+         A.nrun[s], A.wfront[s], A.free_blocks[s], A.evt[s], A.n_ent[s], 0, A.preempt[s], false};
+  double t = A.t[s];
+  int32_t nxt = A.next_arr[s];
+  int64_t step = A.nsteps[s];
+  int32_t st = SC_RUNNING;
+  bool resume = A.resume[s] != 0;
+  Pcg64 g;
+  if (MODE == 2) {
+    const uint64_t* p = A.pcg + 6 * (int64_t)s;
+    g.s_hi = p[0];
+    g.s_lo = p[1];
+    g.i_hi = p[2];
+    g.i_lo = p[3];
+    g.has_u32 = (uint32_t)p[4];
+    g.u32 = (uint32_t)p[5];
+  }
+  int32_t* key = A.key + 3 * (int64_t)s;
+  while (step < A.max_steps) {
+    if (!resume) {
+      while (nxt < c.R && A.arrival[r0 + nxt] <= t) {  // admit (engine.py:323-340)
+        const int64_t gi = r0 + nxt;
+        A.rphase[gi] = RQ_WAITING;
+        A.progress[gi] = 0;
+        A.generated[gi] = 0;
+        A.alloc[gi] = 0;
+        A.eidx[gi] = -1;
+        A.pevt[gi] = 0;
+        c.wait_insert(nxt);
+        nxt++;
+      }
+      const int32_t ne = c.schedule();
+      if (c.err) {
+        st = SC_ERROR;
+        break;
+      }
+      if (ne == 0) {
+        if (nxt >= c.R) {
+          st = SC_DONE;
+          break;
+        }
+        t = A.arrival[r0 + nxt];
+        continue;
+      }
+      int32_t tt = 0;
+      bool all_decode = true;
+      for (int32_t k = 0; k < ne; k++) {
+        tt += c.ech[k];
+        all_decode &= c.epr[k] == 0;
+      }
+      key[0] = tt;
+      key[1] = ne;
+      key[2] = all_decode ? 0 : 1;
+    }
+    resume = false;
+    const int32_t tt = key[0], conc = key[1], ph = key[2];
+    double lat;
+    if (MODE == 0) {
+      lat = A.lat_in[(int64_t)s * A.max_steps + step];
+    } else if (MODE == 1) {
+      const double m = ph ? A.gt_mult : 1.0;
+      lat = __dmul_rn(m, __dadd_rn(__dadd_rn(A.gt_base, __dmul_rn(A.gt_tok, (double)tt)), __dmul_rn(A.gt_seq, (double)conc)));
+      if (A.gt_cv > 0.0) {
+        const uint2 k2 = make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32));
+        double f = 0.0;
+        for (uint32_t round = 0;; round++) {
+          const uint4 r = philox4x32_10(make_uint4((uint32_t)step, (uint32_t)((uint64_t)step >> 32), (uint32_t)s, round), k2);
+          const double u1 = ((double)((((uint64_t)r.x << 32) | r.y) >> 11) + 1.0) * (1.0 / 9007199254740992.0);
+          const double u2 = (double)((((uint64_t)r.z << 32) | r.w) >> 11) * (1.0 / 9007199254740992.0);
+          double sn, cs;
+          sincospi(2.0 * u2, &sn, &cs);
+          f = __dadd_rn(1.0, __dmul_rn(A.gt_cv, sqrt(-2.0 * log(u1)) * cs));
+          if (f > 0.0) break;
+        }
+        lat = __dmul_rn(lat, f);
+      }
+    } else {
+      const int64_t idx = map_find<false>(A.map, ph, tt, conc);
+      const long long e = idx >= 0 ? __ldcg(map_entry_ptr(A.map, idx)) : 0;
+      if (e <= 0) {  // no pool yet: pause; the host builds it and relaunches
+        st = SC_PAUSED;
+        A.resume[s] = 1;
+        break;
+      }
+      const double u = unit_double(pcg64_next64(g));
+      const PoolPick pk = pool_pick<true>(A.arena, e, u);
+      uint32_t j = 0;
+      if (pk.n > 1) {
+        const uint32_t w0 = pcg64_next32(g);
+        j = lemire_index((uint32_t)pk.n, w0, [&]() { return pcg64_next32(g); });
+      }
+      lat = __ldcg((ph ? A.s1 : A.s0) + pk.soff + (int32_t)j);
+    }
+    // _apply_outcome (engine.py:464-483)
+    int32_t tokens = 0, fin = 0;
+    for (int32_t k = 0; k < c.ne; k++) {
+      const int32_t r = c.eid[k];
+      const int64_t gi = r0 + r;
+      A.eidx[gi] = -1;
+      if (c.epr[k]) {
+        A.progress[gi] += c.ech[k];
+        if (A.progress[gi] == A.prompt[gi]) {
+          A.rphase[gi] = RQ_DECODING;
+          A.generated[gi] += 1;
+          tokens++;
+        }
+      } else {
+        A.generated[gi] += 1;
+        tokens++;
+      }
+      if (A.rphase[gi] == RQ_DECODING && A.generated[gi] >= A.target[gi]) {
+        A.rphase[gi] = RQ_FINISHED;
+        c.release(r);
+        int32_t q = 0;
+        while (q < c.nrun && c.run[q] != r) q++;
+        for (; q + 1 < c.nrun; q++) c.run[q] = c.run[q + 1];
+        c.nrun--;
+        fin++;
+      }
+    }
+    if (c.err) {
+      st = SC_ERROR;
+      break;
+    }
+    const int64_t o = (int64_t)s * A.max_steps + step;
+    A.o_tt[o] = tt;
+    A.o_conc[o] = conc;
+    A.o_ph[o] = (uint8_t)ph;
+    A.o_lat[o] = lat;
+    A.o_tok[o] = tokens;
+    A.o_fin[o] = fin;
+    A.o_pre[o] = c.npre;
+    c.ne = 0;
+    t = __dadd_rn(t, lat);
+    step++;
+  }
+  if (st == SC_RUNNING && step >= A.max_steps) st = SC_DONE;
+  A.t[s] = t;
+  A.next_arr[s] = nxt;
+  A.nsteps[s] = step;
+  A.nrun[s] = c.nrun;
+  A.wfront[s] = c.wfront;
+  A.free_blocks[s] = c.freeb;
+  A.evt[s] = c.evt;
+  A.preempt[s] = c.npre;
+  A.n_ent[s] = c.ne;
+  A.status[s] = st;
+  if (st != SC_PAUSED) A.resume[s] = 0;
+  if (MODE == 2) {
+    uint64_t* p = A.pcg + 6 * (int64_t)s;
+    p[0] = g.s_hi;
+    p[1] = g.s_lo;
+    p[2] = g.i_hi;
+    p[3] = g.i_lo;
+    p[4] = g.has_u32;
+    p[5] = g.u32;
+  }
+}
+
+}  // namespace emu
+
+using namespace emu;
+
+namespace emu {
+// oracle.cu: the cache views the closed loop reads, and the pool build for keys
+int oracle_views(emu_oracle_t o, MapView* m, const Slot** arena, const double** s0, const double** s1);
+}
+
+struct emu_sched_s {
+  SchedArgs a{};
+  int32_t S = 0;
+  int64_t R = 0, W = 0, max_steps = 0;
+  std::vector<void*> owned;
+  std::vector<int64_t> roff_h;
+  template <typename T>
+  int alloc(T** p, int64_t n) {
+    *p = nullptr;
+    EMU_CUDA(cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<int64_t>(1, n)));
+    owned.push_back((void*)*p);
+    return EMU_OK;
+  }
+  ~emu_sched_s() {
+    for (void* p : owned) cudaFree(p);
+  }
+};
+
+static std::string fmt_i(int64_t v) { return std::to_string(v); }
+
+static int sched_reset(emu_sched_t sc, cudaStream_t s) {
+  SchedArgs& a = sc->a;
+  const int32_t S = sc->S;
+  EMU_CUDA(cudaMemsetAsync(a.wbits, 0, 4 * sc->W, s));
+  EMU_CUDA(cudaMemsetAsync(a.t, 0, 8 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.next_arr, 0, 4 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.nrun, 0, 4 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.wfront, 0, 4 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.nsteps, 0, 8 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.evt, 0, 4 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.preempt, 0, 8 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.status, 0, 4 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.n_ent, 0, 4 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.resume, 0, 4 * S, s));
+  std::vector<int32_t> fb((size_t)S, a.num_blocks);
+  EMU_CUDA(cudaMemcpyAsync(a.free_blocks, fb.data(), 4 * S, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  return EMU_OK;
+}
+
+extern "C" {
+
+int emu_sched_create(int32_t S, const int64_t* req_off, const int32_t* prompt, const int32_t* target,
+                     const double* arrival, int32_t num_gpu_blocks, int32_t block_size, int32_t max_model_len,
+                     int32_t max_num_batched_tokens, int32_t max_num_seqs, int64_t max_steps, emu_sched_t* out) {
+  if (!out) return fail(EMU_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  // EngineConfig.validate (engine.py:85-104)
+  if (block_size < 1) return fail(EMU_ERR_INVALID, "block_size must be >= 1, got " + fmt_i(block_size));
+  if (num_gpu_blocks < 1) return fail(EMU_ERR_INVALID, "num_gpu_blocks must be >= 1, got " + fmt_i(num_gpu_blocks));
+  if (max_model_len < 1) return fail(EMU_ERR_INVALID, "max_model_len must be >= 1, got " + fmt_i(max_model_len));
+  if (max_num_batched_tokens < block_size)
+    return fail(EMU_ERR_INVALID, "max_num_batched_tokens " + fmt_i(max_num_batched_tokens) + " must be >= block_size " +
+                                     fmt_i(block_size));
+  if (max_num_seqs < 1) return fail(EMU_ERR_INVALID, "max_num_seqs must be >= 1, got " + fmt_i(max_num_seqs));
+  if (max_num_batched_tokens < max_num_seqs)
+    return fail(EMU_ERR_INVALID, "max_num_batched_tokens " + fmt_i(max_num_batched_tokens) +
+                                     " must be >= max_num_seqs " + fmt_i(max_num_seqs));
+  if (S < 1 || !req_off || max_steps < 1) return fail(EMU_ERR_INVALID, "need S >= 1 scenarios and max_steps >= 1");
+  std::vector<int64_t> roff(req_off, req_off + S + 1);
+  if (roff[0] != 0) return fail(EMU_ERR_INVALID, "req_off[0] must be 0");
+  std::vector<int64_t> woff((size_t)S + 1, 0);
+  for (int32_t s = 0; s < S; s++) {
+    const int64_t n = roff[s + 1] - roff[s];
+    if (n < 0 || n > (1LL << 30)) return fail(EMU_ERR_INVALID, "bad request offsets");
+    woff[s + 1] = woff[s] + (n + 31) / 32;
+  }
+  const int64_t R = roff[S];
+  // admission checks (engine.py:323-336) and ascending arrival offsets
+  for (int32_t s = 0; s < S; s++)
+    for (int64_t i = roff[s]; i < roff[s + 1]; i++) {
+      if (prompt[i] < 1) return fail(EMU_ERR_INVALID, "prompt_tokens must be >= 1, got " + fmt_i(prompt[i]));
+      if (target[i] < 1) return fail(EMU_ERR_INVALID, "max_tokens must be >= 1, got " + fmt_i(target[i]));
+      const int64_t total = (int64_t)prompt[i] + target[i];
+      if (total > max_model_len)
+        return fail(EMU_ERR_INVALID, "prompt_tokens + max_tokens = " + fmt_i(total) + " exceeds max_model_len " +
+                                         fmt_i(max_model_len));
+      const int64_t fb = (total + block_size - 1) / block_size;
+      if (fb > num_gpu_blocks)
+        return fail(EMU_ERR_INVALID, "request needs " + fmt_i(fb) + " KV blocks but the engine has only " +
+                                         fmt_i(num_gpu_blocks));
+      if (i > roff[s] && arrival[i] < arrival[i - 1]) return fail(EMU_ERR_INVALID, "arrival offsets must ascend");
+    }
+  auto* sc = new emu_sched_s();
+  sc->S = S;
+  sc->R = R;
+  sc->W = woff[S];
+  sc->max_steps = max_steps;
+  sc->roff_h = roff;
+  SchedArgs& a = sc->a;
+  a.num_blocks = num_gpu_blocks;
+  a.block_size = block_size;
+  a.max_batched = max_num_batched_tokens;
+  a.max_seqs = max_num_seqs;
+  a.max_steps = max_steps;
+  a.S = S;
+  int rc;
+  int64_t *d_roff, *d_woff;
+  int32_t *d_prompt, *d_target;
+  double* d_arr;
+  const int64_t SM = (int64_t)S * max_steps, SQ = (int64_t)S * max_num_seqs;
+  if ((rc = sc->alloc(&d_roff, S + 1)) || (rc = sc->alloc(&d_woff, S + 1)) || (rc = sc->alloc(&d_prompt, R)) ||
+      (rc = sc->alloc(&d_target, R)) || (rc = sc->alloc(&d_arr, R)) || (rc = sc->alloc(&a.progress, R)) ||
+      (rc = sc->alloc(&a.generated, R)) || (rc = sc->alloc(&a.alloc, R)) || (rc = sc->alloc(&a.rphase, R)) ||
+      (rc = sc->alloc(&a.eidx, R)) || (rc = sc->alloc(&a.pevt, R)) || (rc = sc->alloc(&a.running, R)) ||
+      (rc = sc->alloc(&a.snap, R)) || (rc = sc->alloc(&a.wbits, sc->W)) || (rc = sc->alloc(&a.ent_id, SQ)) ||
+      (rc = sc->alloc(&a.ent_chunk, SQ)) || (rc = sc->alloc(&a.ent_pre, SQ)) || (rc = sc->alloc(&a.t, S)) ||
+      (rc = sc->alloc(&a.next_arr, S)) || (rc = sc->alloc(&a.nrun, S)) || (rc = sc->alloc(&a.wfront, S)) ||
+      (rc = sc->alloc(&a.free_blocks, S)) || (rc = sc->alloc(&a.nsteps, S)) || (rc = sc->alloc(&a.evt, S)) ||
+      (rc = sc->alloc(&a.preempt, S)) || (rc = sc->alloc(&a.status, S)) || (rc = sc->alloc(&a.n_ent, S)) ||
+      (rc = sc->alloc(&a.resume, S)) || (rc = sc->alloc(&a.key, 3 * (int64_t)S)) ||
+      (rc = sc->alloc(&a.pcg, 6 * (int64_t)S)) || (rc = sc->alloc(&a.o_tt, SM)) || (rc = sc->alloc(&a.o_conc, SM)) ||
+      (rc = sc->alloc(&a.o_ph, SM)) || (rc = sc->alloc(&a.o_lat, SM)) || (rc = sc->alloc(&a.o_tok, SM)) ||
+      (rc = sc->alloc(&a.o_fin, SM)) || (rc = sc->alloc(&a.o_pre, SM))) {
+    delete sc;
+    return rc;
+  }
+  a.roff = d_roff;
+  a.woff = d_woff;
+  a.prompt = d_prompt;
+  a.target = d_target;
+  a.arrival = d_arr;
+  if (cudaMemcpy(d_roff, roff.data(), 8 * (S + 1), cudaMemcpyDefault) != cudaSuccess ||
+      cudaMemcpy(d_woff, woff.data(), 8 * (S + 1), cudaMemcpyDefault) != cudaSuccess ||
+      cudaMemcpy(d_prompt, prompt, 4 * R, cudaMemcpyDefault) != cudaSuccess ||
+      cudaMemcpy(d_target, target, 4 * R, cudaMemcpyDefault) != cudaSuccess ||
+      cudaMemcpy(d_arr, arrival, 8 * R, cudaMemcpyDefault) != cudaSuccess) {
+    delete sc;
+    return cuda_fail(cudaGetLastError(), "emu_sched_create copies");
+  }
+  *out = sc;
+  return EMU_OK;
+}
+
+void emu_sched_destroy(emu_sched_t sc) { delete sc; }
+
+static int launch_sched(emu_sched_t sc, int mode, cudaStream_t s) {
+  const int threads = 32;
+  const int grid = (sc->S + threads - 1) / threads;
+  if (mode == 0) EMU_LAUNCH("sched", s, k_sched<0><<<grid, threads, 0, s>>>(sc->a));
+  if (mode == 1) EMU_LAUNCH("sched", s, k_sched<1><<<grid, threads, 0, s>>>(sc->a));
+  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, threads, 0, s>>>(sc->a));
+  EMU_CUDA(cudaGetLastError());
+  return EMU_OK;
+}
+
+int emu_sched_run_replay(emu_sched_t sc, const double* lat, void* stream) {
+  if (!sc || !lat) return fail(EMU_ERR_INVALID, "NULL scheduler/latencies");
+  cudaStream_t s = as_stream(stream);
+  int rc = sched_reset(sc, s);
+  if (rc) return rc;
+  double* d = nullptr;
+  EMU_CUDA(cudaMalloc(&d, 8 * (size_t)sc->S * sc->max_steps));
+  EMU_CUDA(cudaMemcpyAsync(d, lat, 8 * (size_t)sc->S * sc->max_steps, cudaMemcpyDefault, s));
+  sc->a.lat_in = d;
+  rc = launch_sched(sc, 0, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  sc->a.lat_in = nullptr;
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "k_sched");
+  return EMU_OK;
+}
+
+int emu_sched_run_ground_truth(emu_sched_t sc, double base_s, double per_token_s, double per_seq_s,
+                               double prefill_multiplier, double noise_cv, uint64_t seed, void* stream) {
+  if (!sc) return fail(EMU_ERR_INVALID, "NULL scheduler");
+  if (!(base_s > 0)) return fail(EMU_ERR_INVALID, "base_s must be > 0");
+  if (per_token_s < 0 || per_seq_s < 0) return fail(EMU_ERR_INVALID, "per_token_s and per_seq_s must be >= 0");
+  if (prefill_multiplier < 1.0) return fail(EMU_ERR_INVALID, "prefill_multiplier must be >= 1");
+  if (noise_cv < 0) return fail(EMU_ERR_INVALID, "noise_cv must be >= 0");
+  cudaStream_t s = as_stream(stream);
+  int rc = sched_reset(sc, s);
+  if (rc) return rc;
+  sc->a.gt_base = base_s;
+  sc->a.gt_tok = per_token_s;
+  sc->a.gt_seq = per_seq_s;
+  sc->a.gt_mult = prefill_multiplier;
+  sc->a.gt_cv = noise_cv;
+  sc->a.seed = seed;
+  if ((rc = launch_sched(sc, 1, s))) return rc;
+  EMU_CUDA(cudaStreamSynchronize(s));
+  return EMU_OK;
+}
+
+int emu_oracle_prefetch(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc, const uint8_t* q_phase, int64_t n,
+                        void* stream);
+
+int emu_sched_run_oracle(emu_sched_t sc, emu_oracle_t o, const uint64_t* pcg_states, int64_t* rounds_out,
+                         void* stream) {
+  if (!sc || !o || !pcg_states) return fail(EMU_ERR_INVALID, "NULL scheduler/oracle/states");
+  cudaStream_t s = as_stream(stream);
+  int rc = sched_reset(sc, s);
+  if (rc) return rc;
+  const int32_t S = sc->S;
+  EMU_CUDA(cudaMemcpyAsync(sc->a.pcg, pcg_states, 48 * (size_t)S, cudaMemcpyDefault, s));
+  std::vector<int32_t> st((size_t)S), key((size_t)3 * S), ptt, pcc;
+  std::vector<uint8_t> pph;
+  int32_t *k_tt = nullptr, *k_cc = nullptr;
+  uint8_t* k_ph = nullptr;
+  EMU_CUDA(cudaMalloc(&k_tt, 4 * (size_t)S));
+  EMU_CUDA(cudaMalloc(&k_cc, 4 * (size_t)S));
+  EMU_CUDA(cudaMalloc(&k_ph, (size_t)S));
+  int64_t rounds = 0;
+  for (;;) {
+    rounds++;
+    if ((rc = oracle_views(o, &sc->a.map, &sc->a.arena, &sc->a.s0, &sc->a.s1))) break;
+    if ((rc = launch_sched(sc, 2, s))) break;
+    if (cudaMemcpyAsync(st.data(), sc->a.status, 4 * (size_t)S, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(key.data(), sc->a.key, 12 * (size_t)S, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      rc = cuda_fail(cudaGetLastError(), "k_sched");
+      break;
+    }
+    ptt.clear();
+    pcc.clear();
+    pph.clear();
+    for (int32_t i = 0; i < S; i++)
+      if (st[i] == SC_PAUSED) {
+        ptt.push_back(key[3 * i]);
+        pcc.push_back(key[3 * i + 1]);
+        pph.push_back((uint8_t)key[3 * i + 2]);
+      }
+    if (ptt.empty()) break;
+    const int64_t np = (int64_t)ptt.size();
+    if (cudaMemcpyAsync(k_tt, ptt.data(), 4 * np, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(k_cc, pcc.data(), 4 * np, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(k_ph, pph.data(), np, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      rc = cuda_fail(cudaGetLastError(), "pending keys");
+      break;
+    }
+    if ((rc = emu_oracle_prefetch(o, k_tt, k_cc, k_ph, np, stream))) break;
+  }
+  cudaFree(k_tt);
+  cudaFree(k_cc);
+  cudaFree(k_ph);
+  if (rounds_out) *rounds_out = rounds;
+  return rc;
+}
+
+int emu_sched_results(emu_sched_t sc, int64_t* n_steps, int32_t* status, int32_t* tt, int32_t* conc, uint8_t* phase,
+                      double* lat, int32_t* tokens, int32_t* finished, int64_t* preempt) {
+  if (!sc) return fail(EMU_ERR_INVALID, "NULL scheduler");
+  const size_t S = (size_t)sc->S, SM = S * (size_t)sc->max_steps;
+  if (n_steps) EMU_CUDA(cudaMemcpy(n_steps, sc->a.nsteps, 8 * S, cudaMemcpyDefault));
+  if (status) EMU_CUDA(cudaMemcpy(status, sc->a.status, 4 * S, cudaMemcpyDefault));
+  if (tt) EMU_CUDA(cudaMemcpy(tt, sc->a.o_tt, 4 * SM, cudaMemcpyDefault));
+  if (conc) EMU_CUDA(cudaMemcpy(conc, sc->a.o_conc, 4 * SM, cudaMemcpyDefault));
+  if (phase) EMU_CUDA(cudaMemcpy(phase, sc->a.o_ph, SM, cudaMemcpyDefault));
+  if (lat) EMU_CUDA(cudaMemcpy(lat, sc->a.o_lat, 8 * SM, cudaMemcpyDefault));
+  if (tokens) EMU_CUDA(cudaMemcpy(tokens, sc->a.o_tok, 4 * SM, cudaMemcpyDefault));
+  if (finished) EMU_CUDA(cudaMemcpy(finished, sc->a.o_fin, 4 * SM, cudaMemcpyDefault));
+  if (preempt) EMU_CUDA(cudaMemcpy(preempt, sc->a.o_pre, 8 * SM, cudaMemcpyDefault));
+  return EMU_OK;
+}
+
+}  // extern "C"

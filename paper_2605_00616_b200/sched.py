@@ -1,0 +1,109 @@
+"""The reference scheduler in virtual time on the GPU.
+
+``emulate`` runs S independent what-if scenarios of the reference engine
+(``EmulatorEngine.admit`` / ``_schedule_step`` / ``_apply_outcome``,
+/root/reference/pkg/src/serve_emu/engine.py:323-483) in virtual time, one GPU
+thread per scenario (``emu_sched_*`` in csrc/sched.cu): arrivals <= t are
+admitted, a step is scheduled, its latency is taken from the backend, the
+outcome applied and t advanced by the latency.  Backends:
+
+* ``"oracle"``: a :class:`LatencyOracle` in the closed loop -- scenario s draws
+  from its own numpy PCG64 stream seeded ``seeds[s]``, exactly what a reference
+  engine with ``LatencyOracle(pack, OracleConfig(..., rng_seed=seeds[s]))``
+  would draw; pools are built lazily (paused scenarios, batched build);
+* ``"ground_truth"``: ``ground_truth_latency`` with Philox noise (capture stand-in);
+* ``"replay"``: recorded per-step latencies (parity with a recorded run).
+
+Workloads (request lengths, arrival offsets) come from the caller, e.g. the
+reference's ``generate_workload`` / ``generate_arrivals`` (bench.py:77-116).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .capture import GroundTruthParams
+from .oracle import LatencyOracle, pcg64_state6
+
+
+@dataclass
+class EngineConfig:
+    """Scheduler knobs (engine.py:77-104)."""
+
+    num_gpu_blocks: int
+    block_size: int = 16
+    max_model_len: int = 4096
+    max_num_batched_tokens: int = 512
+    max_num_seqs: int = 64
+
+
+@dataclass
+class Scenario:
+    prompt_tokens: np.ndarray  # int32 [n]
+    output_tokens: np.ndarray  # int32 [n]
+    arrival_s: np.ndarray      # f64 [n], ascending offsets
+
+
+def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int, *, backend: str = "oracle",
+            oracle: LatencyOracle | None = None, seeds: Sequence[int] | None = None,
+            gt_params: GroundTruthParams | None = None, gt_seed: int = 0, latencies=None) -> dict:
+    """Per-step arrays [S, max_steps] (tt, conc, phase, latency, tokens, finished,
+    preemptions) and n_steps [S]; steps past n_steps[s] are unused."""
+    _lib.require_cuda()
+    S = len(scenarios)
+    off = np.zeros(S + 1, np.int64)
+    off[1:] = np.cumsum([len(sc.prompt_tokens) for sc in scenarios])
+    prompt = np.ascontiguousarray(np.concatenate([np.asarray(sc.prompt_tokens) for sc in scenarios]), np.int32)
+    target = np.ascontiguousarray(np.concatenate([np.asarray(sc.output_tokens) for sc in scenarios]), np.int32)
+    arrival = np.ascontiguousarray(np.concatenate([np.asarray(sc.arrival_s) for sc in scenarios]), np.float64)
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    _lib.check(L.emu_sched_create(S, _lib.ptr(off), _lib.ptr(prompt), _lib.ptr(target), _lib.ptr(arrival),
+                                  int(config.num_gpu_blocks), int(config.block_size), int(config.max_model_len),
+                                  int(config.max_num_batched_tokens), int(config.max_num_seqs), int(max_steps),
+                                  ctypes.byref(h)))
+    try:
+        rounds = ctypes.c_int64(0)
+        if backend == "oracle":
+            if oracle is None:
+                raise ValueError("backend='oracle' needs an oracle")
+            seeds = list(seeds) if seeds is not None else [oracle.cfg.rng_seed] * S
+            st = np.stack([pcg64_state6(np.random.default_rng(int(sd)).bit_generator.state) for sd in seeds])
+            st = np.ascontiguousarray(st, dtype=np.uint64)
+            _lib.check(L.emu_sched_run_oracle(h, oracle._h, _lib.ptr(st), ctypes.byref(rounds), _lib.stream_ptr()))
+        elif backend == "ground_truth":
+            p = gt_params or GroundTruthParams()
+            p.validate()
+            _lib.check(L.emu_sched_run_ground_truth(h, float(p.base_s), float(p.per_token_s), float(p.per_seq_s),
+                                                    float(p.prefill_multiplier), float(p.noise_cv),
+                                                    gt_seed & (2**64 - 1), _lib.stream_ptr()))
+        elif backend == "replay":
+            lat = np.zeros((S, max_steps), np.float64)
+            for s, row in enumerate(latencies):
+                row = np.asarray(row, np.float64)[:max_steps]
+                lat[s, :len(row)] = row
+            _lib.check(L.emu_sched_run_replay(h, _lib.ptr(lat), _lib.stream_ptr()))
+        else:
+            raise ValueError(f"unknown backend {backend!r}")
+        n = np.zeros(S, np.int64)
+        status = np.zeros(S, np.int32)
+        out = {k: np.zeros((S, max_steps), dt) for k, dt in (("tt", np.int32), ("conc", np.int32), ("phase", np.uint8),
+                                                              ("latency_s", np.float64), ("tokens", np.int32),
+                                                              ("finished", np.int32), ("preemptions", np.int64))}
+        _lib.check(L.emu_sched_results(h, _lib.ptr(n), _lib.ptr(status), _lib.ptr(out["tt"]), _lib.ptr(out["conc"]),
+                                       _lib.ptr(out["phase"]), _lib.ptr(out["latency_s"]), _lib.ptr(out["tokens"]),
+                                       _lib.ptr(out["finished"]), _lib.ptr(out["preemptions"])))
+        if (status == 3).any():
+            raise RuntimeError(f"scheduler invariant violated in scenarios {np.flatnonzero(status == 3).tolist()}")
+        out["n_steps"] = n
+        out["rounds"] = int(rounds.value)
+        return out
+    finally:
+        L.emu_sched_destroy(h)
+
+
+__all__ = ["EngineConfig", "Scenario", "emulate"]
