@@ -253,6 +253,46 @@ def c5(args):
                                         "frac": fill_gbs / peak, "bytes_per_entry": 26}}}
 
 
+def sweep(args):
+    """What-if sweep with the reference scheduler on the GPU:
+    512 scenarios (32 request rates x 16 burstiness values), each a virtual-time
+    run of EmulatorEngine's scheduler with the oracle in the closed loop (per-
+    scenario PCG64 stream, lazy pools).  Workloads: log-normal prompt/output
+    lengths (medians 200/100, the reference's generate_workload shape) and
+    Gamma(burstiness) inter-arrival gaps (generate_arrivals), numpy-generated."""
+    from paper_2605_00616_b200.sched import EngineConfig, Scenario, emulate
+
+    _, orc = oracle_for(records_llama(1_000_000, 0), 32)
+    rates = np.geomspace(1, 64, 32)
+    gammas = np.geomspace(0.125, 2, 16)
+    steps = args.steps_sweep
+    cfg = EngineConfig(num_gpu_blocks=8192, block_size=16, max_model_len=4096, max_num_batched_tokens=2048,
+                       max_num_seqs=256)
+    g = np.random.default_rng(17)
+    scen = []
+    horizon = steps * 0.05  # virtual seconds comfortably beyond `steps` steps
+    for r in rates:
+        for gm in gammas:
+            n = int(r * horizon) + 16
+            p = np.clip(np.rint(g.lognormal(np.log(200), 0.6, n)), 4, 2048).astype(np.int32)
+            o = np.clip(np.rint(g.lognormal(np.log(100), 0.7, n)), 2, 512).astype(np.int32)
+            gaps = g.gamma(gm, 1.0 / (r * gm), n - 1)
+            scen.append(Scenario(p, o, np.concatenate([[0.0], np.cumsum(gaps)])))
+    scen = scen[: args.scenarios]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = emulate(cfg, scen, steps, backend="oracle", oracle=orc, seeds=list(range(len(scen))))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    total = int(out["n_steps"].sum())
+    return {"config": "sweep", "workload": f"{len(scen)} scenarios (rate x burstiness) x up to {steps} steps, "
+                                            "reference scheduler + oracle closed loop on the GPU",
+            "steps_total": total, "wall_s": wall, "steps_per_s": total / wall, "rounds": out["rounds"],
+            "tokens_total": int(out["tokens"].sum()), "requests": int(sum(len(s.prompt_tokens) for s in scen)),
+            "cpu_reference_note": "the reference engine + LatencyOracle runs ~4k steps/s per core in virtual time "
+                                  "(tests/golden/make_sched_golden.py: 21k steps in ~5 s)"}
+
+
 def codec(args):
     """pack JSON -> SoA and trace JSONL -> records -> GPU tables.
     Reference-algorithm times use this package's json path (the reference's
@@ -328,9 +368,10 @@ def main():
     ap.add_argument("--scenarios", type=int, default=512)
     ap.add_argument("--steps-c5", type=int, default=1_000_000)
     ap.add_argument("--records-codec", type=int, default=1_000_000)
+    ap.add_argument("--steps-sweep", type=int, default=20_000)
     args = ap.parse_args()
     for c in args.configs:
-        res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5, "codec": codec}[c](args)
+        res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5, "codec": codec, "sweep": sweep}[c](args)
         print(json.dumps(res), flush=True)
         torch.cuda.empty_cache()
 

@@ -235,10 +235,13 @@ struct Scen {
   }
 };
 
+// One scenario per CTA (lane 0): scenarios diverge completely, so packing 32 of
+// them into one warp would serialise their paths; one warp each keeps S
+// independent instruction streams spread over the SMs.
 template <int MODE>
-__global__ void k_sched(SchedArgs A) {
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= A.S) return;
+__global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
+  const int32_t s = blockIdx.x;
+  if (threadIdx.x != 0 || s >= A.S) return;
   if (A.status[s] == SC_DONE || A.status[s] == SC_ERROR) return;
   const int64_t r0 = A.roff[s];
   Scen c{A, s, r0, (int32_t)(A.roff[s + 1] - r0), A.running + r0, A.snap + r0, A.wbits + A.woff[s],
@@ -547,11 +550,10 @@ int emu_sched_create(int32_t S, const int64_t* req_off, const int32_t* prompt, c
 void emu_sched_destroy(emu_sched_t sc) { delete sc; }
 
 static int launch_sched(emu_sched_t sc, int mode, cudaStream_t s) {
-  const int threads = 32;
-  const int grid = (sc->S + threads - 1) / threads;
-  if (mode == 0) EMU_LAUNCH("sched", s, k_sched<0><<<grid, threads, 0, s>>>(sc->a));
-  if (mode == 1) EMU_LAUNCH("sched", s, k_sched<1><<<grid, threads, 0, s>>>(sc->a));
-  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, threads, 0, s>>>(sc->a));
+  const int grid = sc->S;
+  if (mode == 0) EMU_LAUNCH("sched", s, k_sched<0><<<grid, 32, 0, s>>>(sc->a));
+  if (mode == 1) EMU_LAUNCH("sched", s, k_sched<1><<<grid, 32, 0, s>>>(sc->a));
+  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, 32, 0, s>>>(sc->a));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
 }

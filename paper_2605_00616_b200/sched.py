@@ -48,11 +48,39 @@ class Scenario:
     arrival_s: np.ndarray      # f64 [n], ascending offsets
 
 
+def step_key_domain(config: EngineConfig):
+    """Every step key the scheduler can produce: decode steps (c, c) and mixed
+    steps (t, c) with c <= t <= max_num_batched_tokens, c <= max_num_seqs."""
+    c = np.arange(1, config.max_num_seqs + 1, dtype=np.int64)
+    dec = (c, c, np.zeros(len(c), np.uint8))
+    reps = np.maximum(0, config.max_num_batched_tokens - c + 1)
+    mc = np.repeat(c, reps)
+    start = np.repeat(c - np.concatenate([[0], np.cumsum(reps)[:-1]]), reps)
+    mt = np.arange(len(mc), dtype=np.int64) + start
+    mix = (mt, mc, np.ones(len(mc), np.uint8))
+    return tuple(np.concatenate([d, m]) for d, m in zip(dec, mix))
+
+
+def prefetch_domain(oracle: LatencyOracle, config: EngineConfig) -> int:
+    """Build the pools of every step key of `config` up front (emu_oracle_prefetch):
+    pools are pure functions of the key, so this changes no draw -- it only
+    removes the closed loop's pause-and-build rounds."""
+    torch = _lib.require_cuda()
+    tt, cc, ph = step_key_domain(config)
+    cols = [torch.as_tensor(tt.astype(np.int32), device="cuda"), torch.as_tensor(cc.astype(np.int32), device="cuda"),
+            torch.as_tensor(ph, device="cuda")]
+    _lib.check(_lib.lib().emu_oracle_prefetch(oracle._h, *[_lib.ptr(c) for c in cols], len(tt), _lib.stream_ptr()))
+    return len(tt)
+
+
 def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int, *, backend: str = "oracle",
             oracle: LatencyOracle | None = None, seeds: Sequence[int] | None = None,
-            gt_params: GroundTruthParams | None = None, gt_seed: int = 0, latencies=None) -> dict:
+            gt_params: GroundTruthParams | None = None, gt_seed: int = 0, latencies=None,
+            prefetch: bool | None = None) -> dict:
     """Per-step arrays [S, max_steps] (tt, conc, phase, latency, tokens, finished,
-    preemptions) and n_steps [S]; steps past n_steps[s] are unused."""
+    preemptions) and n_steps [S]; steps past n_steps[s] are unused.  With the
+    oracle backend, `prefetch` (default: when the key domain has <= 2M keys)
+    builds every reachable pool first, so the closed loop runs in one launch."""
     _lib.require_cuda()
     S = len(scenarios)
     off = np.zeros(S + 1, np.int64)
@@ -74,6 +102,9 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
             seeds = list(seeds) if seeds is not None else [oracle.cfg.rng_seed] * S
             st = np.stack([pcg64_state6(np.random.default_rng(int(sd)).bit_generator.state) for sd in seeds])
             st = np.ascontiguousarray(st, dtype=np.uint64)
+            domain = config.max_num_seqs * config.max_num_batched_tokens
+            if prefetch or (prefetch is None and domain <= 2_000_000):
+                prefetch_domain(oracle, config)
             _lib.check(L.emu_sched_run_oracle(h, oracle._h, _lib.ptr(st), ctypes.byref(rounds), _lib.stream_ptr()))
         elif backend == "ground_truth":
             p = gt_params or GroundTruthParams()
@@ -106,4 +137,4 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
         L.emu_sched_destroy(h)
 
 
-__all__ = ["EngineConfig", "Scenario", "emulate"]
+__all__ = ["EngineConfig", "Scenario", "emulate", "prefetch_domain", "step_key_domain"]

@@ -44,16 +44,17 @@ def test_closed_loop_oracle_matches_reference(c1_records):
     from paper_2605_00616_b200 import build_pack_arrays
 
     pack = build_pack_arrays(*c1_records, num_gpu_blocks=1000, canonical=True)
-    orc = LatencyOracle(pack, OracleConfig(reliability_floor=32, rng_seed=11))
     cfg, sc = scenario("oracle")
     n = len(G["oracle_lat"])
-    out = emulate(cfg, [sc, sc, sc], n, backend="oracle", oracle=orc, seeds=[11, 11, 11])
-    for s in range(3):
-        assert out["n_steps"][s] == n
-        keys = np.stack([out["tt"][s], out["conc"][s], out["phase"][s].astype(np.int32)], 1)
-        assert np.array_equal(keys, G["oracle_keys"])
-        assert np.array_equal(out["latency_s"][s].view(np.uint64), G["oracle_lat"].view(np.uint64))
-    assert out["rounds"] > 1
+    for prefetch in (False, True):  # lazy pools (pause + build rounds) / every reachable pool first
+        orc = LatencyOracle(pack, OracleConfig(reliability_floor=32, rng_seed=11))
+        out = emulate(cfg, [sc, sc, sc], n, backend="oracle", oracle=orc, seeds=[11, 11, 11], prefetch=prefetch)
+        for s in range(3):
+            assert out["n_steps"][s] == n
+            keys = np.stack([out["tt"][s], out["conc"][s], out["phase"][s].astype(np.int32)], 1)
+            assert np.array_equal(keys, G["oracle_keys"])
+            assert np.array_equal(out["latency_s"][s].view(np.uint64), G["oracle_lat"].view(np.uint64))
+        assert (out["rounds"] == 1) if prefetch else (out["rounds"] > 1)
 
 
 def test_ground_truth_backend_runs_and_is_deterministic():
