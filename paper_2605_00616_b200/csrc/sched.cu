@@ -36,6 +36,7 @@
 
 namespace emu {
 
+constexpr unsigned kFull = 0xffffffffu;
 enum : uint8_t { RQ_WAITING = 0, RQ_PREFILLING = 1, RQ_DECODING = 2, RQ_PREEMPTED = 3, RQ_FINISHED = 4 };
 enum : int32_t { SC_RUNNING = 0, SC_DONE = 1, SC_PAUSED = 2, SC_ERROR = 3 };
 
@@ -197,13 +198,70 @@ struct Scen {
     budget -= chunk;
     return true;
   }
-  // _schedule_step; returns the number of entries (0 = nothing to run)
+  // _schedule_step; returns the number of entries (0 = nothing to run).
+  // Executed by the whole warp: sequential parts run identically on every
+  // lane (uniform control flow, identical writes); the per-request loops are
+  // lane-parallel where the reference's order cannot be observed.
   __device__ int32_t schedule() {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     budget = A.max_batched;
     ne = 0;
     const int32_t ns = nrun;
-    for (int32_t k = 0; k < ns; k++) snp[k] = run[k];
-    for (int32_t k = 0; k < ns; k++) {  // decoding requests first, one token each
+    for (int32_t k = lane; k < ns; k += 32) snp[k] = run[k];
+    __syncwarp();
+    // decoding requests first, one token each.  Per chunk of 32: if the KV
+    // demand of every admitted decode entry fits in the free blocks, no
+    // make_room can fire and the chunk commits in parallel (same order, same
+    // final state); otherwise commit up to the first entry that would have to
+    // preempt and finish the pass sequentially.
+    int32_t k_seq = ns;  // where the sequential remainder starts (ns = none)
+    bool stop = false;
+    for (int32_t base = 0; base < ns && !stop; base += 32) {
+      const int32_t k = base + lane;
+      int32_t r = -1, demand = 0;
+      bool dec = false;
+      if (k < ns) {
+        r = snp[k];
+        const int64_t g = r0 + r;
+        dec = A.rphase[g] == RQ_DECODING;
+        if (dec) demand = blocks_needed((int64_t)A.progress[g] + A.generated[g] + 1) - A.alloc[g];
+      }
+      const unsigned dm = __ballot_sync(kFull, dec);
+      const int32_t allow = min(budget, A.max_seqs - ne);
+      const int32_t rank = __popc(dm & lt);
+      const bool ok = dec && rank < allow;
+      int32_t cum = ok && demand > 0 ? demand : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(kFull, cum, o);
+        if (lane >= o) cum += y;
+      }
+      const unsigned fail = __ballot_sync(kFull, ok && cum > freeb);
+      const unsigned okm = __ballot_sync(kFull, ok) & (fail ? ((1u << (__ffs(fail) - 1)) - 1u) : kFull);
+      if (okm & (1u << lane)) {
+        const int64_t g = r0 + r;
+        if (demand > 0) A.alloc[g] += demand;
+        const int32_t e = ne + __popc(okm & lt);
+        eid[e] = r;
+        ech[e] = 1;
+        epr[e] = 0;
+        A.eidx[g] = e;
+      }
+      const int32_t nok = __popc(okm);
+      const int32_t used = __shfl_sync(kFull, cum, okm ? 31 - __clz(okm) : 0);
+      if (okm) freeb -= used;
+      ne += nok;
+      budget -= nok;
+      __syncwarp();
+      if (fail) {
+        k_seq = base + __ffs(fail) - 1;
+        stop = true;
+      } else if (__popc(dm) > allow) {
+        stop = true;  // the reference breaks at the first decode request over the budget
+      }
+    }
+    for (int32_t k = k_seq; k < ns; k++) {  // sequential remainder (preemption possible)
       const int32_t r = snp[k];
       const int64_t g = r0 + r;
       if (A.rphase[g] != RQ_DECODING) continue;
@@ -216,18 +274,31 @@ struct Scen {
       }
       add_entry(r, 1, false);
       budget -= 1;
+      __syncwarp();
     }
     // prefills: running partial prefills, then the waiting queue (both as of now)
     int32_t nc = 0;
-    for (int32_t k = 0; k < nrun; k++)
-      if (A.rphase[r0 + run[k]] == RQ_PREFILLING) snp[nc++] = run[k];
+    for (int32_t base = 0; base < nrun; base += 32) {
+      const int32_t k = base + lane;
+      const int32_t r = k < nrun ? run[k] : 0;
+      const bool pf = k < nrun && A.rphase[r0 + r] == RQ_PREFILLING;
+      const unsigned m = __ballot_sync(kFull, pf);
+      __syncwarp();
+      if (pf) snp[nc + __popc(m & lt)] = r;
+      nc += __popc(m);
+    }
+    __syncwarp();
     const int32_t snap_evt = evt;
     const int32_t wstart = wfront;
     bool go = true;
-    for (int32_t k = 0; k < nc && go; k++) go = prefill_candidate(snp[k]);
+    for (int32_t k = 0; k < nc && go; k++) {
+      go = prefill_candidate(snp[k]);
+      __syncwarp();
+    }
     for (int32_t r = wait_next(wstart); go && r < R; r = wait_next(r + 1)) {
       if (A.pevt[r0 + r] > snap_evt) continue;  // preempted after the snapshot
       go = prefill_candidate(r);
+      __syncwarp();
     }
     // keep wfront a lower bound of the waiting ids
     wfront = wait_next(wfront);
@@ -235,13 +306,15 @@ struct Scen {
   }
 };
 
-// One scenario per CTA (lane 0): scenarios diverge completely, so packing 32 of
-// them into one warp would serialise their paths; one warp each keeps S
-// independent instruction streams spread over the SMs.
+// One scenario per warp (CTA of 32): scenarios diverge completely, so one warp
+// each keeps S independent instruction streams spread over the SMs; the warp's
+// lanes share the per-request loops of a step.
 template <int MODE>
 __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
   const int32_t s = blockIdx.x;
-  if (threadIdx.x != 0 || s >= A.S) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  if (s >= A.S) return;
   if (A.status[s] == SC_DONE || A.status[s] == SC_ERROR) return;
   const int64_t r0 = A.roff[s];
   Scen c{A, s, r0, (int32_t)(A.roff[s + 1] - r0), A.running + r0, A.snap + r0, A.wbits + A.woff[s],
@@ -338,9 +411,12 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
       }
       lat = __ldcg((ph ? A.s1 : A.s0) + pk.soff + (int32_t)j);
     }
-    // _apply_outcome (engine.py:464-483)
-    int32_t tokens = 0, fin = 0;
-    for (int32_t k = 0; k < c.ne; k++) {
+    // _apply_outcome (engine.py:464-483): entries are distinct requests, so the
+    // per-entry updates run lane-parallel; finished requests leave the running
+    // list in one order-preserving compaction.
+    int32_t tokens = 0, fin = 0, freed = 0;
+    bool dfree = false;
+    for (int32_t k = lane; k < c.ne; k += 32) {
       const int32_t r = c.eid[k];
       const int64_t gi = r0 + r;
       A.eidx[gi] = -1;
@@ -357,13 +433,34 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
       }
       if (A.rphase[gi] == RQ_DECODING && A.generated[gi] >= A.target[gi]) {
         A.rphase[gi] = RQ_FINISHED;
-        c.release(r);
-        int32_t q = 0;
-        while (q < c.nrun && c.run[q] != r) q++;
-        for (; q + 1 < c.nrun; q++) c.run[q] = c.run[q + 1];
-        c.nrun--;
+        dfree |= A.alloc[gi] == 0;
+        freed += A.alloc[gi];
+        A.alloc[gi] = 0;
         fin++;
       }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tokens += __shfl_xor_sync(kFull, tokens, o);
+      fin += __shfl_xor_sync(kFull, fin, o);
+      freed += __shfl_xor_sync(kFull, freed, o);
+    }
+    if (__any_sync(kFull, dfree)) c.err = true;
+    c.freeb += freed;
+    __syncwarp();
+    if (fin) {
+      int32_t out = 0;
+      for (int32_t base = 0; base < c.nrun; base += 32) {
+        const int32_t k = base + lane;
+        const int32_t r = k < c.nrun ? c.run[k] : 0;
+        const bool keep = k < c.nrun && A.rphase[r0 + r] != RQ_FINISHED;
+        const unsigned m = __ballot_sync(kFull, keep);
+        __syncwarp();
+        if (keep) c.run[out + __popc(m & lt)] = r;
+        out += __popc(m);
+        __syncwarp();
+      }
+      c.nrun = out;
     }
     if (c.err) {
       st = SC_ERROR;
