@@ -361,7 +361,7 @@ def codec(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("configs", nargs="*", default=["c1", "c3", "c4", "c5"])
+    ap.add_argument("configs", nargs="*", default=["c1", "c4", "c3", "c5", "codec", "sweep"])
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--queries", type=int, default=10_000_000)
     ap.add_argument("--records-c4", type=int, default=100_000_000)
@@ -373,6 +373,9 @@ def main():
     for c in args.configs:
         res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5, "codec": codec, "sweep": sweep}[c](args)
         print(json.dumps(res), flush=True)
+        import gc
+
+        gc.collect()
         torch.cuda.empty_cache()
 
 
