@@ -17,7 +17,8 @@ other configs on one GPU so every SURVEY §8 row has a number:
       values) x 1M steps, keys generated on the GPU per scenario, Philox
       draws; plus the synthetic token fill over 256M entries.
 
-    python bench_configs.py [c1 c3 c4 c5] [--steps K]
+    python bench_configs.py [c1 c3 c4 c5 codec sweep] [--steps K]
+    torchrun --nproc-per-node N bench_configs.py c4 sweep   (range-partitioned build, sharded sweep)
 """
 from __future__ import annotations
 
@@ -148,8 +149,59 @@ def c3(args):
     return out
 
 
+def world():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def c4_dist(args):
+    """Config 4 across ranks: each rank synthesises n/size records,
+    tt-range partition (all-reduced histogram -> splitters), one all_to_all per
+    column over NCCL, local canonical build of its tt slice.  Time = max over ranks."""
+    import torch.distributed as dist
+
+    from paper_2605_00616_b200.capture import records_device
+    from paper_2605_00616_b200.dist import exchange_records, partition_by_tt
+
+    rank, size = world()
+    n = args.records_c4
+    dev = list(records_device(n // size, seed=100 + rank))
+
+    def step():
+        spl = partition_by_tt(dev[0], size)
+        cols = exchange_records(dev, dev[0], spl)
+        t = DeviceTables.build(*cols, canonical=True)
+        nb = sum(t.info(i)["n_buckets"] for i in range(3))
+        del t
+        return nb
+
+    step()
+    times = []
+    for _ in range(max(1, args.steps // 3)):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        nb = step()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    tl = torch.tensor([statistics.mean(times), float(nb)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tl[:1], op=dist.ReduceOp.MAX)
+    dist.all_reduce(tl[1:], op=dist.ReduceOp.SUM)
+    ms = float(tl[0].item()) * 1e3
+    return {"config": "c4", "workload": f"{n} synthetic records (generator G) over {size} ranks: tt-range partition, "
+                                        "NCCL all_to_all exchange, per-rank canonical build",
+            "n_gpus": size, "ms_per_build": ms, "records_per_s": n / (ms / 1e3), "buckets_total": int(tl[1].item()),
+            "scaling": "strong"}
+
+
 def c4(args):
     from paper_2605_00616_b200.capture import records_device
+
+    if world()[1] > 1:
+        return c4_dist(args)
 
     n = args.records_c4
     torch.cuda.synchronize()
@@ -279,12 +331,23 @@ def sweep(args):
             gaps = g.gamma(gm, 1.0 / (r * gm), n - 1)
             scen.append(Scenario(p, o, np.concatenate([[0.0], np.cumsum(gaps)])))
     scen = scen[: args.scenarios]
+    rank, size = world()
+    mine = list(range(rank, len(scen), size))  # scenarios shard across ranks, no collective in the loop
     torch.cuda.synchronize()
+    if size > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     t0 = time.perf_counter()
-    out = emulate(cfg, scen, steps, backend="oracle", oracle=orc, seeds=list(range(len(scen))))
+    out = emulate(cfg, [scen[k] for k in mine], steps, backend="oracle", oracle=orc, seeds=mine)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     total = int(out["n_steps"].sum())
+    if size > 1:
+        tl = torch.tensor([wall, float(total)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tl[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tl[1:], op=dist.ReduceOp.SUM)
+        wall, total = float(tl[0].item()), int(tl[1].item())
     return {"config": "sweep", "workload": f"{len(scen)} scenarios (rate x burstiness) x up to {steps} steps, "
                                             "reference scheduler + oracle closed loop on the GPU",
             "steps_total": total, "wall_s": wall, "steps_per_s": total / wall, "rounds": out["rounds"],
@@ -370,9 +433,20 @@ def main():
     ap.add_argument("--records-codec", type=int, default=1_000_000)
     ap.add_argument("--steps-sweep", type=int, default=20_000)
     args = ap.parse_args()
+    size = int(os.environ.get("WORLD_SIZE", 1))
+    if size > 1:  # torchrun: one process per GPU; configs c4 and sweep shard, the rest run on rank 0's GPU
+        import torch.distributed as dist
+
+        local = int(os.environ.get("LOCAL_RANK", 0))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank = int(os.environ.get("RANK", 0))
     for c in args.configs:
+        if size > 1 and c not in ("c4", "sweep"):
+            continue
         res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5, "codec": codec, "sweep": sweep}[c](args)
-        print(json.dumps(res), flush=True)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
         import gc
 
         gc.collect()
