@@ -1517,7 +1517,11 @@ int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q
   // draws (s) and chunk i-2's copy-out (cp_out).  Draws are pure functions of
   // (query, uniforms / counter, pool), so chunking never changes a result.
   // Staging covers all Q queries: no buffer is reused within a call.
-  const int64_t chunk = std::min<int64_t>(std::max<int64_t>(o->chunk_cap, 1), kHostChunk);
+  static const int64_t host_chunk = [] {
+    const char* v = getenv("EMU_HOST_CHUNK");
+    return v ? std::max<int64_t>(1024, atoll(v)) : kHostChunk;
+  }();
+  const int64_t chunk = std::min<int64_t>(std::max<int64_t>(o->chunk_cap, 1), host_chunk);
   const int64_t nch = (Q + chunk - 1) / chunk;
   if (!o->cp_in) {
     EMU_CUDA(cudaStreamCreateWithFlags(&o->cp_in, cudaStreamNonBlocking));
