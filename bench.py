@@ -42,8 +42,8 @@ WORKLOAD = ("C2: 10M-query batched oracle sweep over a 1M-record Llama-3.1-8B-sh
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--queries", type=int, default=10_000_000, help="queries per GPU per step")
     ap.add_argument("--records", type=int, default=1_000_000)
@@ -59,7 +59,7 @@ def env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled every 20 ms during the timed region."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -73,7 +73,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -285,9 +285,10 @@ def run_b200(args):
         if size > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(max(3, args.steps // 2)):
+        n_e2e = min(20, max(3, args.steps // 2))
+        for _ in range(n_e2e):
             e2e_step()
-        e2e_s = (time.perf_counter() - t0) / max(3, args.steps // 2)
+        e2e_s = (time.perf_counter() - t0) / n_e2e
         e2e_s = all_reduce_max(e2e_s)
         h2d = Q * (4 + 4 + 1 + (12 if args.rng == "explicit" else 0))
         line["e2e"] = {"value": size * Q / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d,
