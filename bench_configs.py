@@ -339,7 +339,8 @@ def sweep(args):
 
         dist.barrier()
     t0 = time.perf_counter()
-    out = emulate(cfg, [scen[k] for k in mine], steps, backend="oracle", oracle=orc, seeds=mine)
+    out = emulate(cfg, [scen[k] for k in mine], steps, backend="oracle", oracle=orc, seeds=mine,
+                  keep_steps=steps <= 50_000)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     total = int(out["n_steps"].sum())

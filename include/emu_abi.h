@@ -268,6 +268,9 @@ int emu_sched_run_oracle(emu_sched_t sc, emu_oracle_t o, const uint64_t* pcg_sta
                          void* stream);
 int emu_sched_results(emu_sched_t sc, int64_t* n_steps, int32_t* status, int32_t* tt, int32_t* conc,
                       uint8_t* phase, double* lat, int32_t* tokens, int32_t* finished, int64_t* preempt);
+/* Per-scenario totals [S x 4]: steps, tokens emitted, requests finished,
+ * preemptions -- without copying the per-step arrays to the host. */
+int emu_sched_summary(emu_sched_t sc, int64_t* out4);
 void emu_sched_destroy(emu_sched_t sc);
 
 /* --------------------------------------------------------------- codecs --

@@ -72,6 +72,7 @@ SIGNATURES = {
     "emu_sched_run_ground_truth": (c_int, [c_vp, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_u64, c_vp]),
     "emu_sched_run_oracle": (c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_i64), c_vp]),
     "emu_sched_results": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "emu_sched_summary": (c_int, [c_vp, c_vp]),
     "emu_sched_destroy": (None, [c_vp]),
     "emu_pack_parse_json": (c_int, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
     "emu_pack_parsed_info": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_vp,

@@ -749,6 +749,53 @@ int emu_sched_run_oracle(emu_sched_t sc, emu_oracle_t o, const uint64_t* pcg_sta
   return rc;
 }
 
+}  // extern "C"
+
+namespace emu {
+// Per-scenario totals without copying the per-step arrays out.
+__global__ void k_sched_sum(const int64_t* nsteps, const int32_t* tok, const int32_t* fin, const int64_t* pre,
+                            int64_t max_steps, int64_t* out) {
+  const int32_t s = blockIdx.x;
+  const int64_t n = nsteps[s];
+  long long a = 0, b = 0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    a += tok[s * max_steps + k];
+    b += fin[s * max_steps + k];
+  }
+  __shared__ long long sa[256], sb[256];
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      sa[threadIdx.x] += sa[threadIdx.x + o];
+      sb[threadIdx.x] += sb[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[4 * s] = n;
+    out[4 * s + 1] = sa[0];
+    out[4 * s + 2] = sb[0];
+    out[4 * s + 3] = n ? pre[s * max_steps + n - 1] : 0;
+  }
+}
+}  // namespace emu
+
+extern "C" {
+
+int emu_sched_summary(emu_sched_t sc, int64_t* out4) {
+  if (!sc || !out4) return fail(EMU_ERR_INVALID, "NULL scheduler/output");
+  int64_t* d = nullptr;
+  EMU_CUDA(cudaMalloc(&d, 32 * (size_t)sc->S));
+  EMU_LAUNCH("sched_sum", 0, k_sched_sum<<<sc->S, 256>>>(sc->a.nsteps, sc->a.o_tok, sc->a.o_fin, sc->a.o_pre,
+                                                          sc->max_steps, d));
+  const cudaError_t e = cudaMemcpy(out4, d, 32 * (size_t)sc->S, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "emu_sched_summary");
+  return EMU_OK;
+}
+
 int emu_sched_results(emu_sched_t sc, int64_t* n_steps, int32_t* status, int32_t* tt, int32_t* conc, uint8_t* phase,
                       double* lat, int32_t* tokens, int32_t* finished, int64_t* preempt) {
   if (!sc) return fail(EMU_ERR_INVALID, "NULL scheduler");

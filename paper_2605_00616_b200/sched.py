@@ -76,7 +76,7 @@ def prefetch_domain(oracle: LatencyOracle, config: EngineConfig) -> int:
 def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int, *, backend: str = "oracle",
             oracle: LatencyOracle | None = None, seeds: Sequence[int] | None = None,
             gt_params: GroundTruthParams | None = None, gt_seed: int = 0, latencies=None,
-            prefetch: bool | None = None) -> dict:
+            prefetch: bool | None = None, keep_steps: bool = True) -> dict:
     """Per-step arrays [S, max_steps] (tt, conc, phase, latency, tokens, finished,
     preemptions) and n_steps [S]; steps past n_steps[s] are unused.  With the
     oracle backend, `prefetch` (default: when the key domain has <= 2M keys)
@@ -122,6 +122,14 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
             raise ValueError(f"unknown backend {backend!r}")
         n = np.zeros(S, np.int64)
         status = np.zeros(S, np.int32)
+        if not keep_steps:  # totals only (long sweeps): no per-step arrays cross PCIe
+            summ = np.zeros((S, 4), np.int64)
+            _lib.check(L.emu_sched_summary(h, _lib.ptr(summ)))
+            _lib.check(L.emu_sched_results(h, None, _lib.ptr(status), None, None, None, None, None, None, None))
+            if (status == 3).any():
+                raise RuntimeError(f"scheduler invariant violated in scenarios {np.flatnonzero(status == 3).tolist()}")
+            return {"n_steps": summ[:, 0], "tokens": summ[:, 1], "finished": summ[:, 2], "preemptions": summ[:, 3],
+                    "rounds": int(rounds.value)}
         out = {k: np.zeros((S, max_steps), dt) for k, dt in (("tt", np.int32), ("conc", np.int32), ("phase", np.uint8),
                                                               ("latency_s", np.float64), ("tokens", np.int32),
                                                               ("finished", np.int32), ("preemptions", np.int64))}
