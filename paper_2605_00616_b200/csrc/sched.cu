@@ -93,7 +93,13 @@ struct SchedArgs {
   const Slot* arena;
   const double* s0;
   const double* s1;
+  // EMU_SCHED_PROF=1: per-scenario cycle / event counters [S * kProfN]
+  long long* prof;
 };
+// prof slots: cycles in admit, decode pass, prefill pass, draw, apply+compact;
+// then counts: steps, sequential-remainder iterations, waiting candidates,
+// waiting-bitmap words scanned, preemptions' entry shifts
+constexpr int kProfN = 10;
 
 struct Scen {
   const SchedArgs& A;
@@ -109,6 +115,9 @@ struct Scen {
   int32_t nrun, wfront, freeb, evt, ne, budget;
   int64_t npre;
   bool err;
+  long long nseq = 0, ncand = 0, nwords = 0, nshift = 0;  // EMU_SCHED_PROF counters
+  long long t_dec = 0;                                     // clock at the end of the decode pass
+  int32_t lim = 0;  // requests admitted so far: every waiting id is below it
 
   __device__ int32_t blocks_needed(int64_t tokens) const {
     return (int32_t)((tokens + A.block_size - 1) / A.block_size);
@@ -118,15 +127,17 @@ struct Scen {
     if (r < wfront) wfront = r;
   }
   __device__ void wait_remove(int32_t r) { wb[r >> 5] &= ~(1u << (r & 31)); }
-  // next waiting id >= r (or R)
-  __device__ int32_t wait_next(int32_t r) const {
+  // next waiting id >= r (or R); the scan stops at `lim`, so an empty queue
+  // costs O(1) words instead of a pass over the not-yet-arrived tail
+  __device__ int32_t wait_next(int32_t r) {
     int32_t w = r >> 5;
-    const int32_t nw = (R + 31) >> 5;
+    const int32_t nw = (lim + 31) >> 5;
     if (w >= nw) return R;
     uint32_t m = wb[w] & (0xffffffffu << (r & 31));
     while (!m) {
       if (++w >= nw) return R;
       m = wb[w];
+      nwords++;
     }
     return w * 32 + __ffs(m) - 1;
   }
@@ -155,6 +166,7 @@ struct Scen {
     const int32_t k = A.eidx[g];
     if (k >= 0) {  // drop its entry (order kept) and refund its budget
       budget += ech[k];
+      nshift += ne - k - 1;
       for (int32_t q = k + 1; q < ne; q++) {
         eid[q - 1] = eid[q];
         ech[q - 1] = ech[q];
@@ -262,6 +274,7 @@ struct Scen {
       }
     }
     for (int32_t k = k_seq; k < ns; k++) {  // sequential remainder (preemption possible)
+      nseq++;
       const int32_t r = snp[k];
       const int64_t g = r0 + r;
       if (A.rphase[g] != RQ_DECODING) continue;
@@ -276,6 +289,7 @@ struct Scen {
       budget -= 1;
       __syncwarp();
     }
+    if (A.prof) t_dec = clock64();
     // prefills: running partial prefills, then the waiting queue (both as of now)
     int32_t nc = 0;
     for (int32_t base = 0; base < nrun; base += 32) {
@@ -296,6 +310,7 @@ struct Scen {
       __syncwarp();
     }
     for (int32_t r = wait_next(wstart); go && r < R; r = wait_next(r + 1)) {
+      ncand++;
       if (A.pevt[r0 + r] > snap_evt) continue;  // preempted after the snapshot
       go = prefill_candidate(r);
       __syncwarp();
@@ -336,6 +351,16 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
     g.u32 = (uint32_t)p[5];
   }
   int32_t* key = A.key + 3 * (int64_t)s;
+  const bool P = A.prof != nullptr;
+  const int64_t step0 = step;
+  long long pc[5] = {0, 0, 0, 0, 0}, tc = P ? clock64() : 0;
+  auto lap = [&](int i) {
+    if (P) {
+      const long long n = clock64();
+      pc[i] += n - tc;
+      tc = n;
+    }
+  };
   while (step < A.max_steps) {
     if (!resume) {
       while (nxt < c.R && A.arrival[r0 + nxt] <= t) {  // admit (engine.py:323-340)
@@ -349,7 +374,14 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
         c.wait_insert(nxt);
         nxt++;
       }
+      lap(0);
+      c.lim = nxt;
       const int32_t ne = c.schedule();
+      if (P) {
+        pc[1] += c.t_dec - tc;
+        tc = c.t_dec;
+        lap(2);
+      }
       if (c.err) {
         st = SC_ERROR;
         break;
@@ -411,6 +443,7 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
       }
       lat = __ldcg((ph ? A.s1 : A.s0) + pk.soff + (int32_t)j);
     }
+    lap(3);
     // _apply_outcome (engine.py:464-483): entries are distinct requests, so the
     // per-entry updates run lane-parallel; finished requests leave the running
     // list in one order-preserving compaction.
@@ -477,6 +510,16 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
     c.ne = 0;
     t = __dadd_rn(t, lat);
     step++;
+    lap(4);
+  }
+  if (P && lane == 0) {
+    long long* q = A.prof + (int64_t)s * kProfN;
+    for (int i = 0; i < 5; i++) q[i] += pc[i];
+    q[5] += step - step0;
+    q[6] += c.nseq;
+    q[7] += c.ncand;
+    q[8] += c.nwords;
+    q[9] += c.nshift;
   }
   if (st == SC_RUNNING && step >= A.max_steps) st = SC_DONE;
   A.t[s] = t;
@@ -524,7 +567,28 @@ struct emu_sched_s {
     return EMU_OK;
   }
   ~emu_sched_s() {
+    if (a.prof) print_prof();
     for (void* p : owned) cudaFree(p);
+  }
+  void print_prof() {
+    std::vector<long long> h((size_t)S * kProfN);
+    if (cudaMemcpy(h.data(), a.prof, 8 * h.size(), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    static const char* names[kProfN] = {"admit_cyc", "decode_cyc", "prefill_cyc", "draw_cyc", "apply_cyc",
+                                        "steps",     "seq_iters",  "wait_cands",  "wait_words", "entry_shifts"};
+    std::vector<long long> sum(kProfN, 0);
+    int32_t slow = 0;
+    long long slow_c = -1;
+    for (int32_t s = 0; s < S; s++) {
+      long long c = 0;
+      for (int i = 0; i < kProfN; i++) sum[i] += h[(size_t)s * kProfN + i];
+      for (int i = 0; i < 5; i++) c += h[(size_t)s * kProfN + i];
+      if (c > slow_c) slow_c = c, slow = s;
+    }
+    fprintf(stderr, "[sched prof] all scenarios:");
+    for (int i = 0; i < kProfN; i++) fprintf(stderr, " %s=%lld", names[i], sum[i]);
+    fprintf(stderr, "\n[sched prof] slowest scenario %d:", slow);
+    for (int i = 0; i < kProfN; i++) fprintf(stderr, " %s=%lld", names[i], h[(size_t)slow * kProfN + i]);
+    fprintf(stderr, "\n");
   }
 };
 
@@ -626,6 +690,14 @@ int emu_sched_create(int32_t S, const int64_t* req_off, const int32_t* prompt, c
       (rc = sc->alloc(&a.o_fin, SM)) || (rc = sc->alloc(&a.o_pre, SM))) {
     delete sc;
     return rc;
+  }
+  const char* pe = getenv("EMU_SCHED_PROF");
+  if (pe && pe[0] == '1') {
+    if ((rc = sc->alloc(&a.prof, (int64_t)S * kProfN)) ||
+        cudaMemset(a.prof, 0, 8 * (size_t)S * kProfN) != cudaSuccess) {
+      delete sc;
+      return rc ? rc : cuda_fail(cudaGetLastError(), "prof");
+    }
   }
   a.roff = d_roff;
   a.woff = d_woff;
