@@ -37,11 +37,13 @@
 namespace emu {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kPf = 8;  // chunks of 32 requests whose loads are issued together
 enum : uint8_t { RQ_WAITING = 0, RQ_PREFILLING = 1, RQ_DECODING = 2, RQ_PREEMPTED = 3, RQ_FINISHED = 4 };
 enum : int32_t { SC_RUNNING = 0, SC_DONE = 1, SC_PAUSED = 2, SC_ERROR = 3 };
 
 struct SchedArgs {
   int32_t num_blocks, block_size, max_batched, max_seqs;
+  int32_t bs_shift;  // log2(block_size) when it is a power of two, else -1
   int64_t max_steps;
   int32_t S;
   // requests (per scenario slice [roff[s], roff[s+1]))
@@ -95,6 +97,7 @@ struct SchedArgs {
   const double* s1;
   // EMU_SCHED_PROF=1: per-scenario cycle / event counters [S * kProfN]
   long long* prof;
+  int32_t smem;  // running list + entries in dynamic shared memory (17 B x max_seqs)
 };
 // prof slots: cycles in admit, decode pass, prefill pass, draw, apply+compact;
 // then counts: steps, sequential-remainder iterations, waiting candidates,
@@ -118,9 +121,12 @@ struct Scen {
   long long nseq = 0, ncand = 0, nwords = 0, nshift = 0;  // EMU_SCHED_PROF counters
   long long t_dec = 0;                                     // clock at the end of the decode pass
   int32_t lim = 0;  // requests admitted so far: every waiting id is below it
+  int32_t cap = 0;  // capacity of run / snp (max_seqs when they live in shared memory)
 
+  // token counts stay below max_model_len + max_num_batched_tokens: 32-bit division
   __device__ int32_t blocks_needed(int64_t tokens) const {
-    return (int32_t)((tokens + A.block_size - 1) / A.block_size);
+    const uint32_t n = (uint32_t)tokens + (uint32_t)A.block_size - 1u;
+    return (int32_t)(A.bs_shift >= 0 ? n >> A.bs_shift : n / (uint32_t)A.block_size);
   }
   __device__ void wait_insert(int32_t r) {
     wb[r >> 5] |= 1u << (r & 31);
@@ -199,6 +205,10 @@ struct Scen {
     } else {
       if (demand > freeb) return false;
       wait_remove(r);
+      if (nrun >= cap) {  // cannot happen: admissions need every running request to hold an entry
+        err = true;
+        return false;
+      }
       run[nrun++] = r;
       A.rphase[g] = RQ_PREFILLING;
     }
@@ -222,54 +232,119 @@ struct Scen {
     const int32_t ns = nrun;
     for (int32_t k = lane; k < ns; k += 32) snp[k] = run[k];
     __syncwarp();
-    // decoding requests first, one token each.  Per chunk of 32: if the KV
-    // demand of every admitted decode entry fits in the free blocks, no
-    // make_room can fire and the chunk commits in parallel (same order, same
-    // final state); otherwise commit up to the first entry that would have to
-    // preempt and finish the pass sequentially.
+    // decoding requests first, one token each.  Per group of 32 x kPf
+    // requests (lane-contiguous): decode ranks and the KV demand of the
+    // admitted ones come from two warp scans; if every admitted entry's demand
+    // fits in the free blocks, no make_room can fire and the group commits at
+    // once (same order, same final state); otherwise commit up to the first
+    // entry that would have to preempt and finish the pass sequentially.
     int32_t k_seq = ns;  // where the sequential remainder starts (ns = none)
     bool stop = false;
-    for (int32_t base = 0; base < ns && !stop; base += 32) {
-      const int32_t k = base + lane;
-      int32_t r = -1, demand = 0;
-      bool dec = false;
-      if (k < ns) {
-        r = snp[k];
-        const int64_t g = r0 + r;
-        dec = A.rphase[g] == RQ_DECODING;
-        if (dec) demand = blocks_needed((int64_t)A.progress[g] + A.generated[g] + 1) - A.alloc[g];
+    for (int32_t base0 = 0; base0 < ns && !stop; base0 += 32 * kPf) {
+      const int32_t kl = base0 + kPf * lane;
+      int32_t rr[kPf], dmd[kPf], al[kPf];
+      bool dc[kPf];
+#pragma unroll
+      for (int i = 0; i < kPf; i++) {
+        rr[i] = -1;
+        dmd[i] = 0;
+        al[i] = 0;
+        dc[i] = false;
+        if (kl + i < ns) {
+          const int32_t r = snp[kl + i];
+          const int64_t g = r0 + r;
+          rr[i] = r;
+          const uint8_t ph = A.rphase[g];
+          const int32_t pg = A.progress[g], gn = A.generated[g];
+          al[i] = A.alloc[g];
+          dc[i] = ph == RQ_DECODING;
+          dmd[i] = blocks_needed((int64_t)pg + gn + 1) - al[i];
+        }
       }
-      const unsigned dm = __ballot_sync(kFull, dec);
-      const int32_t allow = min(budget, A.max_seqs - ne);
-      const int32_t rank = __popc(dm & lt);
-      const bool ok = dec && rank < allow;
-      int32_t cum = ok && demand > 0 ? demand : 0;
+      int32_t cnt = 0;
+#pragma unroll
+      for (int i = 0; i < kPf; i++) cnt += dc[i] ? 1 : 0;
+      int32_t rk = cnt;  // inclusive scan of decode counts
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(kFull, cum, o);
-        if (lane >= o) cum += y;
+        const int32_t y = __shfl_up_sync(kFull, rk, o);
+        if (lane >= o) rk += y;
       }
-      const unsigned fail = __ballot_sync(kFull, ok && cum > freeb);
-      const unsigned okm = __ballot_sync(kFull, ok) & (fail ? ((1u << (__ffs(fail) - 1)) - 1u) : kFull);
-      if (okm & (1u << lane)) {
-        const int64_t g = r0 + r;
-        if (demand > 0) A.alloc[g] += demand;
-        const int32_t e = ne + __popc(okm & lt);
-        eid[e] = r;
-        ech[e] = 1;
-        epr[e] = 0;
-        A.eidx[g] = e;
+      const int32_t ndec = __shfl_sync(kFull, rk, 31);
+      rk -= cnt;  // decode rank of this lane's first request
+      const int32_t allow = min(budget, A.max_seqs - ne);
+      bool ok[kPf];
+      int32_t lc[kPf], dsum = 0;
+      {
+        int32_t q = rk;
+#pragma unroll
+        for (int i = 0; i < kPf; i++) {
+          ok[i] = dc[i] && q < allow;
+          q += dc[i] ? 1 : 0;
+          dsum += ok[i] && dmd[i] > 0 ? dmd[i] : 0;
+          lc[i] = dsum;
+        }
       }
-      const int32_t nok = __popc(okm);
-      const int32_t used = __shfl_sync(kFull, cum, okm ? 31 - __clz(okm) : 0);
-      if (okm) freeb -= used;
-      ne += nok;
-      budget -= nok;
+      int32_t dx = dsum;  // inclusive scan of admitted demand
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(kFull, dx, o);
+        if (lane >= o) dx += y;
+      }
+      const int32_t dtot = __shfl_sync(kFull, dx, 31);
+      dx -= dsum;
+      int32_t fi = kPf;
+#pragma unroll
+      for (int i = kPf - 1; i >= 0; i--)
+        if (ok[i] && dx + lc[i] > freeb) fi = i;
+      const unsigned fl = __ballot_sync(kFull, fi < kPf);
+      int32_t fpos = ns, ncom, used;
+      if (fl) {
+        const int src = __ffs(fl) - 1;
+        // the failing entry's rank = entries committed; demand before it
+        int32_t frank = 0, fused = 0;
+        if (lane == src) {
+          int32_t q = rk, u = 0;
+#pragma unroll
+          for (int i = 0; i < kPf; i++)
+            if (i < fi) {
+              q += dc[i] ? 1 : 0;
+              u += ok[i] && dmd[i] > 0 ? dmd[i] : 0;
+            }
+          frank = q;
+          fused = dx + u;
+        }
+        fpos = base0 + kPf * src + __shfl_sync(kFull, fi, src);
+        ncom = __shfl_sync(kFull, frank, src);
+        used = __shfl_sync(kFull, fused, src);
+      } else {
+        ncom = min(ndec, allow);
+        used = dtot;
+      }
+      {
+        int32_t q = rk;
+#pragma unroll
+        for (int i = 0; i < kPf; i++) {
+          if (ok[i] && kl + i < fpos) {
+            const int64_t g = r0 + rr[i];
+            if (dmd[i] > 0) A.alloc[g] = al[i] + dmd[i];
+            const int32_t e = ne + q;
+            eid[e] = rr[i];
+            ech[e] = 1;
+            epr[e] = 0;
+            A.eidx[g] = e;
+          }
+          q += dc[i] ? 1 : 0;
+        }
+      }
+      freeb -= used;
+      ne += ncom;
+      budget -= ncom;
       __syncwarp();
-      if (fail) {
-        k_seq = base + __ffs(fail) - 1;
+      if (fl) {
+        k_seq = fpos;
         stop = true;
-      } else if (__popc(dm) > allow) {
+      } else if (ndec > allow) {
         stop = true;  // the reference breaks at the first decode request over the budget
       }
     }
@@ -292,14 +367,22 @@ struct Scen {
     if (A.prof) t_dec = clock64();
     // prefills: running partial prefills, then the waiting queue (both as of now)
     int32_t nc = 0;
-    for (int32_t base = 0; base < nrun; base += 32) {
-      const int32_t k = base + lane;
-      const int32_t r = k < nrun ? run[k] : 0;
-      const bool pf = k < nrun && A.rphase[r0 + r] == RQ_PREFILLING;
-      const unsigned m = __ballot_sync(kFull, pf);
-      __syncwarp();
-      if (pf) snp[nc + __popc(m & lt)] = r;
-      nc += __popc(m);
+    __syncwarp();
+    for (int32_t base0 = 0; base0 < nrun; base0 += 32 * kPf) {
+      int32_t pr[kPf];
+      bool pf[kPf];
+#pragma unroll
+      for (int j = 0; j < kPf; j++) {
+        const int32_t k = base0 + 32 * j + lane;
+        pr[j] = k < nrun ? run[k] : 0;
+        pf[j] = k < nrun && A.rphase[r0 + pr[j]] == RQ_PREFILLING;
+      }
+#pragma unroll
+      for (int j = 0; j < kPf; j++) {
+        const unsigned m = __ballot_sync(kFull, pf[j]);
+        if (pf[j]) snp[nc + __popc(m & lt)] = pr[j];
+        nc += __popc(m);
+      }
     }
     __syncwarp();
     const int32_t snap_evt = evt;
@@ -335,6 +418,28 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
   Scen c{A, s, r0, (int32_t)(A.roff[s + 1] - r0), A.running + r0, A.snap + r0, A.wbits + A.woff[s],
          A.ent_id + (int64_t)s * A.max_seqs, A.ent_chunk + (int64_t)s * A.max_seqs, A.ent_pre + (int64_t)s * A.max_seqs,
          A.nrun[s], A.wfront[s], A.free_blocks[s], A.evt[s], A.n_ent[s], 0, A.preempt[s], false};
+  c.cap = c.R;
+  // running list, its snapshot and the step's entries live in shared memory
+  // when max_seqs allows (running <= max_seqs: an admission needs every running
+  // request to hold one of the <= max_seqs entries)
+  extern __shared__ __align__(16) unsigned char dsm[];
+  if (A.smem) {
+    const int32_t q = A.max_seqs;
+    int32_t* rs = reinterpret_cast<int32_t*>(dsm);
+    for (int32_t k = lane; k < c.nrun; k += 32) rs[k] = c.run[k];
+    for (int32_t k = lane; k < c.ne; k += 32) {
+      rs[2 * q + k] = c.eid[k];
+      rs[3 * q + k] = c.ech[k];
+      reinterpret_cast<uint8_t*>(rs + 4 * q)[k] = c.epr[k];
+    }
+    c.run = rs;
+    c.snp = rs + q;
+    c.eid = rs + 2 * q;
+    c.ech = rs + 3 * q;
+    c.epr = reinterpret_cast<uint8_t*>(rs + 4 * q);
+    c.cap = q;
+    __syncwarp();
+  }
   double t = A.t[s];
   int32_t nxt = A.next_arr[s];
   int64_t step = A.nsteps[s];
@@ -353,14 +458,13 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
   int32_t* key = A.key + 3 * (int64_t)s;
   const bool P = A.prof != nullptr;
   const int64_t step0 = step;
-  long long pc[5] = {0, 0, 0, 0, 0}, tc = P ? clock64() : 0;
-  auto lap = [&](int i) {
-    if (P) {
-      const long long n = clock64();
-      pc[i] += n - tc;
-      tc = n;
-    }
-  };
+  long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0, pc4 = 0, tc = P ? clock64() : 0;
+#define EMU_LAP(acc)                 \
+  if (P) {                           \
+    const long long n_ = clock64();  \
+    acc += n_ - tc;                  \
+    tc = n_;                         \
+  }
   while (step < A.max_steps) {
     if (!resume) {
       while (nxt < c.R && A.arrival[r0 + nxt] <= t) {  // admit (engine.py:323-340)
@@ -374,13 +478,13 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
         c.wait_insert(nxt);
         nxt++;
       }
-      lap(0);
+      EMU_LAP(pc0);
       c.lim = nxt;
       const int32_t ne = c.schedule();
       if (P) {
-        pc[1] += c.t_dec - tc;
+        pc1 += c.t_dec - tc;
         tc = c.t_dec;
-        lap(2);
+        EMU_LAP(pc2);
       }
       if (c.err) {
         st = SC_ERROR;
@@ -395,11 +499,14 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
         continue;
       }
       int32_t tt = 0;
-      bool all_decode = true;
-      for (int32_t k = 0; k < ne; k++) {
+      bool mixed = false;
+      for (int32_t k = lane; k < ne; k += 32) {
         tt += c.ech[k];
-        all_decode &= c.epr[k] == 0;
+        mixed |= c.epr[k] != 0;
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(kFull, tt, o);
+      const bool all_decode = !__any_sync(kFull, mixed);
       key[0] = tt;
       key[1] = ne;
       key[2] = all_decode ? 0 : 1;
@@ -443,33 +550,61 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
       }
       lat = __ldcg((ph ? A.s1 : A.s0) + pk.soff + (int32_t)j);
     }
-    lap(3);
+    EMU_LAP(pc3);
     // _apply_outcome (engine.py:464-483): entries are distinct requests, so the
     // per-entry updates run lane-parallel; finished requests leave the running
     // list in one order-preserving compaction.
     int32_t tokens = 0, fin = 0, freed = 0;
     bool dfree = false;
-    for (int32_t k = lane; k < c.ne; k += 32) {
-      const int32_t r = c.eid[k];
-      const int64_t gi = r0 + r;
-      A.eidx[gi] = -1;
-      if (c.epr[k]) {
-        A.progress[gi] += c.ech[k];
-        if (A.progress[gi] == A.prompt[gi]) {
-          A.rphase[gi] = RQ_DECODING;
-          A.generated[gi] += 1;
+    for (int32_t kb = 0; kb < c.ne; kb += 32 * kPf) {
+      int32_t er[kPf], ech[kPf], epg[kPf], epl[kPf], egn[kPf], etg[kPf], eal[kPf];
+      uint8_t eph[kPf], epr[kPf];
+#pragma unroll
+      for (int j = 0; j < kPf; j++) {
+        const int32_t k = kb + 32 * j + lane;
+        er[j] = -1;
+        if (k < c.ne) {
+          const int32_t r = c.eid[k];
+          const int64_t gi = r0 + r;
+          er[j] = r;
+          ech[j] = c.ech[k];
+          epr[j] = c.epr[k];
+          epg[j] = A.progress[gi];
+          epl[j] = A.prompt[gi];
+          egn[j] = A.generated[gi];
+          etg[j] = A.target[gi];
+          eal[j] = A.alloc[gi];
+          eph[j] = A.rphase[gi];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kPf; j++) {
+        if (er[j] < 0) continue;
+        const int64_t gi = r0 + er[j];
+        A.eidx[gi] = -1;
+        uint8_t ph = eph[j];
+        int32_t gn = egn[j];
+        if (epr[j]) {
+          const int32_t pg = epg[j] + ech[j];
+          A.progress[gi] = pg;
+          if (pg == epl[j]) {
+            ph = RQ_DECODING;
+            gn += 1;
+            tokens++;
+          }
+        } else {
+          gn += 1;
           tokens++;
         }
-      } else {
-        A.generated[gi] += 1;
-        tokens++;
-      }
-      if (A.rphase[gi] == RQ_DECODING && A.generated[gi] >= A.target[gi]) {
-        A.rphase[gi] = RQ_FINISHED;
-        dfree |= A.alloc[gi] == 0;
-        freed += A.alloc[gi];
-        A.alloc[gi] = 0;
-        fin++;
+        if (ph == RQ_DECODING && gn >= etg[j]) {
+          ph = RQ_FINISHED;
+          dfree |= eal[j] == 0;
+          freed += eal[j];
+          A.alloc[gi] = 0;
+          fin++;
+        }
+        if (gn != egn[j]) A.generated[gi] = gn;
+        if (ph != eph[j]) A.rphase[gi] = ph;
       }
     }
 #pragma unroll
@@ -483,14 +618,22 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
     __syncwarp();
     if (fin) {
       int32_t out = 0;
-      for (int32_t base = 0; base < c.nrun; base += 32) {
-        const int32_t k = base + lane;
-        const int32_t r = k < c.nrun ? c.run[k] : 0;
-        const bool keep = k < c.nrun && A.rphase[r0 + r] != RQ_FINISHED;
-        const unsigned m = __ballot_sync(kFull, keep);
+      for (int32_t base0 = 0; base0 < c.nrun; base0 += 32 * kPf) {
+        int32_t pr[kPf];
+        bool keep[kPf];
+#pragma unroll
+        for (int j = 0; j < kPf; j++) {
+          const int32_t k = base0 + 32 * j + lane;
+          pr[j] = k < c.nrun ? c.run[k] : 0;
+          keep[j] = k < c.nrun && A.rphase[r0 + pr[j]] != RQ_FINISHED;
+        }
         __syncwarp();
-        if (keep) c.run[out + __popc(m & lt)] = r;
-        out += __popc(m);
+#pragma unroll
+        for (int j = 0; j < kPf; j++) {
+          const unsigned m = __ballot_sync(kFull, keep[j]);
+          if (keep[j]) c.run[out + __popc(m & lt)] = pr[j];
+          out += __popc(m);
+        }
         __syncwarp();
       }
       c.nrun = out;
@@ -510,11 +653,15 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
     c.ne = 0;
     t = __dadd_rn(t, lat);
     step++;
-    lap(4);
+    EMU_LAP(pc4);
   }
   if (P && lane == 0) {
     long long* q = A.prof + (int64_t)s * kProfN;
-    for (int i = 0; i < 5; i++) q[i] += pc[i];
+    q[0] += pc0;
+    q[1] += pc1;
+    q[2] += pc2;
+    q[3] += pc3;
+    q[4] += pc4;
     q[5] += step - step0;
     q[6] += c.nseq;
     q[7] += c.ncand;
@@ -531,6 +678,17 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
   A.evt[s] = c.evt;
   A.preempt[s] = c.npre;
   A.n_ent[s] = c.ne;
+  if (A.smem) {  // back to the scenario's global slices for the next launch
+    __syncwarp();
+    int32_t* gr = A.running + r0;
+    const int64_t e0 = (int64_t)s * A.max_seqs;
+    for (int32_t k = lane; k < c.nrun; k += 32) gr[k] = c.run[k];
+    for (int32_t k = lane; k < c.ne; k += 32) {
+      A.ent_id[e0 + k] = c.eid[k];
+      A.ent_chunk[e0 + k] = c.ech[k];
+      A.ent_pre[e0 + k] = c.epr[k];
+    }
+  }
   A.status[s] = st;
   if (st != SC_PAUSED) A.resume[s] = 0;
   if (MODE == 2) {
@@ -593,6 +751,9 @@ struct emu_sched_s {
 };
 
 static std::string fmt_i(int64_t v) { return std::to_string(v); }
+
+static size_t sched_smem_bytes(int32_t max_seqs) { return ((size_t)17 * max_seqs + 15) & ~(size_t)15; }
+constexpr size_t kSchedSmemMax = 160 * 1024;  // larger max_num_seqs keep the lists in global memory
 
 static int sched_reset(emu_sched_t sc, cudaStream_t s) {
   SchedArgs& a = sc->a;
@@ -666,6 +827,10 @@ int emu_sched_create(int32_t S, const int64_t* req_off, const int32_t* prompt, c
   SchedArgs& a = sc->a;
   a.num_blocks = num_gpu_blocks;
   a.block_size = block_size;
+  a.bs_shift = -1;
+  if ((block_size & (block_size - 1)) == 0)
+    for (int b = 0; b < 31; b++)
+      if ((1 << b) == block_size) a.bs_shift = b;
   a.max_batched = max_num_batched_tokens;
   a.max_seqs = max_num_seqs;
   a.max_steps = max_steps;
@@ -720,9 +885,17 @@ void emu_sched_destroy(emu_sched_t sc) { delete sc; }
 
 static int launch_sched(emu_sched_t sc, int mode, cudaStream_t s) {
   const int grid = sc->S;
-  if (mode == 0) EMU_LAUNCH("sched", s, k_sched<0><<<grid, 32, 0, s>>>(sc->a));
-  if (mode == 1) EMU_LAUNCH("sched", s, k_sched<1><<<grid, 32, 0, s>>>(sc->a));
-  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, 32, 0, s>>>(sc->a));
+  const size_t sm = sched_smem_bytes(sc->a.max_seqs);
+  sc->a.smem = sm <= kSchedSmemMax ? 1 : 0;
+  const size_t dyn = sc->a.smem ? sm : 0;
+  if (dyn > 48 * 1024) {
+    EMU_CUDA(cudaFuncSetAttribute(k_sched<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    EMU_CUDA(cudaFuncSetAttribute(k_sched<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    EMU_CUDA(cudaFuncSetAttribute(k_sched<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  }
+  if (mode == 0) EMU_LAUNCH("sched", s, k_sched<0><<<grid, 32, dyn, s>>>(sc->a));
+  if (mode == 1) EMU_LAUNCH("sched", s, k_sched<1><<<grid, 32, dyn, s>>>(sc->a));
+  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, 32, dyn, s>>>(sc->a));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
 }
