@@ -37,7 +37,7 @@
 namespace emu {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kPf = 8;  // chunks of 32 requests whose loads are issued together
+constexpr int kPf = 4;  // chunks of 32 requests whose loads are issued together
 enum : uint8_t { RQ_WAITING = 0, RQ_PREFILLING = 1, RQ_DECODING = 2, RQ_PREEMPTED = 3, RQ_FINISHED = 4 };
 enum : int32_t { SC_RUNNING = 0, SC_DONE = 1, SC_PAUSED = 2, SC_ERROR = 3 };
 
