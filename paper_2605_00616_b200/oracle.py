@@ -15,6 +15,7 @@ call for trace replay / what-if sweeps) and ``pools`` (explicit pool CSR).
 """
 from __future__ import annotations
 
+import collections
 import ctypes
 import weakref
 from dataclasses import dataclass
@@ -113,7 +114,10 @@ def normalized_distance(query: tuple[int, int], bucket: tuple[int, int], tt_rang
 # Device tables + oracle handles for packs/tables used through the functional
 # API, keyed by object identity (the reference's pack/table classes define
 # __eq__ and are unhashable) and invalidated if the content size changes.
-_tables_cache: dict[int, tuple] = {}
+# Bounded (least recently used first out): an entry made by sample_latency
+# holds its pack, so the weakref alone would never release it.
+_tables_cache: "collections.OrderedDict[int, tuple]" = collections.OrderedDict()
+_TABLES_CACHE_MAX = 16
 
 
 def _nbuckets(t) -> int:
@@ -148,6 +152,9 @@ def _cached_oracle(obj, tables, make_pack, floor: int, p: float, eps: float) -> 
         ref = weakref.ref(obj, lambda _r, k=key: _tables_cache.pop(k, None))
         entry = (ref, fp, make_pack(), {})
         _tables_cache[key] = entry
+        while len(_tables_cache) > _TABLES_CACHE_MAX:
+            _tables_cache.popitem(last=False)
+    _tables_cache.move_to_end(key)
     oracles = entry[3]
     okey = (floor, p, eps)
     if okey not in oracles:

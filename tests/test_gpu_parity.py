@@ -426,3 +426,22 @@ def test_device_tables_roundtrip(c1_pack):
         assert soa_equal(s, O.Table(*[getattr(c1_pack.soas()[i], k) for k in ("tt", "conc", "off", "samples")]))
     arrs = dt.device_arrays(2)
     assert arrs["row_start"][-1].item() == dt.info(2)["n_buckets"]
+
+
+def test_functional_api_cache_is_bounded():
+    """sample_latency on many distinct packs keeps at most _TABLES_CACHE_MAX
+    device oracles alive (entries hold their pack, so the weakref alone would
+    never release them)."""
+    from paper_2605_00616_b200 import oracle as orc_mod
+    from paper_2605_00616_b200.oracle import OracleQuery, sample_latency
+    from paper_2605_00616_b200.profile import Bucket, PhaseTable, ProfilePack, StepPhase, TableKind
+
+    rng = np.random.default_rng(0)
+    for i in range(3 * orc_mod._TABLES_CACHE_MAX):
+        b = [Bucket(4 + i, 2, [0.01 + 0.001 * i]), Bucket(9, 3, [0.02, 0.03])]
+        pack = ProfilePack(1, PhaseTable.from_buckets(TableKind.DECODE, []),
+                           PhaseTable.from_buckets(TableKind.MIXED, b), PhaseTable.from_buckets(TableKind.COMBINED, b))
+        v = sample_latency(pack, OracleQuery(4 + i, 2, StepPhase.PREFILL_OR_MIXED), OracleConfig(reliability_floor=1),
+                           rng)
+        assert v == 0.01 + 0.001 * i
+        assert len(orc_mod._tables_cache) <= orc_mod._TABLES_CACHE_MAX
