@@ -1284,7 +1284,16 @@ static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
 
 static int64_t map_entries(emu_oracle_t o) { return 2LL * o->map.dom_tt * o->map.dom_conc + 2 * o->map.hcap; }
 
-constexpr int kPrepGrid = kNumSMs * 4;
+static int grid_knob(int which, int dflt) {  // EMU_GRIDS=<prep>,<sample> CTAs per SM (tuning)
+  static int g[2] = {-1, -1};
+  if (g[0] < 0) {
+    g[0] = 4;
+    g[1] = 16;
+    if (const char* v = getenv("EMU_GRIDS")) sscanf(v, "%d,%d", &g[0], &g[1]);
+  }
+  return g[which] > 0 ? g[which] : dflt;
+}
+#define kPrepGrid (kNumSMs * grid_knob(0, 4))
 
 // Build missing pools for a chunk of queries: mark -> prep (thread/key) ->
 // warp (sort, prefix, CDF) -> CTA escalation.  No host round trip.
@@ -1394,7 +1403,7 @@ template <int RNG, int QPT, bool HINT>
 static void launch_sample_t(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t n,
                             const uint64_t* us, const uint32_t* ui, uint64_t seed, uint64_t ctr, double* lat,
                             int32_t* sidx, cudaStream_t s) {
-  const int grid = grid_for((n + QPT - 1) / QPT, kSampleThreads, kNumSMs * 16);
+  const int grid = grid_for((n + QPT - 1) / QPT, kSampleThreads, kNumSMs * grid_knob(1, 16));
   EMU_LAUNCH("sample", s, k_sample<RNG, QPT, HINT><<<grid, kSampleThreads, 0, s>>>(
                               o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, n, us, ui, seed,
                               ctr, lat, sidx, &o->ctl->flags));
