@@ -352,7 +352,7 @@ def sweep(args):
     return {"config": "sweep", "workload": f"{len(scen)} scenarios (rate x burstiness) x up to {steps} steps, "
                                             "reference scheduler + oracle closed loop on the GPU",
             "steps_total": total, "wall_s": wall, "steps_per_s": total / wall, "rounds": out["rounds"],
-            "tokens_total": int(out["tokens"].sum()), "requests": int(sum(len(s.prompt_tokens) for s in scen)),
+            "tokens_total": int(out["tokens"].sum()), "host_s": out["host_s"], "requests": int(sum(len(s.prompt_tokens) for s in scen)),
             "cpu_reference_note": "the reference engine + LatencyOracle runs ~4k steps/s per core in virtual time "
                                   "(tests/golden/make_sched_golden.py: 21k steps in ~5 s)"}
 

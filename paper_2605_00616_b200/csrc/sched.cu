@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -803,21 +805,43 @@ int emu_sched_create(int32_t S, const int64_t* req_off, const int32_t* prompt, c
     woff[s + 1] = woff[s] + (n + 31) / 32;
   }
   const int64_t R = roff[S];
-  // admission checks (engine.py:323-336) and ascending arrival offsets
-  for (int32_t s = 0; s < S; s++)
-    for (int64_t i = roff[s]; i < roff[s + 1]; i++) {
-      if (prompt[i] < 1) return fail(EMU_ERR_INVALID, "prompt_tokens must be >= 1, got " + fmt_i(prompt[i]));
-      if (target[i] < 1) return fail(EMU_ERR_INVALID, "max_tokens must be >= 1, got " + fmt_i(target[i]));
+  // admission checks (engine.py:323-336) and ascending arrival offsets; the
+  // request table is split over host threads, the first bad request reports
+  std::atomic<int64_t> first_bad{R};
+  auto check_range = [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi && i < first_bad.load(std::memory_order_relaxed); i++) {
       const int64_t total = (int64_t)prompt[i] + target[i];
-      if (total > max_model_len)
-        return fail(EMU_ERR_INVALID, "prompt_tokens + max_tokens = " + fmt_i(total) + " exceeds max_model_len " +
-                                         fmt_i(max_model_len));
-      const int64_t fb = (total + block_size - 1) / block_size;
-      if (fb > num_gpu_blocks)
-        return fail(EMU_ERR_INVALID, "request needs " + fmt_i(fb) + " KV blocks but the engine has only " +
-                                         fmt_i(num_gpu_blocks));
-      if (i > roff[s] && arrival[i] < arrival[i - 1]) return fail(EMU_ERR_INVALID, "arrival offsets must ascend");
+      const bool bad = prompt[i] < 1 || target[i] < 1 || total > max_model_len ||
+                       (total + block_size - 1) / block_size > num_gpu_blocks ||
+                       (i > 0 && arrival[i] < arrival[i - 1] && !std::binary_search(roff.begin(), roff.end(), i));
+      if (bad) {
+        int64_t cur = first_bad.load();
+        while (i < cur && !first_bad.compare_exchange_weak(cur, i)) {
+        }
+        return;
+      }
     }
+  };
+  {
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), R / (1 << 20)));
+    std::vector<std::thread> th;
+    for (int k = 0; k < nt; k++) th.emplace_back(check_range, R * k / nt, R * (k + 1) / nt);
+    for (auto& t : th) t.join();
+  }
+  if (first_bad.load() < R) {
+    const int64_t i = first_bad.load();
+    if (prompt[i] < 1) return fail(EMU_ERR_INVALID, "prompt_tokens must be >= 1, got " + fmt_i(prompt[i]));
+    if (target[i] < 1) return fail(EMU_ERR_INVALID, "max_tokens must be >= 1, got " + fmt_i(target[i]));
+    const int64_t total = (int64_t)prompt[i] + target[i];
+    if (total > max_model_len)
+      return fail(EMU_ERR_INVALID, "prompt_tokens + max_tokens = " + fmt_i(total) + " exceeds max_model_len " +
+                                       fmt_i(max_model_len));
+    const int64_t fb = (total + block_size - 1) / block_size;
+    if (fb > num_gpu_blocks)
+      return fail(EMU_ERR_INVALID, "request needs " + fmt_i(fb) + " KV blocks but the engine has only " +
+                                       fmt_i(num_gpu_blocks));
+    return fail(EMU_ERR_INVALID, "arrival offsets must ascend");
+  }
   auto* sc = new emu_sched_s();
   sc->S = S;
   sc->R = R;

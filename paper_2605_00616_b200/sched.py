@@ -20,6 +20,8 @@ reference's ``generate_workload`` / ``generate_arrivals`` (bench.py:77-116).
 from __future__ import annotations
 
 import ctypes
+import os
+import time
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -73,6 +75,30 @@ def prefetch_domain(oracle: LatencyOracle, config: EngineConfig) -> int:
     return len(tt)
 
 
+def _concat(parts, off: np.ndarray, dtype) -> np.ndarray:
+    """np.concatenate into one request table, scenario slices copied by a thread
+    pool (numpy copies release the GIL; large sweeps are first-touch bound)."""
+    out = np.empty(int(off[-1]), dtype)
+    if off[-1] < (1 << 22) or len(parts) == 1:
+        for k, p in enumerate(parts):
+            out[off[k]:off[k + 1]] = np.asarray(p)
+        return out
+    from concurrent.futures import ThreadPoolExecutor
+
+    def put(k):
+        out[off[k]:off[k + 1]] = np.asarray(parts[k])
+
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(put, range(len(parts))))
+    return out
+
+
+def _phases(tm: dict) -> dict:
+    """Seconds per phase of emulate() (wall clock, host side; `run` includes the kernel)."""
+    ks = list(tm)
+    return {b: round(tm[b] - tm[a], 4) for a, b in zip(ks, ks[1:])}
+
+
 def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int, *, backend: str = "oracle",
             oracle: LatencyOracle | None = None, seeds: Sequence[int] | None = None,
             gt_params: GroundTruthParams | None = None, gt_seed: int = 0, latencies=None,
@@ -82,18 +108,21 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
     oracle backend, `prefetch` (default: when the key domain has <= 2M keys)
     builds every reachable pool first, so the closed loop runs in one launch."""
     _lib.require_cuda()
+    tm = {"start": time.perf_counter()}
     S = len(scenarios)
     off = np.zeros(S + 1, np.int64)
     off[1:] = np.cumsum([len(sc.prompt_tokens) for sc in scenarios])
-    prompt = np.ascontiguousarray(np.concatenate([np.asarray(sc.prompt_tokens) for sc in scenarios]), np.int32)
-    target = np.ascontiguousarray(np.concatenate([np.asarray(sc.output_tokens) for sc in scenarios]), np.int32)
-    arrival = np.ascontiguousarray(np.concatenate([np.asarray(sc.arrival_s) for sc in scenarios]), np.float64)
+    prompt = _concat([sc.prompt_tokens for sc in scenarios], off, np.int32)
+    target = _concat([sc.output_tokens for sc in scenarios], off, np.int32)
+    arrival = _concat([sc.arrival_s for sc in scenarios], off, np.float64)
     L = _lib.lib()
     h = ctypes.c_void_p()
+    tm["concat"] = time.perf_counter()
     _lib.check(L.emu_sched_create(S, _lib.ptr(off), _lib.ptr(prompt), _lib.ptr(target), _lib.ptr(arrival),
                                   int(config.num_gpu_blocks), int(config.block_size), int(config.max_model_len),
                                   int(config.max_num_batched_tokens), int(config.max_num_seqs), int(max_steps),
                                   ctypes.byref(h)))
+    tm["create"] = time.perf_counter()
     try:
         rounds = ctypes.c_int64(0)
         if backend == "oracle":
@@ -105,6 +134,7 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
             domain = config.max_num_seqs * config.max_num_batched_tokens
             if prefetch or (prefetch is None and domain <= 2_000_000):
                 prefetch_domain(oracle, config)
+            tm["prefetch"] = time.perf_counter()
             _lib.check(L.emu_sched_run_oracle(h, oracle._h, _lib.ptr(st), ctypes.byref(rounds), _lib.stream_ptr()))
         elif backend == "ground_truth":
             p = gt_params or GroundTruthParams()
@@ -120,6 +150,7 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
             _lib.check(L.emu_sched_run_replay(h, _lib.ptr(lat), _lib.stream_ptr()))
         else:
             raise ValueError(f"unknown backend {backend!r}")
+        tm["run"] = time.perf_counter()
         n = np.zeros(S, np.int64)
         status = np.zeros(S, np.int32)
         if not keep_steps:  # totals only (long sweeps): no per-step arrays cross PCIe
@@ -128,8 +159,9 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
             _lib.check(L.emu_sched_results(h, None, _lib.ptr(status), None, None, None, None, None, None, None))
             if (status == 3).any():
                 raise RuntimeError(f"scheduler invariant violated in scenarios {np.flatnonzero(status == 3).tolist()}")
+            tm["results"] = time.perf_counter()
             return {"n_steps": summ[:, 0], "tokens": summ[:, 1], "finished": summ[:, 2], "preemptions": summ[:, 3],
-                    "rounds": int(rounds.value)}
+                    "rounds": int(rounds.value), "host_s": _phases(tm)}
         out = {k: np.zeros((S, max_steps), dt) for k, dt in (("tt", np.int32), ("conc", np.int32), ("phase", np.uint8),
                                                               ("latency_s", np.float64), ("tokens", np.int32),
                                                               ("finished", np.int32), ("preemptions", np.int64))}
@@ -140,6 +172,8 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
             raise RuntimeError(f"scheduler invariant violated in scenarios {np.flatnonzero(status == 3).tolist()}")
         out["n_steps"] = n
         out["rounds"] = int(rounds.value)
+        tm["results"] = time.perf_counter()
+        out["host_s"] = _phases(tm)
         return out
     finally:
         L.emu_sched_destroy(h)
