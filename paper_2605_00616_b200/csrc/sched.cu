@@ -911,6 +911,8 @@ static int launch_sched(emu_sched_t sc, int mode, cudaStream_t s) {
   const int grid = sc->S;
   const size_t sm = sched_smem_bytes(sc->a.max_seqs);
   sc->a.smem = sm <= kSchedSmemMax ? 1 : 0;
+  if (const char* v = getenv("EMU_SCHED_SMEM"))  // 0: force the global-memory lists (tests)
+    if (v[0] == '0') sc->a.smem = 0;
   const size_t dyn = sc->a.smem ? sm : 0;
   if (dyn > 48 * 1024) {
     EMU_CUDA(cudaFuncSetAttribute(k_sched<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));

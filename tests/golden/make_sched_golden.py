@@ -68,6 +68,11 @@ def main():
                                   max_num_seqs=32), (3000, 300, 150, 8), (20.0, 1.0, 43)),
         "gt_bursty": (EngineConfig(num_gpu_blocks=1024, block_size=16, max_model_len=4096, max_num_batched_tokens=384,
                                    max_num_seqs=48), (3000, 150, 80, 9), (16.0, 0.25, 44)),
+        # max_num_seqs > 128: the device decode pass spans several lane groups
+        "gt_wide": (EngineConfig(num_gpu_blocks=4096, block_size=16, max_model_len=4096, max_num_batched_tokens=2048,
+                                 max_num_seqs=256), (6000, 120, 160, 11), (400.0, 1.0, 46)),
+        "gt_wide300": (EngineConfig(num_gpu_blocks=6000, block_size=16, max_model_len=4096, max_num_batched_tokens=4096,
+                                    max_num_seqs=300), (6000, 120, 160, 12), (500.0, 0.5, 47)),
         "oracle": (EngineConfig(num_gpu_blocks=1500, block_size=16, max_model_len=4096, max_num_batched_tokens=512,
                                 max_num_seqs=64), (3000, 200, 100, 10), (12.0, 1.0, 45)),
     }
@@ -84,7 +89,7 @@ def main():
             n_steps = 3000
         else:
             backend = GroundTruthBackend(GroundTruthParams(noise_cv=0.05), seed=3)
-            n_steps = 6000
+            n_steps = 6000 if not name.startswith("gt_wide") else 2500
         rows = run(cfg, entries, arrivals, backend, n_steps)
         a = np.array(rows, dtype=np.float64)
         out[f"{name}_cfg"] = np.array([cfg.num_gpu_blocks, cfg.block_size, cfg.max_model_len,

@@ -22,9 +22,16 @@ def scenario(name):
     return cfg, Scenario(G[f"{name}_prompt"], G[f"{name}_output"], G[f"{name}_arrivals"])
 
 
-@pytest.mark.parametrize("name", ["gt_c1", "gt_tight", "gt_bursty"])
-def test_replay_matches_reference_scheduler(name):
-    """Same latencies in -> the same step keys, emissions, finishes and preemptions."""
+@pytest.mark.parametrize("name,lists", [("gt_c1", "smem"), ("gt_tight", "smem"), ("gt_bursty", "smem"),
+                                        ("gt_wide", "smem"), ("gt_wide300", "smem"), ("gt_tight", "global"),
+                                        ("gt_wide", "global")])
+def test_replay_matches_reference_scheduler(name, lists, monkeypatch):
+    """Same latencies in -> the same step keys, emissions, finishes and preemptions.
+    gt_wide / gt_wide300 run 256 / 300 requests at once (several lane groups in
+    the decode pass, preemptions across group boundaries); `global` forces the
+    running lists out of shared memory (the path for very large max_num_seqs)."""
+    if lists == "global":
+        monkeypatch.setenv("EMU_SCHED_SMEM", "0")
     cfg, sc = scenario(name)
     lat = G[f"{name}_lat"]
     n = len(lat)
