@@ -269,8 +269,11 @@ int emu_sched_run_oracle(emu_sched_t sc, emu_oracle_t o, const uint64_t* pcg_sta
 int emu_sched_results(emu_sched_t sc, int64_t* n_steps, int32_t* status, int32_t* tt, int32_t* conc,
                       uint8_t* phase, double* lat, int32_t* tokens, int32_t* finished, int64_t* preempt);
 /* Per-scenario totals [S x 4]: steps, tokens emitted, requests finished,
- * preemptions -- without copying the per-step arrays to the host. */
+ * preemptions (accumulated by the kernel; valid with or without per-step outputs). */
 int emu_sched_summary(emu_sched_t sc, int64_t* out4);
+/* keep = 0 before a run: no per-step outputs (no S x max_steps x 33 B arrays; runs
+ * of any length), totals only through emu_sched_summary.  Default 1. */
+int emu_sched_keep_steps(emu_sched_t sc, int32_t keep);
 void emu_sched_destroy(emu_sched_t sc);
 
 /* --------------------------------------------------------------- codecs --

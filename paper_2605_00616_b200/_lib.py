@@ -73,6 +73,7 @@ SIGNATURES = {
     "emu_sched_run_oracle": (c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_i64), c_vp]),
     "emu_sched_results": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "emu_sched_summary": (c_int, [c_vp, c_vp]),
+    "emu_sched_keep_steps": (c_int, [c_vp, c_i32]),
     "emu_sched_destroy": (None, [c_vp]),
     "emu_pack_parse_json": (c_int, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
     "emu_pack_parsed_info": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_vp,

@@ -81,7 +81,7 @@ struct SchedArgs {
   int32_t* resume;
   int32_t* key;  // [S * 3] pending / current key (tt, conc, phase)
   uint64_t* pcg;  // [S * 6]
-  // outputs [S * max_steps]
+  // per-step outputs [S * max_steps], NULL when the run keeps totals only
   int32_t* o_tt;
   int32_t* o_conc;
   uint8_t* o_ph;
@@ -90,6 +90,8 @@ struct SchedArgs {
   int32_t* o_fin;
   int64_t* o_pre;
   // latency sources
+  int64_t* tot_tok;  // [S] tokens emitted / requests finished, summed over the run
+  int64_t* tot_fin;
   const double* lat_in;  // MODE 0: [S * max_steps]
   double gt_base, gt_tok, gt_seq, gt_mult, gt_cv;
   uint64_t seed;
@@ -460,6 +462,7 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
   int32_t* key = A.key + 3 * (int64_t)s;
   const bool P = A.prof != nullptr;
   const int64_t step0 = step;
+  long long tok_sum = 0, fin_sum = 0;
   long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0, pc4 = 0, tc = P ? clock64() : 0;
 #define EMU_LAP(acc)                 \
   if (P) {                           \
@@ -644,14 +647,18 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
       st = SC_ERROR;
       break;
     }
-    const int64_t o = (int64_t)s * A.max_steps + step;
-    A.o_tt[o] = tt;
-    A.o_conc[o] = conc;
-    A.o_ph[o] = (uint8_t)ph;
-    A.o_lat[o] = lat;
-    A.o_tok[o] = tokens;
-    A.o_fin[o] = fin;
-    A.o_pre[o] = c.npre;
+    if (A.o_tt) {
+      const int64_t o = (int64_t)s * A.max_steps + step;
+      A.o_tt[o] = tt;
+      A.o_conc[o] = conc;
+      A.o_ph[o] = (uint8_t)ph;
+      A.o_lat[o] = lat;
+      A.o_tok[o] = tokens;
+      A.o_fin[o] = fin;
+      A.o_pre[o] = c.npre;
+    }
+    tok_sum += tokens;
+    fin_sum += fin;
     c.ne = 0;
     t = __dadd_rn(t, lat);
     step++;
@@ -680,6 +687,10 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
   A.evt[s] = c.evt;
   A.preempt[s] = c.npre;
   A.n_ent[s] = c.ne;
+  if (lane == 0) {
+    A.tot_tok[s] += tok_sum;
+    A.tot_fin[s] += fin_sum;
+  }
   if (A.smem) {  // back to the scenario's global slices for the next launch
     __syncwarp();
     int32_t* gr = A.running + r0;
@@ -717,6 +728,7 @@ struct emu_sched_s {
   SchedArgs a{};
   int32_t S = 0;
   int64_t R = 0, W = 0, max_steps = 0;
+  bool keep = true;  // per-step outputs (allocated by the first run that keeps them)
   std::vector<void*> owned;
   std::vector<int64_t> roff_h;
   template <typename T>
@@ -766,6 +778,16 @@ static int sched_reset(emu_sched_t sc, cudaStream_t s) {
   EMU_CUDA(cudaMemsetAsync(a.nrun, 0, 4 * S, s));
   EMU_CUDA(cudaMemsetAsync(a.wfront, 0, 4 * S, s));
   EMU_CUDA(cudaMemsetAsync(a.nsteps, 0, 8 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.tot_tok, 0, 8 * S, s));
+  EMU_CUDA(cudaMemsetAsync(a.tot_fin, 0, 8 * S, s));
+  if (sc->keep && !a.o_tt) {  // per-step outputs, S x max_steps x 33 B
+    const int64_t SM = (int64_t)S * sc->max_steps;
+    int rc;
+    if ((rc = sc->alloc(&a.o_tt, SM)) || (rc = sc->alloc(&a.o_conc, SM)) || (rc = sc->alloc(&a.o_ph, SM)) ||
+        (rc = sc->alloc(&a.o_lat, SM)) || (rc = sc->alloc(&a.o_tok, SM)) || (rc = sc->alloc(&a.o_fin, SM)) ||
+        (rc = sc->alloc(&a.o_pre, SM)))
+      return rc;
+  }
   EMU_CUDA(cudaMemsetAsync(a.evt, 0, 4 * S, s));
   EMU_CUDA(cudaMemsetAsync(a.preempt, 0, 8 * S, s));
   EMU_CUDA(cudaMemsetAsync(a.status, 0, 4 * S, s));
@@ -863,7 +885,7 @@ int emu_sched_create(int32_t S, const int64_t* req_off, const int32_t* prompt, c
   int64_t *d_roff, *d_woff;
   int32_t *d_prompt, *d_target;
   double* d_arr;
-  const int64_t SM = (int64_t)S * max_steps, SQ = (int64_t)S * max_num_seqs;
+  const int64_t SQ = (int64_t)S * max_num_seqs;
   if ((rc = sc->alloc(&d_roff, S + 1)) || (rc = sc->alloc(&d_woff, S + 1)) || (rc = sc->alloc(&d_prompt, R)) ||
       (rc = sc->alloc(&d_target, R)) || (rc = sc->alloc(&d_arr, R)) || (rc = sc->alloc(&a.progress, R)) ||
       (rc = sc->alloc(&a.generated, R)) || (rc = sc->alloc(&a.alloc, R)) || (rc = sc->alloc(&a.rphase, R)) ||
@@ -874,9 +896,7 @@ int emu_sched_create(int32_t S, const int64_t* req_off, const int32_t* prompt, c
       (rc = sc->alloc(&a.free_blocks, S)) || (rc = sc->alloc(&a.nsteps, S)) || (rc = sc->alloc(&a.evt, S)) ||
       (rc = sc->alloc(&a.preempt, S)) || (rc = sc->alloc(&a.status, S)) || (rc = sc->alloc(&a.n_ent, S)) ||
       (rc = sc->alloc(&a.resume, S)) || (rc = sc->alloc(&a.key, 3 * (int64_t)S)) ||
-      (rc = sc->alloc(&a.pcg, 6 * (int64_t)S)) || (rc = sc->alloc(&a.o_tt, SM)) || (rc = sc->alloc(&a.o_conc, SM)) ||
-      (rc = sc->alloc(&a.o_ph, SM)) || (rc = sc->alloc(&a.o_lat, SM)) || (rc = sc->alloc(&a.o_tok, SM)) ||
-      (rc = sc->alloc(&a.o_fin, SM)) || (rc = sc->alloc(&a.o_pre, SM))) {
+      (rc = sc->alloc(&a.pcg, 6 * (int64_t)S)) || (rc = sc->alloc(&a.tot_tok, S)) || (rc = sc->alloc(&a.tot_fin, S))) {
     delete sc;
     return rc;
   }
@@ -914,14 +934,16 @@ static int launch_sched(emu_sched_t sc, int mode, cudaStream_t s) {
   if (const char* v = getenv("EMU_SCHED_SMEM"))  // 0: force the global-memory lists (tests)
     if (v[0] == '0') sc->a.smem = 0;
   const size_t dyn = sc->a.smem ? sm : 0;
+  SchedArgs la = sc->a;
+  if (!sc->keep) la.o_tt = nullptr;  // totals only
   if (dyn > 48 * 1024) {
     EMU_CUDA(cudaFuncSetAttribute(k_sched<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     EMU_CUDA(cudaFuncSetAttribute(k_sched<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     EMU_CUDA(cudaFuncSetAttribute(k_sched<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   }
-  if (mode == 0) EMU_LAUNCH("sched", s, k_sched<0><<<grid, 32, dyn, s>>>(sc->a));
-  if (mode == 1) EMU_LAUNCH("sched", s, k_sched<1><<<grid, 32, dyn, s>>>(sc->a));
-  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, 32, dyn, s>>>(sc->a));
+  if (mode == 0) EMU_LAUNCH("sched", s, k_sched<0><<<grid, 32, dyn, s>>>(la));
+  if (mode == 1) EMU_LAUNCH("sched", s, k_sched<1><<<grid, 32, dyn, s>>>(la));
+  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, 32, dyn, s>>>(la));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
 }
@@ -1022,48 +1044,24 @@ int emu_sched_run_oracle(emu_sched_t sc, emu_oracle_t o, const uint64_t* pcg_sta
 
 }  // extern "C"
 
-namespace emu {
-// Per-scenario totals without copying the per-step arrays out.
-__global__ void k_sched_sum(const int64_t* nsteps, const int32_t* tok, const int32_t* fin, const int64_t* pre,
-                            int64_t max_steps, int64_t* out) {
-  const int32_t s = blockIdx.x;
-  const int64_t n = nsteps[s];
-  long long a = 0, b = 0;
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-    a += tok[s * max_steps + k];
-    b += fin[s * max_steps + k];
-  }
-  __shared__ long long sa[256], sb[256];
-  sa[threadIdx.x] = a;
-  sb[threadIdx.x] = b;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) {
-      sa[threadIdx.x] += sa[threadIdx.x + o];
-      sb[threadIdx.x] += sb[threadIdx.x + o];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    out[4 * s] = n;
-    out[4 * s + 1] = sa[0];
-    out[4 * s + 2] = sb[0];
-    out[4 * s + 3] = n ? pre[s * max_steps + n - 1] : 0;
-  }
-}
-}  // namespace emu
-
 extern "C" {
+
+int emu_sched_keep_steps(emu_sched_t sc, int32_t keep) {
+  if (!sc) return fail(EMU_ERR_INVALID, "NULL scheduler");
+  sc->keep = keep != 0;
+  return EMU_OK;
+}
 
 int emu_sched_summary(emu_sched_t sc, int64_t* out4) {
   if (!sc || !out4) return fail(EMU_ERR_INVALID, "NULL scheduler/output");
-  int64_t* d = nullptr;
-  EMU_CUDA(cudaMalloc(&d, 32 * (size_t)sc->S));
-  EMU_LAUNCH("sched_sum", 0, k_sched_sum<<<sc->S, 256>>>(sc->a.nsteps, sc->a.o_tok, sc->a.o_fin, sc->a.o_pre,
-                                                          sc->max_steps, d));
-  const cudaError_t e = cudaMemcpy(out4, d, 32 * (size_t)sc->S, cudaMemcpyDeviceToHost);
-  cudaFree(d);
-  if (e != cudaSuccess) return cuda_fail(e, "emu_sched_summary");
+  const size_t S = (size_t)sc->S;
+  std::vector<int64_t> v(4 * S);
+  EMU_CUDA(cudaMemcpy(v.data(), sc->a.nsteps, 8 * S, cudaMemcpyDeviceToHost));
+  EMU_CUDA(cudaMemcpy(v.data() + S, sc->a.tot_tok, 8 * S, cudaMemcpyDeviceToHost));
+  EMU_CUDA(cudaMemcpy(v.data() + 2 * S, sc->a.tot_fin, 8 * S, cudaMemcpyDeviceToHost));
+  EMU_CUDA(cudaMemcpy(v.data() + 3 * S, sc->a.preempt, 8 * S, cudaMemcpyDeviceToHost));
+  for (size_t s = 0; s < S; s++)
+    for (int k = 0; k < 4; k++) out4[4 * s + k] = v[k * S + s];
   return EMU_OK;
 }
 
@@ -1071,6 +1069,8 @@ int emu_sched_results(emu_sched_t sc, int64_t* n_steps, int32_t* status, int32_t
                       double* lat, int32_t* tokens, int32_t* finished, int64_t* preempt) {
   if (!sc) return fail(EMU_ERR_INVALID, "NULL scheduler");
   const size_t S = (size_t)sc->S, SM = S * (size_t)sc->max_steps;
+  if ((tt || conc || phase || lat || tokens || finished || preempt) && !(sc->keep && sc->a.o_tt))
+    return fail(EMU_ERR_INVALID, "per-step results were not kept (emu_sched_keep_steps(sc, 0) before the run)");
   if (n_steps) EMU_CUDA(cudaMemcpy(n_steps, sc->a.nsteps, 8 * S, cudaMemcpyDefault));
   if (status) EMU_CUDA(cudaMemcpy(status, sc->a.status, 4 * S, cudaMemcpyDefault));
   if (tt) EMU_CUDA(cudaMemcpy(tt, sc->a.o_tt, 4 * SM, cudaMemcpyDefault));

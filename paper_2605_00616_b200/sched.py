@@ -124,6 +124,7 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
                                   ctypes.byref(h)))
     tm["create"] = time.perf_counter()
     try:
+        _lib.check(L.emu_sched_keep_steps(h, 1 if keep_steps else 0))
         rounds = ctypes.c_int64(0)
         if backend == "oracle":
             if oracle is None:

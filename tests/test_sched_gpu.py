@@ -81,3 +81,19 @@ def test_config_validation_messages():
     big = Scenario(np.array([4000], np.int32), np.array([200], np.int32), np.array([0.0]))
     with pytest.raises(ValueError, match="prompt_tokens \\+ max_tokens = 4200 exceeds max_model_len 4096"):
         emulate(EngineConfig(1000), [big], 10, backend="ground_truth")
+
+
+def test_totals_only_run_matches_per_step_outputs():
+    """keep_steps=False allocates no per-step arrays; the kernel's running totals
+    equal the sums of a per-step run (replay of gt_wide: preemptions included)."""
+    cfg, sc = scenario("gt_wide")
+    lat = G["gt_wide_lat"]
+    n = len(lat)
+    full = emulate(cfg, [sc, sc], n, backend="replay", latencies=[lat, lat])
+    tot = emulate(cfg, [sc, sc], n, backend="replay", latencies=[lat, lat], keep_steps=False)
+    for s in range(2):
+        assert tot["n_steps"][s] == full["n_steps"][s] == n
+        assert tot["tokens"][s] == full["tokens"][s].sum() == G["gt_wide_stats"][:, 0].sum()
+        assert tot["finished"][s] == full["finished"][s].sum()
+        assert tot["preemptions"][s] == full["preemptions"][s][n - 1] == G["gt_wide_stats"][-1, 2]
+    assert "tt" not in tot
