@@ -408,16 +408,67 @@ struct Scen {
   }
 };
 
-// One scenario per warp (CTA of 32): scenarios diverge completely, so one warp
-// each keeps S independent instruction streams spread over the SMs; the warp's
-// lanes share the per-request loops of a step.
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ Pcg64 load_pcg(const uint64_t* p) {
+  Pcg64 g;
+  g.s_hi = p[0];
+  g.s_lo = p[1];
+  g.i_hi = p[2];
+  g.i_lo = p[3];
+  g.has_u32 = (uint32_t)p[4];
+  g.u32 = (uint32_t)p[5];
+  return g;
+}
+
+// The oracle draw of a step whose pool entry `e` exists (LatencyOracle._draw,
+// oracle.py:130-135): choice over the pool CDF, then the sample index.
+__device__ __forceinline__ double oracle_draw(const SchedArgs& A, long long e, int ph, Pcg64& g) {
+  const double u = unit_double(pcg64_next64(g));
+  const PoolPick pk = pool_pick<true>(A.arena, e, u);
+  uint32_t j = 0;
+  if (pk.n > 1) {
+    const uint32_t w0 = pcg64_next32(g);
+    j = lemire_index((uint32_t)pk.n, w0, [&]() { return pcg64_next32(g); });
+  }
+  return __ldcg((ph ? A.s1 : A.s0) + pk.soff + (int32_t)j);
+}
+
+// One scenario per CTA: scenarios diverge completely, so one warp each keeps S
+// independent instruction streams spread over the SMs; the warp's lanes share
+// the per-request loops of a step.  In the oracle closed loop (MODE 2) a
+// second warp owns the scenario's PCG64 stream and draws the step's latency
+// while the first applies the step's outcome (which does not need it).
 template <int MODE>
-__global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
+__global__ void __launch_bounds__(64, 1) k_sched(SchedArgs A) {
   const int32_t s = blockIdx.x;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   if (s >= A.S) return;
   if (A.status[s] == SC_DONE || A.status[s] == SC_ERROR) return;
+  __shared__ long long s_e;
+  __shared__ double s_lat;
+  __shared__ int s_ph, s_cmd;
+  if (MODE == 2 && threadIdx.x >= 32) {  // the drawer warp
+    uint64_t* p = A.pcg + 6 * (int64_t)s;
+    Pcg64 g = load_pcg(p);
+    for (;;) {
+      named_bar(1, 64);
+      if (!s_cmd) break;
+      const double lat = oracle_draw(A, s_e, s_ph, g);
+      if (lane == 0) s_lat = lat;
+      named_bar(2, 64);
+    }
+    if (lane == 0) {
+      p[0] = g.s_hi;
+      p[1] = g.s_lo;
+      p[2] = g.i_hi;
+      p[3] = g.i_lo;
+      p[4] = g.has_u32;
+      p[5] = g.u32;
+    }
+    return;
+  }
   const int64_t r0 = A.roff[s];
   Scen c{A, s, r0, (int32_t)(A.roff[s + 1] - r0), A.running + r0, A.snap + r0, A.wbits + A.woff[s],
          A.ent_id + (int64_t)s * A.max_seqs, A.ent_chunk + (int64_t)s * A.max_seqs, A.ent_pre + (int64_t)s * A.max_seqs,
@@ -449,16 +500,6 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
   int64_t step = A.nsteps[s];
   int32_t st = SC_RUNNING;
   bool resume = A.resume[s] != 0;
-  Pcg64 g;
-  if (MODE == 2) {
-    const uint64_t* p = A.pcg + 6 * (int64_t)s;
-    g.s_hi = p[0];
-    g.s_lo = p[1];
-    g.i_hi = p[2];
-    g.i_lo = p[3];
-    g.has_u32 = (uint32_t)p[4];
-    g.u32 = (uint32_t)p[5];
-  }
   int32_t* key = A.key + 3 * (int64_t)s;
   const bool P = A.prof != nullptr;
   const int64_t step0 = step;
@@ -546,14 +587,13 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
         A.resume[s] = 1;
         break;
       }
-      const double u = unit_double(pcg64_next64(g));
-      const PoolPick pk = pool_pick<true>(A.arena, e, u);
-      uint32_t j = 0;
-      if (pk.n > 1) {
-        const uint32_t w0 = pcg64_next32(g);
-        j = lemire_index((uint32_t)pk.n, w0, [&]() { return pcg64_next32(g); });
+      if (lane == 0) {  // hand the draw to the drawer warp
+        s_e = e;
+        s_ph = ph;
+        s_cmd = 1;
       }
-      lat = __ldcg((ph ? A.s1 : A.s0) + pk.soff + (int32_t)j);
+      named_bar(1, 64);
+      lat = 0.0;  // arrives after the outcome is applied
     }
     EMU_LAP(pc3);
     // _apply_outcome (engine.py:464-483): entries are distinct requests, so the
@@ -643,6 +683,10 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
       }
       c.nrun = out;
     }
+    if (MODE == 2) {
+      named_bar(2, 64);
+      lat = s_lat;
+    }
     if (c.err) {
       st = SC_ERROR;
       break;
@@ -704,14 +748,9 @@ __global__ void __launch_bounds__(32) k_sched(SchedArgs A) {
   }
   A.status[s] = st;
   if (st != SC_PAUSED) A.resume[s] = 0;
-  if (MODE == 2) {
-    uint64_t* p = A.pcg + 6 * (int64_t)s;
-    p[0] = g.s_hi;
-    p[1] = g.s_lo;
-    p[2] = g.i_hi;
-    p[3] = g.i_lo;
-    p[4] = g.has_u32;
-    p[5] = g.u32;
+  if (MODE == 2) {  // release the drawer warp
+    if (lane == 0) s_cmd = 0;
+    named_bar(1, 64);
   }
 }
 
@@ -943,7 +982,7 @@ static int launch_sched(emu_sched_t sc, int mode, cudaStream_t s) {
   }
   if (mode == 0) EMU_LAUNCH("sched", s, k_sched<0><<<grid, 32, dyn, s>>>(la));
   if (mode == 1) EMU_LAUNCH("sched", s, k_sched<1><<<grid, 32, dyn, s>>>(la));
-  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, 32, dyn, s>>>(la));
+  if (mode == 2) EMU_LAUNCH("sched", s, k_sched<2><<<grid, 64, dyn, s>>>(la));
   EMU_CUDA(cudaGetLastError());
   return EMU_OK;
 }
