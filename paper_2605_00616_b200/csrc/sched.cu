@@ -511,9 +511,13 @@ __global__ void __launch_bounds__(64, 1) k_sched(SchedArgs A) {
     acc += n_ - tc;                  \
     tc = n_;                         \
   }
+  // arrival offsets of requests nxt .. nxt+3 in registers (+inf past the end)
+  const double kNever = __longlong_as_double(0x7ff0000000000000LL);
+  auto arrival_at = [&](int32_t i) { return i < c.R ? A.arrival[r0 + i] : kNever; };
+  double a0 = arrival_at(nxt), a1 = arrival_at(nxt + 1), a2 = arrival_at(nxt + 2), a3 = arrival_at(nxt + 3);
   while (step < A.max_steps) {
     if (!resume) {
-      while (nxt < c.R && A.arrival[r0 + nxt] <= t) {  // admit (engine.py:323-340)
+      while (a0 <= t) {  // admit (engine.py:323-340)
         const int64_t gi = r0 + nxt;
         A.rphase[gi] = RQ_WAITING;
         A.progress[gi] = 0;
@@ -523,6 +527,10 @@ __global__ void __launch_bounds__(64, 1) k_sched(SchedArgs A) {
         A.pevt[gi] = 0;
         c.wait_insert(nxt);
         nxt++;
+        a0 = a1;  // the arrival window slides; its new tail load is not awaited here
+        a1 = a2;
+        a2 = a3;
+        a3 = arrival_at(nxt + 3);
       }
       EMU_LAP(pc0);
       c.lim = nxt;
@@ -541,7 +549,7 @@ __global__ void __launch_bounds__(64, 1) k_sched(SchedArgs A) {
           st = SC_DONE;
           break;
         }
-        t = A.arrival[r0 + nxt];
+        t = a0;
         continue;
       }
       int32_t tt = 0;
