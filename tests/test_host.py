@@ -161,3 +161,33 @@ def test_workload_generators_are_deterministic():
     assert (tt[ph == 0] == conc[ph == 0]).all() and tt.max() <= 2048 and conc.max() <= 256
     tt, conc, ph = queries_sparse(5000, 1)
     assert tt.max() <= 131072
+
+
+def test_scheduler_admission_checks_without_gpu():
+    """emu_sched_create validates the request table on host threads before any
+    device allocation (engine.py:323-336 messages, the first bad request wins)."""
+    lib = _lib.load_library()
+    S, n = 3, 1 << 21  # large enough for the threaded path
+    off = np.array([0, n, 2 * n, 3 * n], np.int64)
+    prompt = np.full(3 * n, 100, np.int32)
+    target = np.full(3 * n, 50, np.int32)
+    arrival = np.concatenate([np.arange(n, dtype=np.float64)] * 3)  # restarts per scenario: fine
+
+    def create(p, t, a, blocks=1000, max_len=4096):
+        h = ctypes.c_void_p()
+        rc = lib.emu_sched_create(S, _lib.ptr(off), _lib.ptr(p), _lib.ptr(t), _lib.ptr(a), blocks, 16, max_len, 512,
+                                  64, 10, ctypes.byref(h))
+        return rc, _lib.last_error(), h
+
+    p = prompt.copy()
+    p[2 * n + 5] = 0
+    p[n + 7] = 5000  # the earlier bad request reports
+    rc, msg, _ = create(p, target, arrival)
+    assert rc == _lib.EMU_ERR_INVALID and "exceeds max_model_len" in msg and "5050" in msg
+    t = target.copy()
+    t[3] = 0
+    assert "max_tokens must be >= 1, got 0" in create(prompt, t, arrival)[1]
+    assert "KV blocks" in create(prompt, target, arrival, blocks=5)[1]
+    a = arrival.copy()
+    a[n + 10] = -1.0
+    assert "arrival offsets must ascend" in create(prompt, target, a)[1]
