@@ -275,11 +275,11 @@ __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t*
     }
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
+    if (!__syncthreads_or(wcnt)) continue;  // warm tile: nothing claimed in this CTA
     int woff = 0;
     if (lane == 0 && wcnt) woff = atomicAdd(&s_cnt, wcnt);
     __syncthreads();
-    if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(&ctl->new_count, s_cnt) : 0;
+    if (threadIdx.x == 0) s_base = atomicAdd(&ctl->new_count, s_cnt);
     __syncthreads();
     if (!wcnt) continue;
     woff = __shfl_sync(kFull, woff, 0) + s_base;
@@ -1304,10 +1304,11 @@ static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, c
   EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
   {
     // EMU_MARK=<qpt>,<ctas per SM> (tuning knob).  Default 2 queries per
-    // thread, up to 32 CTAs per SM: 0.121 ms per 10M-query cold sweep vs 0.153
+    // thread, up to 8 CTAs per SM: 0.124 ms per 10M-query cold sweep vs 0.153
     // for 4 x 16 and 0.183 for 8 x 16 (the first wave's CAS round trips sit on
-    // each tile's critical path, so shorter tiles and more CTAs hide them better)
-    static int mq = -1, mg = 32;
+    // each tile's critical path, so shorter tiles hide them better); 32 CTAs
+    // per SM gain 3 us there but cost 18 % on warm 1M-query batches (config 5)
+    static int mq = -1, mg = 8;
     if (mq < 0) {
       mq = 2;
       if (const char* v = getenv("EMU_MARK")) sscanf(v, "%d,%d", &mq, &mg);

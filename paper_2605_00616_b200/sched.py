@@ -3,7 +3,7 @@
 ``emulate`` runs S independent what-if scenarios of the reference engine
 (``EmulatorEngine.admit`` / ``_schedule_step`` / ``_apply_outcome``,
 /root/reference/pkg/src/serve_emu/engine.py:323-483) in virtual time, one GPU
-thread per scenario (``emu_sched_*`` in csrc/sched.cu): arrivals <= t are
+warp per scenario (``emu_sched_*`` in csrc/sched.cu): arrivals <= t are
 admitted, a step is scheduled, its latency is taken from the backend, the
 outcome applied and t advanced by the latency.  Backends:
 
@@ -152,32 +152,31 @@ def emulate(config: EngineConfig, scenarios: Sequence[Scenario], max_steps: int,
         else:
             raise ValueError(f"unknown backend {backend!r}")
         tm["run"] = time.perf_counter()
-        n = np.zeros(S, np.int64)
         status = np.zeros(S, np.int32)
         if not keep_steps:  # totals only (long sweeps): no per-step arrays cross PCIe
             summ = np.zeros((S, 4), np.int64)
             _lib.check(L.emu_sched_summary(h, _lib.ptr(summ)))
             _lib.check(L.emu_sched_results(h, None, _lib.ptr(status), None, None, None, None, None, None, None))
-            if (status == 3).any():
-                raise RuntimeError(f"scheduler invariant violated in scenarios {np.flatnonzero(status == 3).tolist()}")
-            tm["results"] = time.perf_counter()
-            return {"n_steps": summ[:, 0], "tokens": summ[:, 1], "finished": summ[:, 2], "preemptions": summ[:, 3],
-                    "rounds": int(rounds.value), "host_s": _phases(tm)}
-        out = {k: np.zeros((S, max_steps), dt) for k, dt in (("tt", np.int32), ("conc", np.int32), ("phase", np.uint8),
-                                                              ("latency_s", np.float64), ("tokens", np.int32),
-                                                              ("finished", np.int32), ("preemptions", np.int64))}
-        _lib.check(L.emu_sched_results(h, _lib.ptr(n), _lib.ptr(status), _lib.ptr(out["tt"]), _lib.ptr(out["conc"]),
-                                       _lib.ptr(out["phase"]), _lib.ptr(out["latency_s"]), _lib.ptr(out["tokens"]),
-                                       _lib.ptr(out["finished"]), _lib.ptr(out["preemptions"])))
+            res = {"n_steps": summ[:, 0], "tokens": summ[:, 1], "finished": summ[:, 2], "preemptions": summ[:, 3]}
+        else:
+            res = {k: np.zeros((S, max_steps), dt) for k, dt in (("tt", np.int32), ("conc", np.int32),
+                                                                ("phase", np.uint8), ("latency_s", np.float64),
+                                                                ("tokens", np.int32), ("finished", np.int32),
+                                                                ("preemptions", np.int64))}
+            res["n_steps"] = np.zeros(S, np.int64)
+            _lib.check(L.emu_sched_results(h, _lib.ptr(res["n_steps"]), _lib.ptr(status), _lib.ptr(res["tt"]),
+                                           _lib.ptr(res["conc"]), _lib.ptr(res["phase"]), _lib.ptr(res["latency_s"]),
+                                           _lib.ptr(res["tokens"]), _lib.ptr(res["finished"]),
+                                           _lib.ptr(res["preemptions"])))
         if (status == 3).any():
             raise RuntimeError(f"scheduler invariant violated in scenarios {np.flatnonzero(status == 3).tolist()}")
-        out["n_steps"] = n
-        out["rounds"] = int(rounds.value)
+        res["rounds"] = int(rounds.value)
         tm["results"] = time.perf_counter()
-        out["host_s"] = _phases(tm)
-        return out
     finally:
         L.emu_sched_destroy(h)
+    tm["destroy"] = time.perf_counter()
+    res["host_s"] = _phases(tm)
+    return res
 
 
 __all__ = ["EngineConfig", "Scenario", "emulate", "prefetch_domain", "step_key_domain"]
