@@ -384,6 +384,7 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
   tb.tt_hi = t1;
   tb.c_lo = mm[0];
   tb.c_hi = mm[1];
+  if (!index_on_host()) return build_search_index_dev(tb, s);
   std::vector<int32_t> htt((size_t)nb), hcc((size_t)nb);
   std::vector<int64_t> hoff((size_t)nb + 1);
   EMU_CUDA(cudaMemcpyAsync(htt.data(), tb.bkt_tt, 4 * nb, cudaMemcpyDeviceToHost, s));

@@ -177,6 +177,198 @@ int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, c
   return EMU_OK;
 }
 
+// ---------------------------------------------------------------------------
+// The same search index built on the device from the device bucket arrays
+// (table build / create path; EMU_INDEX_HOST=1 selects the host version above,
+// which the tests use as the cross-check).  Grids are (gnt+1) x (gnc+1) with a
+// zero first row and column.
+// ---------------------------------------------------------------------------
+constexpr int kSatChunk = 256;  // rows per chunk of the column scan
+
+__global__ void k_idx_fill(const int32_t* __restrict__ btt, const int32_t* __restrict__ bcc,
+                           const int64_t* __restrict__ boff, int64_t nb, int32_t tt_lo, int32_t c_lo, int64_t st,
+                           int64_t wpr, int32_t* B, int32_t* S, uint32_t* bm) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = (int64_t)btt[b] - tt_lo, j = (int64_t)bcc[b] - c_lo;
+    B[(i + 1) * st + (j + 1)] = 1;
+    S[(i + 1) * st + (j + 1)] = (int32_t)(boff[b + 1] - boff[b]);
+    atomicOr(&bm[i * wpr + j / 32], 1u << (j % 32));
+  }
+}
+
+// inclusive prefix along each grid row (warp per row), both grids
+__global__ void k_idx_rows(int32_t* B, int32_t* S, int64_t rows, int64_t st) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int32_t cb = 0, cs = 0;
+    for (int64_t j0 = 1; j0 < st; j0 += 32) {
+      const int64_t j = j0 + lane;
+      int32_t vb = j < st ? B[r * st + j] : 0, vs = j < st ? S[r * st + j] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t yb = __shfl_up_sync(0xffffffffu, vb, o), ys = __shfl_up_sync(0xffffffffu, vs, o);
+        if (lane >= o) {
+          vb += yb;
+          vs += ys;
+        }
+      }
+      if (j < st) {
+        B[r * st + j] = cb + vb;
+        S[r * st + j] = cs + vs;
+      }
+      cb += __shfl_sync(0xffffffffu, vb, 31);
+      cs += __shfl_sync(0xffffffffu, vs, 31);
+    }
+  }
+}
+
+// column prefix in three passes: chunk sums, scan of chunk sums, apply
+__global__ void k_idx_col_sums(const int32_t* B, const int32_t* S, int64_t rows, int64_t st, int32_t* PB, int32_t* PS) {
+  const int64_t nch = (rows + kSatChunk - 1) / kSatChunk;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nch * st; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ch = t / st, j = t % st;
+    int32_t sb = 0, ss = 0;
+    for (int64_t r = ch * kSatChunk; r < rows && r < (ch + 1) * kSatChunk; r++) {
+      sb += B[r * st + j];
+      ss += S[r * st + j];
+    }
+    PB[t] = sb;
+    PS[t] = ss;
+  }
+}
+
+__global__ void k_idx_col_scan(int32_t* PB, int32_t* PS, int64_t nch, int64_t st) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < st; j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t ab = 0, as = 0;
+    for (int64_t ch = 0; ch < nch; ch++) {  // exclusive
+      const int32_t vb = PB[ch * st + j], vs = PS[ch * st + j];
+      PB[ch * st + j] = ab;
+      PS[ch * st + j] = as;
+      ab += vb;
+      as += vs;
+    }
+  }
+}
+
+__global__ void k_idx_col_apply(int32_t* B, int32_t* S, int64_t rows, int64_t st, const int32_t* PB, const int32_t* PS) {
+  const int64_t nch = (rows + kSatChunk - 1) / kSatChunk;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nch * st; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ch = t / st, j = t % st;
+    int32_t ab = PB[t], as = PS[t];
+    for (int64_t r = ch * kSatChunk; r < rows && r < (ch + 1) * kSatChunk; r++) {
+      ab += B[r * st + j];
+      as += S[r * st + j];
+      B[r * st + j] = ab;
+      S[r * st + j] = as;
+    }
+  }
+}
+
+// per grid row: first bucket (lower bound of the row's tt in bucket order) and
+// the exclusive popcount prefix of its bitmap words
+__global__ void k_idx_bitrows(const int32_t* __restrict__ btt, int64_t nb, int32_t tt_lo, int64_t gnt,
+                              const uint32_t* __restrict__ bm, int64_t wpr, int32_t* wp, int32_t* rbase) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= gnt; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = (int64_t)tt_lo + i;
+    int64_t lo = 0, hi = nb;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)btt[mid] < v)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    rbase[i] = (int32_t)lo;
+    if (i < gnt) {
+      int32_t acc = 0;
+      for (int64_t k = 0; k < wpr; k++) {
+        wp[i * wpr + k] = acc;
+        acc += __popc(bm[i * wpr + k]);
+      }
+    }
+  }
+}
+
+// column index: buckets ordered by (conc, tt).  col_start from the SAT's last
+// row; a bucket's rank in its column = occupied cells above it in that column
+__global__ void k_idx_colstart(const int32_t* B, int64_t gnt, int64_t st, int32_t* cstart) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int32_t* last = B + gnt * st;  // SAT row gnt: column j+1 holds the count of columns <= j
+    cstart[0] = 0;
+    for (int64_t j = 1; j < st; j++) cstart[j] = last[j];
+  }
+}
+
+__global__ void k_idx_cols(const int32_t* __restrict__ btt, const int32_t* __restrict__ bcc, int64_t nb, int32_t tt_lo,
+                           int32_t c_lo, int64_t st, const int32_t* B, const int32_t* cstart, int32_t* ctt, int32_t* cb) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = (int64_t)btt[b] - tt_lo, j = (int64_t)bcc[b] - c_lo;
+    // rows 0..i-1 of column j: SAT(i, j+1) - SAT(i, j)
+    const int64_t k = cstart[j] + (B[i * st + j + 1] - B[i * st + j]);
+    ctt[k] = btt[b];
+    cb[k] = (int32_t)b;
+  }
+}
+
+int build_search_index_dev(TableBuf& tb, cudaStream_t s) {
+  if (tb.nb == 0) return EMU_OK;
+  const int64_t span_t = (int64_t)tb.tt_hi - tb.tt_lo, span_c = (int64_t)tb.c_hi - tb.c_lo;
+  tb.lt = std::min<int64_t>(span_t + 1, kMaxSqTable);
+  tb.lc = std::min<int64_t>(span_c + 1, kMaxSqTable);
+  EMU_CUDA(cudaMalloc((void**)&tb.sq_t, 8 * tb.lt));
+  EMU_CUDA(cudaMalloc((void**)&tb.sq_c, 8 * tb.lc));
+  EMU_LAUNCH("index", s, k_sq_table<<<(unsigned)std::min<int64_t>(1024, (tb.lt + 255) / 256), 256, 0, s>>>(tb.sq_t, tb.lt, span_t));
+  EMU_LAUNCH("index", s, k_sq_table<<<(unsigned)std::min<int64_t>(1024, (tb.lc + 255) / 256), 256, 0, s>>>(tb.sq_c, tb.lc, span_c));
+  EMU_CUDA(cudaGetLastError());
+  const int64_t gnt = span_t + 1, gnc = span_c + 1;
+  if (gnt > kMaxGridCells || gnc > kMaxGridCells || (gnt + 1) * (gnc + 1) > kMaxGridCells) {
+    EMU_CUDA(cudaStreamSynchronize(s));
+    return EMU_OK;
+  }
+  const int64_t st = gnc + 1, rows = gnt + 1, cells = rows * st, wpr = (gnc + 31) / 32;
+  const int64_t nch = (rows + kSatChunk - 1) / kSatChunk;
+  EMU_CUDA(cudaMalloc((void**)&tb.bsat, 4 * cells));
+  EMU_CUDA(cudaMalloc((void**)&tb.ssat, 4 * cells));
+  EMU_CUDA(cudaMalloc((void**)&tb.bmap, 4 * gnt * wpr));
+  EMU_CUDA(cudaMalloc((void**)&tb.wpre, 4 * gnt * wpr));
+  EMU_CUDA(cudaMalloc((void**)&tb.rowbase, 4 * (gnt + 1)));
+  EMU_CUDA(cudaMalloc((void**)&tb.col_start, 4 * (gnc + 1)));
+  EMU_CUDA(cudaMalloc((void**)&tb.col_tt, 4 * std::max<int64_t>(1, tb.nb)));
+  EMU_CUDA(cudaMalloc((void**)&tb.col_b, 4 * std::max<int64_t>(1, tb.nb)));
+  int32_t* part = nullptr;
+  EMU_CUDA(cudaMallocAsync((void**)&part, 8 * (size_t)nch * st, s));
+  EMU_CUDA(cudaMemsetAsync(tb.bsat, 0, 4 * cells, s));
+  EMU_CUDA(cudaMemsetAsync(tb.ssat, 0, 4 * cells, s));
+  EMU_CUDA(cudaMemsetAsync(tb.bmap, 0, 4 * gnt * wpr, s));
+  const auto g = [](int64_t n, int t) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + t - 1) / t, kNumSMs * 8)); };
+  EMU_LAUNCH("index", s, k_idx_fill<<<g(tb.nb, 256), 256, 0, s>>>(tb.bkt_tt, tb.bkt_conc, tb.bkt_off, tb.nb, tb.tt_lo,
+                                                                   tb.c_lo, st, wpr, tb.bsat, tb.ssat, tb.bmap));
+  EMU_LAUNCH("index", s, k_idx_rows<<<g(rows * 32, 256), 256, 0, s>>>(tb.bsat, tb.ssat, rows, st));
+  EMU_LAUNCH("index", s, k_idx_col_sums<<<g(nch * st, 256), 256, 0, s>>>(tb.bsat, tb.ssat, rows, st, part,
+                                                                          part + nch * st));
+  EMU_LAUNCH("index", s, k_idx_col_scan<<<g(st, 128), 128, 0, s>>>(part, part + nch * st, nch, st));
+  EMU_LAUNCH("index", s, k_idx_col_apply<<<g(nch * st, 256), 256, 0, s>>>(tb.bsat, tb.ssat, rows, st, part,
+                                                                           part + nch * st));
+  EMU_LAUNCH("index", s, k_idx_bitrows<<<g(gnt + 1, 256), 256, 0, s>>>(tb.bkt_tt, tb.nb, tb.tt_lo, gnt, tb.bmap, wpr,
+                                                                       tb.wpre, tb.rowbase));
+  EMU_LAUNCH("index", s, k_idx_colstart<<<1, 32, 0, s>>>(tb.bsat, gnt, st, tb.col_start));
+  EMU_LAUNCH("index", s, k_idx_cols<<<g(tb.nb, 256), 256, 0, s>>>(tb.bkt_tt, tb.bkt_conc, tb.nb, tb.tt_lo, tb.c_lo, st,
+                                                                   tb.bsat, tb.col_start, tb.col_tt, tb.col_b));
+  EMU_CUDA(cudaGetLastError());
+  EMU_CUDA(cudaFreeAsync(part, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  tb.wpr = (int32_t)wpr;
+  tb.gnt = gnt;
+  tb.gnc = gnc;
+  return EMU_OK;
+}
+
+bool index_on_host() {
+  const char* v = getenv("EMU_INDEX_HOST");
+  return v && v[0] == '1';
+}
+
 template <typename T>
 static int dev_alloc(T** p, int64_t n) {
   *p = nullptr;
@@ -264,7 +456,7 @@ static int upload_table(const emu_table_view* v, const char* name, cudaStream_t 
   EMU_CUDA(cudaMemcpyAsync(tb.row_tt, row_tt.data(), 4 * tb.nrows, cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMemcpyAsync(tb.row_start, row_start.data(), 8 * (tb.nrows + 1), cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaStreamSynchronize(s));
-  return build_search_index(tb, tt.data(), cc.data(), off.data(), s);
+  return index_on_host() ? build_search_index(tb, tt.data(), cc.data(), off.data(), s) : build_search_index_dev(tb, s);
 }
 
 }  // namespace emu

@@ -33,6 +33,10 @@ struct TableBuf {
 // Build the search index (summed-area tables + squared-delta tables) from
 // host copies of the bucket keys/offsets (construction time, not per query).
 int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, const int64_t* h_off, cudaStream_t s);
+// The same index built on the device from tb's device bucket arrays (default);
+// index_on_host() (EMU_INDEX_HOST=1) selects the host version instead.
+int build_search_index_dev(TableBuf& tb, cudaStream_t s);
+bool index_on_host();
 
 }  // namespace emu
 

@@ -445,3 +445,24 @@ def test_functional_api_cache_is_bounded():
                            rng)
         assert v == 0.01 + 0.001 * i
         assert len(orc_mod._tables_cache) <= orc_mod._TABLES_CACHE_MAX
+
+
+@pytest.mark.parametrize("gen", ["llama", "sparse"])
+def test_device_search_index_matches_host_index(gen, monkeypatch):
+    """The table build's search index (summed-area tables, occupancy bitmap,
+    row bases, column index) is built on the device; EMU_INDEX_HOST=1 builds it
+    on the host.  Both must give bit-identical pools for 20k keys, in-grid and not."""
+    rec = (records_llama if gen == "llama" else records_sparse)(1_000_000, 3)
+    rng = np.random.default_rng(5)
+    n = 20_000
+    kt = rng.integers(-10, 3000 if gen == "llama" else 140_000, n)
+    kc = rng.integers(-3, 300, n)
+    kp = rng.integers(0, 2, n)
+    out = []
+    for host in ("0", "1"):
+        monkeypatch.setenv("EMU_INDEX_HOST", host)
+        pack = build_pack_arrays(*rec, num_gpu_blocks=1000, canonical=True)
+        orc = LatencyOracle(pack, OracleConfig(reliability_floor=32))
+        out.append(orc.pools(kt, kc, kp))
+    for g, w in zip(*out):
+        assert np.array_equal(g, w)
