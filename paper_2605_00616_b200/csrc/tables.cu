@@ -183,7 +183,6 @@ int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, c
 // which the tests use as the cross-check).  Grids are (gnt+1) x (gnc+1) with a
 // zero first row and column.
 // ---------------------------------------------------------------------------
-constexpr int kSatChunk = 256;  // rows per chunk of the column scan
 
 __global__ void k_idx_fill(const int32_t* __restrict__ btt, const int32_t* __restrict__ bcc,
                            const int64_t* __restrict__ boff, int64_t nb, int32_t tt_lo, int32_t c_lo, int64_t st,
@@ -224,12 +223,14 @@ __global__ void k_idx_rows(int32_t* B, int32_t* S, int64_t rows, int64_t st) {
 }
 
 // column prefix in three passes: chunk sums, scan of chunk sums, apply
-__global__ void k_idx_col_sums(const int32_t* B, const int32_t* S, int64_t rows, int64_t st, int32_t* PB, int32_t* PS) {
-  const int64_t nch = (rows + kSatChunk - 1) / kSatChunk;
+__global__ void k_idx_col_sums(const int32_t* B, const int32_t* S, int64_t rows, int64_t st, int64_t chunk,
+                               int32_t* PB, int32_t* PS) {
+  const int64_t nch = (rows + chunk - 1) / chunk;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nch * st; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ch = t / st, j = t % st;
     int32_t sb = 0, ss = 0;
-    for (int64_t r = ch * kSatChunk; r < rows && r < (ch + 1) * kSatChunk; r++) {
+#pragma unroll 8
+    for (int64_t r = ch * chunk; r < rows && r < (ch + 1) * chunk; r++) {
       sb += B[r * st + j];
       ss += S[r * st + j];
     }
@@ -241,6 +242,7 @@ __global__ void k_idx_col_sums(const int32_t* B, const int32_t* S, int64_t rows,
 __global__ void k_idx_col_scan(int32_t* PB, int32_t* PS, int64_t nch, int64_t st) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < st; j += (int64_t)gridDim.x * blockDim.x) {
     int32_t ab = 0, as = 0;
+#pragma unroll 8
     for (int64_t ch = 0; ch < nch; ch++) {  // exclusive
       const int32_t vb = PB[ch * st + j], vs = PS[ch * st + j];
       PB[ch * st + j] = ab;
@@ -251,12 +253,14 @@ __global__ void k_idx_col_scan(int32_t* PB, int32_t* PS, int64_t nch, int64_t st
   }
 }
 
-__global__ void k_idx_col_apply(int32_t* B, int32_t* S, int64_t rows, int64_t st, const int32_t* PB, const int32_t* PS) {
-  const int64_t nch = (rows + kSatChunk - 1) / kSatChunk;
+__global__ void k_idx_col_apply(int32_t* B, int32_t* S, int64_t rows, int64_t st, int64_t chunk, const int32_t* PB,
+                                const int32_t* PS) {
+  const int64_t nch = (rows + chunk - 1) / chunk;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nch * st; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ch = t / st, j = t % st;
     int32_t ab = PB[t], as = PS[t];
-    for (int64_t r = ch * kSatChunk; r < rows && r < (ch + 1) * kSatChunk; r++) {
+#pragma unroll 8
+    for (int64_t r = ch * chunk; r < rows && r < (ch + 1) * chunk; r++) {
       ab += B[r * st + j];
       as += S[r * st + j];
       B[r * st + j] = ab;
@@ -327,7 +331,8 @@ int build_search_index_dev(TableBuf& tb, cudaStream_t s) {
     return EMU_OK;
   }
   const int64_t st = gnc + 1, rows = gnt + 1, cells = rows * st, wpr = (gnc + 31) / 32;
-  const int64_t nch = (rows + kSatChunk - 1) / kSatChunk;
+  // column scan in chunks of rows: short per-thread chains, at most 512 chunks
+  const int64_t chunk = std::max<int64_t>(16, (rows + 511) / 512), nch = (rows + chunk - 1) / chunk;
   EMU_CUDA(cudaMalloc((void**)&tb.bsat, 4 * cells));
   EMU_CUDA(cudaMalloc((void**)&tb.ssat, 4 * cells));
   EMU_CUDA(cudaMalloc((void**)&tb.bmap, 4 * gnt * wpr));
@@ -345,10 +350,10 @@ int build_search_index_dev(TableBuf& tb, cudaStream_t s) {
   EMU_LAUNCH("index", s, k_idx_fill<<<g(tb.nb, 256), 256, 0, s>>>(tb.bkt_tt, tb.bkt_conc, tb.bkt_off, tb.nb, tb.tt_lo,
                                                                    tb.c_lo, st, wpr, tb.bsat, tb.ssat, tb.bmap));
   EMU_LAUNCH("index", s, k_idx_rows<<<g(rows * 32, 256), 256, 0, s>>>(tb.bsat, tb.ssat, rows, st));
-  EMU_LAUNCH("index", s, k_idx_col_sums<<<g(nch * st, 256), 256, 0, s>>>(tb.bsat, tb.ssat, rows, st, part,
+  EMU_LAUNCH("index", s, k_idx_col_sums<<<g(nch * st, 256), 256, 0, s>>>(tb.bsat, tb.ssat, rows, st, chunk, part,
                                                                           part + nch * st));
   EMU_LAUNCH("index", s, k_idx_col_scan<<<g(st, 128), 128, 0, s>>>(part, part + nch * st, nch, st));
-  EMU_LAUNCH("index", s, k_idx_col_apply<<<g(nch * st, 256), 256, 0, s>>>(tb.bsat, tb.ssat, rows, st, part,
+  EMU_LAUNCH("index", s, k_idx_col_apply<<<g(nch * st, 256), 256, 0, s>>>(tb.bsat, tb.ssat, rows, st, chunk, part,
                                                                            part + nch * st));
   EMU_LAUNCH("index", s, k_idx_bitrows<<<g(gnt + 1, 256), 256, 0, s>>>(tb.bkt_tt, tb.nb, tb.tt_lo, gnt, tb.bmap, wpr,
                                                                        tb.wpre, tb.rowbase));
