@@ -39,7 +39,7 @@ constexpr int kWarpBytes = kWarpCap * 12 + 40 * 8 + 10 * 8 + 3 * 32 * 4 + kWarpC
 #ifndef EMU_WARP_MINB
 #define EMU_WARP_MINB 8  // 64 registers: 8 CTAs x 4 warps per SM (smem 4.9 KB per warp)
 #endif
-constexpr int kWarpGrid = kNumSMs * 8;
+constexpr int kWarpGrid = kNumSMs * EMU_WARP_MINB;
 constexpr int kCtaThreads = 256;
 constexpr int kCtaCap = 8192;  // candidates in shared memory per CTA
 constexpr int kCtaSmem = kCtaCap * 12;
