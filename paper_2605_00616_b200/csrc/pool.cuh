@@ -411,6 +411,76 @@ __device__ __forceinline__ void warp_sort_ws(const PoolWS& ws, int C) {
   __syncwarp();
 }
 
+// Multi-warp groups (NT > 32), up to 128 candidates per warp: each warp sorts
+// its run of 128 in registers (warp_bitonic), then every element's final
+// position is its index in its run plus, for each other run, the number of
+// elements there that order before it (binary search in shared memory; the
+// (distance, bucket) keys are distinct, so ranks are exact).  Two passes over
+// shared memory instead of the log^2 stages of the shared-memory bitonic
+// network.  Returns false (caller sorts otherwise) above 128 per warp.
+template <int NT>
+__device__ __forceinline__ bool grp_sort_runs(const PoolWS& ws, int64_t pos) {
+  constexpr int W = NT / 32;
+  if (NT <= 32 || pos > 128 * (int64_t)W) return false;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r0 = w * 128;
+  const int len = (int)max((int64_t)0, min((int64_t)128, pos - r0));
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  double d[4];
+  int32_t b[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int i = q * 32 + lane;
+    d[q] = i < len ? ws.d[r0 + i] : kInf;
+    b[q] = i < len ? ws.b[r0 + i] : 0x7fffffff;
+  }
+  if (len > 0) warp_bitonic<4>(d, b);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int i = q * 32 + lane;
+    if (i < len) {
+      ws.d[r0 + i] = d[q];
+      ws.b[r0 + i] = b[q];
+    }
+  }
+  __syncthreads();
+  int dst[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int i = q * 32 + lane;
+    dst[q] = -1;
+    if (i < len) {
+      int p = i;
+      for (int v = 0; v < W; v++) {
+        const int lv = (int)max((int64_t)0, min((int64_t)128, pos - v * 128));
+        if (v == w || lv == 0) continue;
+        const double* rd = ws.d + v * 128;
+        const int32_t* rb = ws.b + v * 128;
+        int lo = 0, hi = lv;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (cand_less(rd[mid], rb[mid], d[q], b[q]))
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        p += lo;
+      }
+      dst[q] = p;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+    if (dst[q] >= 0) {
+      ws.d[dst[q]] = d[q];
+      ws.b[dst[q]] = b[q];
+    }
+  __syncthreads();
+  return true;
+}
+
 // Shortest prefix of the sorted candidates (sd, sb)[0..C) reaching the floor,
 // or -1 if the C candidates hold fewer than mfloor samples.  Caches each
 // scanned candidate's sample count / first sample in ws.n / ws.o.
@@ -723,7 +793,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
       warp_sort_ws<2>(ws, pos);
     else
       warp_sort_ws<4>(ws, pos);
-  } else {
+  } else if (!grp_sort_runs<NT>(ws, pos)) {
     int64_t P = 1;
     while (P < pos) P <<= 1;
     for (int64_t i = pos + G::rank(); i < P; i += NT) {
