@@ -525,6 +525,30 @@ __device__ int64_t prefix_k(const DevTable& T, const int32_t* sb, int64_t C, int
 //   4. candidates are sorted in registers (warp bitonic, <= 128) or shared
 //      memory, then the prefix reaching the floor is taken.
 // Returns K, -1 if the window exceeds ws.cap (escalate), -2 to fall back.
+// Append a candidate to the workspace.  A warp compacts with a ballot (same
+// order as a scan); multi-warp groups reserve slots with one shared-memory
+// atomic per warp instead of a block-wide scan per round: the order of the
+// candidates does not matter, the sort that follows imposes the total
+// (distance, bucket) order.
+template <int NT>
+__device__ __forceinline__ void append_cand(bool in, double d, int32_t bb, const PoolWS& ws, int& pos, int* acnt) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(kFull, in);
+  int base = pos;
+  if (NT > 32) {
+    base = 0;
+    if (lane == 0 && m) base = atomicAdd(acnt, __popc(m));
+    base = __shfl_sync(kFull, base, 0);
+  } else {
+    pos += __popc(m);
+  }
+  if (in) {
+    const int o = base + __popc(m & ((1u << lane) - 1u));
+    ws.d[o] = d;
+    ws.b[o] = bb;
+  }
+}
+
 template <int NT>
 __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws,
                                    int64_t& sorted_off) {
@@ -605,6 +629,11 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
   if (C > ws.cap) return -1;
   // ---- 3. enumerate (candidates beyond dmax cannot be pooled and are dropped)
   int pos = 0;
+  int* acnt = reinterpret_cast<int*>(ws.scr + 32);  // group tiers: append counter
+  if (NT > 32) {
+    if (G::rank() == 0) *acnt = 0;
+    G::sync();
+  }
   if (C > 0) {
     const int32_t nri = w.i1 - w.i0 + 1;
     const int32_t b0 = T.bsat[w.i0 * st + (st - 1)], b1 = T.bsat[(w.i1 + 1) * st + (st - 1)];
@@ -642,13 +671,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
           d = dist_tab(T, (int64_t)t - T.col_tt[idx], (int64_t)c - (T.c_lo + w.j0 + l0), span_t, span_c);
           in = d <= dmax;
         }
-        long long kt;
-        const int ex2 = (int)G::excl_scan(in ? 1 : 0, kt, ws.scr);
-        if (in) {
-          ws.d[pos + ex2] = d;
-          ws.b[pos + ex2] = bb;
-        }
-        pos += (int)kt;
+        append_cand<NT>(in, d, bb, ws, pos, acnt);
       }
       G::sync();
     } else if (b1 - b0 <= 2 * nri || C == b1 - b0) {  // scan the tt slab
@@ -664,13 +687,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
             in = d <= dmax;
           }
         }
-        long long tot;
-        const int ex = (int)G::excl_scan(in ? 1 : 0, tot, ws.scr);
-        if (in) {
-          ws.d[pos + ex] = d;
-          ws.b[pos + ex] = b;
-        }
-        pos += (int)tot;
+        append_cand<NT>(in, d, b, ws, pos, acnt);
       }
     } else {  // row by row: bsat gives each row's conc sub-range
       for (int32_t base = w.i0; base <= w.i1; base += NT) {
@@ -708,19 +725,17 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
             d = dist_tab(T, ws.rows[2 * NT + lo_r], (int64_t)c - T.bkt_conc[bb], span_t, span_c);
             in = d <= dmax;
           }
-          long long kt;
-          const int ex2 = (int)G::excl_scan(in ? 1 : 0, kt, ws.scr);
-          if (in) {
-            ws.d[pos + ex2] = d;
-            ws.b[pos + ex2] = bb;
-          }
-          pos += (int)kt;
+          append_cand<NT>(in, d, bb, ws, pos, acnt);
         }
         G::sync();
       }
     }
   }
   G::sync();
+  if (NT > 32) {
+    pos = *acnt;
+    G::sync();
+  }
   // ---- 3b. (group / CTA tiers) drop candidates beyond the pool radius bound.
   // d_K lies in [~r1, sqrt(2) r1]: of 8 pivots r1 * (1 + (sqrt(2)-1)(l+1)/8) the
   // smallest whose disc already holds >= floor samples bounds d_K, and every
