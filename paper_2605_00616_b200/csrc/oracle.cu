@@ -47,7 +47,10 @@ constexpr int kCtaCache = 1024;  // cached counts/offsets per CTA workspace
 constexpr int kGrpThreads = 128;  // middle tier: one 4-warp group per key
 constexpr int kGrpCap = 2048;
 constexpr int kGrpSmem = kGrpCap * 12;
-constexpr int kGrpGrid = kNumSMs * 4;
+#ifndef EMU_GRP_MINB
+#define EMU_GRP_MINB 8  // 4-warp groups per SM in the grid (6 fit by shared memory; 8 measured best: C3 M=256 98 -> 84 ms)
+#endif
+constexpr int kGrpGrid = kNumSMs * EMU_GRP_MINB;
 constexpr int kCtaGrid = kNumSMs;
 constexpr int kSampleThreads = 256;
 constexpr int kQPT = 4;  // queries per thread, interleaved for memory-level parallelism
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(kWarpThreads, EMU_WARP_MINB) k_pool_warp(DevTa
 // (windows of 257..2048 candidates, e.g. M = 256 on sparse tables); keys that
 // still overflow go on to the CTA tier.
 template <int MODE>
-__global__ void __launch_bounds__(kGrpThreads) k_pool_grp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
+__global__ void __launch_bounds__(kGrpThreads, EMU_GRP_MINB) k_pool_grp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
                                                           int* work, const int* esc_list, const int* esc_count,
                                                           int* esc2_list, int* esc2_count) {
   extern __shared__ __align__(16) unsigned char smem[];
