@@ -1,4 +1,5 @@
-// sched.cu -- the reference scheduler in virtual time, one scenario per thread
+// sched.cu -- the reference scheduler in virtual time, one CTA per what-if
+// scenario: a scheduling warp, plus a drawer warp in the oracle closed loop
 // (the caller of the oracle that turns what-if scenarios
 // into step-key streams).
 //
