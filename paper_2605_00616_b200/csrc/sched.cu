@@ -761,6 +761,7 @@ __global__ void __launch_bounds__(64, 1) k_sched(SchedArgs A) {
     if (lane == 0) s_cmd = 0;
     named_bar(1, 64);
   }
+#undef EMU_LAP
 }
 
 }  // namespace emu
