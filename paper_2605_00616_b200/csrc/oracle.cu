@@ -48,7 +48,7 @@ constexpr int kGrpThreads = 128;  // middle tier: one 4-warp group per key
 constexpr int kGrpCap = 2048;
 constexpr int kGrpSmem = kGrpCap * 12;
 #ifndef EMU_GRP_MINB
-#define EMU_GRP_MINB 8  // 4-warp groups per SM in the grid (6 fit by shared memory; 8 measured best: C3 M=256 98 -> 84 ms)
+#define EMU_GRP_MINB 4  // 4-warp groups per SM (8 ran C3 M=256 in 84 vs 96 ms but showed intermittent faults in the pool tiers)
 #endif
 constexpr int kGrpGrid = kNumSMs * EMU_GRP_MINB;
 constexpr int kCtaGrid = kNumSMs;
