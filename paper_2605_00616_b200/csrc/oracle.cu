@@ -1790,6 +1790,10 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
   if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
   if (U < 0) return fail(EMU_ERR_INVALID, "negative key count");
   cudaStream_t s = as_stream(stream);
+  static const bool sync_check = [] {
+    const char* v = getenv("EMU_SYNC_CHECK");
+    return v && v[0] == '1';
+  }();
   std::vector<int64_t> off((size_t)U + 1, 0);
   if (U == 0) {
     EMU_CUDA(cudaMemcpyAsync(pool_off, off.data(), sizeof(int64_t), cudaMemcpyHostToDevice, s));
@@ -1827,6 +1831,7 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
   for (int64_t u0 = 0; u0 < U; u0 += chunkU) {
     const int64_t n = std::min(chunkU, U - u0);
     EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
+    EMU_CUDA(cudaMemsetAsync(xK, 0xff, 8 * n, s));  // -1: a key no tier emitted is caught below
     Keys keys{key_tt + u0, key_conc + u0, key_phase + u0, nullptr, nullptr, n};
     Sink sk = make_sink(o);
     sk.x_bkt = xb;
@@ -1837,22 +1842,45 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
     EMU_LAUNCH("pool_prep", s, k_pool_prep<1><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
                                                                         o->kw, o->resv));
     EMU_CUDA(cudaGetLastError());
+    if (sync_check) {
+      const cudaError_t e_ = cudaStreamSynchronize(s);
+      if (e_ != cudaSuccess) return cuda_fail(e_, "emu_oracle_pool after pool_prep");
+    }
     EMU_LAUNCH("pool_warp", s, k_pool_warp<1><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
                                    o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, &o->ctl->work, o->esc, &o->ctl->esc_count));
     EMU_CUDA(cudaGetLastError());
+    if (sync_check) {
+      const cudaError_t e_ = cudaStreamSynchronize(s);
+      if (e_ != cudaSuccess) return cuda_fail(e_, "emu_oracle_pool after pool_warp");
+    }
     EMU_LAUNCH("pool_grp", s, k_pool_grp<1><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(o->plane[0], o->plane[1], keys,
                                                                                     o->cfg, sk, &o->ctl->esc_work,
                                                                                     o->esc, &o->ctl->esc_count, o->esc2,
                                                                                     &o->ctl->esc2_count));
     EMU_CUDA(cudaGetLastError());
+    if (sync_check) {
+      const cudaError_t e_ = cudaStreamSynchronize(s);
+      if (e_ != cudaSuccess) return cuda_fail(e_, "emu_oracle_pool after pool_grp");
+    }
     EMU_LAUNCH("pool_cta", s, k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys,
                                                                                     o->cfg, sk, &o->ctl->esc2_work,
                                                                                     o->esc2, &o->ctl->esc2_count, o->gd,
                                                                                     o->gb, o->gcap));
     EMU_CUDA(cudaGetLastError());
+    if (sync_check) {
+      const cudaError_t e_ = cudaStreamSynchronize(s);
+      if (e_ != cudaSuccess) return cuda_fail(e_, "emu_oracle_pool after pool_cta");
+    }
     EMU_CUDA(cudaMemcpyAsync(hK.data(), xK, 8 * n, cudaMemcpyDeviceToHost, s));
     EMU_CUDA(cudaStreamSynchronize(s));
-    for (int64_t u = 0; u < n; u++) off[u0 + u + 1] = off[u0 + u] + hK[u];
+    for (int64_t u = 0; u < n; u++) {
+      if (hK[u] < 0 || hK[u] > kmax) {
+        cleanup();
+        return fail(EMU_ERR_CUDA, "emu_oracle_pool: key " + std::to_string(u0 + u) + " got no valid pool (K=" +
+                                      std::to_string(hK[u]) + ")");
+      }
+      off[u0 + u + 1] = off[u0 + u] + hK[u];
+    }
     if (off[u0 + n] > cap) over = true;
     if (!over) {
       EMU_CUDA(cudaMemcpyAsync(doff, off.data() + u0, 8 * n, cudaMemcpyHostToDevice, s));
