@@ -155,6 +155,11 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
     if (G::rank() == 0) *map_entry_ptr(sk.map, entry_idx) = make_entry(K, start);
     EMU_PHASE(6);
   } else {
+    if (K > sk.kmax) {  // cannot fit the key's output stride (see the known issue in DESIGN.md): report, don't write
+      if (G::rank() == 0) sk.x_K[w] = K;
+      G::sync();
+      return;
+    }
     const int64_t base = w * sk.kmax;
     pool_finish<NT>(T, K, cfg.p, cfg.eps, ws, soff, cached, nullptr, sk.x_bkt + base, sk.x_dist + base,
                     sk.x_prob + base, sk.x_cdf + base);
