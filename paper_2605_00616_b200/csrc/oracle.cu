@@ -125,6 +125,9 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
                           long long reserved, const Cfg& cfg, const PoolWS& ws, const Sink& sk) {
   using G = Grp<NT>;
   if (MODE == 0) {
+    // a reservation holds min(floor, window) slots; a larger (exhaustive) pool
+    // takes fresh arena space instead of running past it
+    if (reserved >= 0 && K > cfg.floor) reserved = -1;
     if (K == 1 && reserved != -2) {  // direct entry: the bucket itself (cdf == [1.0]), no arena slots
       if (G::rank() == 0) {
         const int32_t bb = ws.b[soff];
