@@ -159,7 +159,7 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
     EMU_PHASE(6);
   } else {
     if (K > sk.kmax) {  // cannot fit the key's output stride (see the known issue in DESIGN.md): report, don't write
-      if (G::rank() == 0) sk.x_K[w] = K;
+      if (G::rank() == 0) sk.x_K[w] = K + (int64_t)NT * 1000000;  // the error message names the tier (32/128/256)
       G::sync();
       return;
     }
