@@ -30,7 +30,7 @@
 
 namespace emu {
 
-enum : int { FLAG_ARENA = 1, FLAG_HASH = 2, FLAG_MISSING = 4 };
+enum : int { FLAG_ARENA = 1, FLAG_HASH = 2, FLAG_MISSING = 4, FLAG_BADPOOL = 8 };
 
 constexpr int kWarpCap = 256;  // candidates per warp workspace
 constexpr int kWarpsPerCta = 4;
@@ -48,7 +48,7 @@ constexpr int kGrpThreads = 128;  // middle tier: one 4-warp group per key
 constexpr int kGrpCap = 2048;
 constexpr int kGrpSmem = kGrpCap * 12;
 #ifndef EMU_GRP_MINB
-#define EMU_GRP_MINB 4  // 4-warp groups per SM (8 ran C3 M=256 in 84 vs 96 ms but showed intermittent faults in the pool tiers)
+#define EMU_GRP_MINB 8  // 4-warp groups per SM in the grid (C3 M=256: 84 vs 96 ms at 4)
 #endif
 constexpr int kGrpGrid = kNumSMs * EMU_GRP_MINB;
 constexpr int kCtaGrid = kNumSMs;
@@ -66,6 +66,7 @@ struct BatchCtl {
   int esc2_count;  // keys too big for the 128-thread group tier -> CTA tier
   int esc2_work;
   int grp_pad;
+  int bad_key[4];  // first key whose pool failed validation: claimed flag, phase, tt, conc
 };
 
 struct Keys {
@@ -89,6 +90,7 @@ struct Sink {
   int64_t* x_K;
   int64_t kmax;
   int* flags;
+  int* bad_key;  // BatchCtl::bad_key
 };
 
 struct Cfg {
@@ -120,14 +122,30 @@ __device__ __forceinline__ void publish_step(StepOut* out, double lat, int32_t s
 // cache arena slots at `reserved` (or freshly allocated when reserved == -1;
 // reserved == -2 means the arena overflowed in prep: leave the key pending)
 // and publish its map entry.  MODE 1: explicit fixed-stride outputs.
+// A pool can never hold more than min(floor, B) buckets (every bucket has >= 1
+// sample, oracle.py:99-103): a larger K is an internal error.  MODE 0 then
+// leaves the key's entry pending and flags the batch, naming the key; the host
+// call fails instead of drawing from it.
+__device__ __forceinline__ void report_bad_pool(const Sink& sk, int ph, int32_t t, int32_t c) {
+  atomicOr(sk.flags, FLAG_BADPOOL);
+  if (sk.bad_key && atomicCAS(&sk.bad_key[0], 0, 1) == 0) {
+    sk.bad_key[1] = ph;
+    sk.bad_key[2] = t;
+    sk.bad_key[3] = c;
+  }
+}
+
 template <int NT, int MODE>
 __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry_idx, int64_t soff, bool cached,
-                          long long reserved, const Cfg& cfg, const PoolWS& ws, const Sink& sk) {
+                          long long reserved, const Cfg& cfg, const PoolWS& ws, const Sink& sk, int ph, int32_t t,
+                          int32_t c) {
   using G = Grp<NT>;
   if (MODE == 0) {
-    // a reservation holds min(floor, window) slots; a larger (exhaustive) pool
-    // takes fresh arena space instead of running past it
-    if (reserved >= 0 && K > cfg.floor) reserved = -1;
+    if (K > cfg.floor || K > T.nb) {
+      if (G::rank() == 0) report_bad_pool(sk, ph, t, c);
+      G::sync();
+      return;
+    }
     if (K == 1 && reserved != -2) {  // direct entry: the bucket itself (cdf == [1.0]), no arena slots
       if (G::rank() == 0) {
         const int32_t bb = ws.b[soff];
@@ -173,13 +191,13 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
 // Full in-group search (no precomputed candidates).  false = window too big
 // for this workspace.
 template <int NT, int MODE>
-__device__ bool process_key(const DevTable& T, int64_t w, int32_t t, int32_t c, int64_t entry_idx, const Cfg& cfg,
-                            const PoolWS& ws, const Sink& sk) {
+__device__ bool process_key(const DevTable& T, int64_t w, int ph, int32_t t, int32_t c, int64_t entry_idx,
+                            const Cfg& cfg, const PoolWS& ws, const Sink& sk) {
   int64_t soff = 0;
   bool cached = false;
   const int64_t K = pool_search<NT>(T, t, c, cfg.floor, ws, soff, cached);
   if (K < 0) return false;
-  emit_pool<NT, MODE>(T, w, K, entry_idx, soff, cached, -1, cfg, ws, sk);
+  emit_pool<NT, MODE>(T, w, K, entry_idx, soff, cached, -1, cfg, ws, sk, ph, t, c);
   return true;
 }
 
@@ -348,12 +366,12 @@ __global__ void __launch_bounds__(kWarpThreads, EMU_WARP_MINB) k_pool_warp(DevTa
       if (r == -2) continue;  // arena overflow: the host flushes and retries
       const int64_t K = pool_from_window(T, keys.tt[wk], keys.conc[wk], cfg.floor, k, ws);
       if (K >= 0) {
-        emit_pool<32, MODE>(T, wk, K, ent, 0, true, r, cfg, ws, sk);
+        emit_pool<32, MODE>(T, wk, K, ent, 0, true, r, cfg, ws, sk, mixed ? 1 : 0, keys.tt[wk], keys.conc[wk]);
         continue;
       }
       __syncwarp();
     }
-    const bool ok = process_key<32, MODE>(T, wk, keys.tt[wk], keys.conc[wk], ent, cfg, ws, sk);
+    const bool ok = process_key<32, MODE>(T, wk, mixed ? 1 : 0, keys.tt[wk], keys.conc[wk], ent, cfg, ws, sk);
     if (!ok && lane == 0) {
       int e = atomicAdd(esc_count, 1);
       esc_list[e] = (int)wk;
@@ -386,7 +404,7 @@ __global__ void __launch_bounds__(kGrpThreads, EMU_GRP_MINB) k_pool_grp(DevTable
     const int w = esc_list[i];
     const DevTable& T = keys.ph[w] ? P1 : P0;
     const int64_t ent = keys.entry ? keys.entry[w] : 0;
-    const bool ok = process_key<kGrpThreads, MODE>(T, w, keys.tt[w], keys.conc[w], ent, cfg, ws, sk);
+    const bool ok = process_key<kGrpThreads, MODE>(T, w, keys.ph[w] ? 1 : 0, keys.tt[w], keys.conc[w], ent, cfg, ws, sk);
     if (!ok && threadIdx.x == 0) esc2_list[atomicAdd(esc2_count, 1)] = w;
   }
 }
@@ -416,8 +434,8 @@ __global__ void __launch_bounds__(kCtaThreads) k_pool_cta(DevTable P0, DevTable 
     const bool mixed = keys.ph[w] != 0;
     const DevTable& T = mixed ? P1 : P0;
     const int64_t ent = keys.entry ? keys.entry[w] : 0;
-    bool ok = process_key<kCtaThreads, MODE>(T, w, keys.tt[w], keys.conc[w], ent, cfg, ws, sk);
-    if (!ok && gd != nullptr) ok = process_key<kCtaThreads, MODE>(T, w, keys.tt[w], keys.conc[w], ent, cfg, wg, sk);
+    bool ok = process_key<kCtaThreads, MODE>(T, w, mixed ? 1 : 0, keys.tt[w], keys.conc[w], ent, cfg, ws, sk);
+    if (!ok && gd != nullptr) ok = process_key<kCtaThreads, MODE>(T, w, mixed ? 1 : 0, keys.tt[w], keys.conc[w], ent, cfg, wg, sk);
     if (!ok && threadIdx.x == 0) atomicOr(sk.flags, FLAG_MISSING);
   }
 }
@@ -804,17 +822,18 @@ __global__ void __launch_bounds__(kCtaThreads) k_step(DevTable P0, DevTable P1, 
   if (s_e == kEntryEmpty) {
     PoolWS ws{(double*)smem, (int32_t*)(smem + kCtaCap * 8), kCtaCap, scr, dsh, rows, ncache,
               ncache + kCtaCache, kCtaCache};
-    bool ok = process_key<kCtaThreads, 0>(T, 0, t, c, idx, cfg, ws, sk);
+    bool ok = process_key<kCtaThreads, 0>(T, 0, ph, t, c, idx, cfg, ws, sk);
     if (!ok && gd != nullptr) {
       PoolWS wg{gd, gb, gcap, scr, dsh, rows, ncache, ncache + kCtaCache, kCtaCache};
-      ok = process_key<kCtaThreads, 0>(T, 0, t, c, idx, cfg, wg, sk);
+      ok = process_key<kCtaThreads, 0>(T, 0, ph, t, c, idx, cfg, wg, sk);
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     const long long e = *(volatile long long*)map_entry_ptr(sk.map, idx);
     if (e <= 0) {
-      publish_step(out, 0.0, -1, (*sk.flags & FLAG_ARENA) ? FLAG_ARENA : FLAG_MISSING, seq);
+      publish_step(out, 0.0, -1, *sk.flags & FLAG_ARENA ? FLAG_ARENA : *sk.flags & FLAG_BADPOOL ? FLAG_BADPOOL : FLAG_MISSING,
+                   seq);
       return;
     }
     Pcg64 g = load_pcg(st6);
@@ -1008,9 +1027,6 @@ struct emu_oracle_s {
   int64_t nk_cap = 0;  // allocated new-key capacity (lazy)
   KeyWin* kw = nullptr;
   long long* resv = nullptr;
-  double* cd = nullptr;
-  int32_t* cb = nullptr;
-  int64_t cand_cap = 0;
   // CTA global scratch
   double* gd = nullptr;
   int32_t* gb = nullptr;
@@ -1051,8 +1067,18 @@ static Sink make_sink(emu_oracle_t o) {
   s.arena_cap = o->arena_cap;
   s.arena_used = o->arena_used;
   s.flags = &o->ctl->flags;
+  s.bad_key = o->ctl->bad_key;
   s.kmax = o->kmax;
   return s;
+}
+
+// FLAG_BADPOOL: fail the call naming the first offending key.
+static int bad_pool_error(emu_oracle_t o, cudaStream_t s) {
+  int bk[4] = {0, 0, 0, 0};
+  EMU_CUDA(cudaMemcpyAsync(bk, o->ctl->bad_key, sizeof(bk), cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  return fail(EMU_ERR_CUDA, "internal error: invalid pool (K > min(floor, buckets)) for key phase=" +
+                                std::to_string(bk[1]) + " tt=" + std::to_string(bk[2]) + " conc=" + std::to_string(bk[3]));
 }
 
 static int oracle_flush(emu_oracle_t o, cudaStream_t s) {
@@ -1213,8 +1239,6 @@ void emu_oracle_destroy(emu_oracle_t o) {
   cudaFree(o->esc2);
   cudaFree(o->kw);
   cudaFree(o->resv);
-  cudaFree(o->cd);
-  cudaFree(o->cb);
   cudaFree(o->gd);
   cudaFree(o->gb);
   cudaFree(o->pcg);
@@ -1271,17 +1295,14 @@ static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
   cudaFree(o->esc2);
   cudaFree(o->kw);
   cudaFree(o->resv);
-  cudaFree(o->cd);
-  cudaFree(o->cb);
   o->nk_tt = nullptr;
   o->nk_c = nullptr;
   o->nk_p = nullptr;
   o->nk_e = nullptr;
   o->esc = nullptr;
+  o->esc2 = nullptr;
   o->kw = nullptr;
   o->resv = nullptr;
-  o->cd = nullptr;
-  o->cb = nullptr;
   o->nk_cap = 0;
   int rc;
   if ((rc = dalloc(&o->nk_tt, need)) || (rc = dalloc(&o->nk_c, need)) || (rc = dalloc(&o->nk_p, need)) ||
@@ -1494,6 +1515,7 @@ int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc
     if ((rc = read_flags(o, s, &flags))) return rc;
     if (flags) {
       if (++attempts > 16) return fail(EMU_ERR_CUDA, "oracle could not fit a chunk after 16 retries");
+      if (flags & FLAG_BADPOOL) return bad_pool_error(o, s);
       if (!(flags & (FLAG_ARENA | FLAG_HASH)))
         return fail(EMU_ERR_CUDA, "internal error: pool missing after build (flags=" + std::to_string(flags) + ")");
       chunk = recover(o, flags, n, s, &rc);
@@ -1529,6 +1551,7 @@ int emu_oracle_sample_pcg64(emu_oracle_t o, const int32_t* q_tt, const int32_t* 
     if ((rc = read_flags(o, s, &flags))) return rc;
     if (flags) {
       if (++attempts > 16) return fail(EMU_ERR_CUDA, "oracle could not fit a chunk after 16 retries");
+      if (flags & FLAG_BADPOOL) return bad_pool_error(o, s);
       if (!(flags & (FLAG_ARENA | FLAG_HASH)))
         return fail(EMU_ERR_CUDA, "internal error: pool missing after build (flags=" + std::to_string(flags) + ")");
       chunk = recover(o, flags, n, s, &rc);
@@ -1666,6 +1689,7 @@ int emu_oracle_prefetch(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_co
     if (rc) return rc;
     int flags = 0;
     if ((rc = read_flags(o, s, &flags))) return rc;
+    if (flags & FLAG_BADPOOL) return bad_pool_error(o, s);
     if (!(flags & (FLAG_ARENA | FLAG_HASH))) return EMU_OK;
     recover(o, flags, n, s, &rc);
     if (rc) return rc;
@@ -1783,6 +1807,7 @@ int emu_oracle_step(emu_oracle_t o, int32_t tt, int32_t conc, int32_t phase, dou
       continue;
     }
     EMU_CUDA(cudaStreamSynchronize(s));
+    if (f & FLAG_BADPOOL) return bad_pool_error(o, s);
     int rc = EMU_OK;
     if (f & FLAG_HASH) rc = alloc_hash(o, o->map.hcap * 4);
     if (!rc) rc = oracle_flush(o, s);
@@ -1817,21 +1842,24 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
   int64_t* xK = nullptr;
   int64_t* doff = nullptr;
   int rc;
-  auto cleanup = [&]() {
-    cudaFree(xb);
-    cudaFree(xd);
-    cudaFree(xp);
-    cudaFree(xc);
-    cudaFree(xK);
-    cudaFree(doff);
-  };
+  struct Scratch {  // freed on every return path
+    int32_t*& xb;
+    double *&xd, *&xp, *&xc;
+    int64_t *&xK, *&doff;
+    ~Scratch() {
+      cudaFree(xb);
+      cudaFree(xd);
+      cudaFree(xp);
+      cudaFree(xc);
+      cudaFree(xK);
+      cudaFree(doff);
+    }
+  } scratch{xb, xd, xp, xc, xK, doff};
   if ((rc = dalloc(&xb, chunkU * kmax)) || (rc = dalloc(&xd, chunkU * kmax)) || (rc = dalloc(&xp, chunkU * kmax)) ||
       (rc = dalloc(&xc, chunkU * kmax)) || (rc = dalloc(&xK, chunkU)) || (rc = dalloc(&doff, chunkU))) {
-    cleanup();
     return rc;
   }
   if ((rc = ensure_key_capacity(o, chunkU))) {
-    cleanup();
     return rc;
   }
   std::vector<int64_t> hK((size_t)chunkU);
@@ -1883,7 +1911,6 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
     EMU_CUDA(cudaStreamSynchronize(s));
     for (int64_t u = 0; u < n; u++) {
       if (hK[u] < 0 || hK[u] > kmax) {
-        cleanup();
         return fail(EMU_ERR_CUDA, "emu_oracle_pool: key " + std::to_string(u0 + u) + " got no valid pool (K=" +
                                       std::to_string(hK[u]) + ")");
       }
@@ -1898,7 +1925,6 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
       EMU_CUDA(cudaStreamSynchronize(s));
     }
   }
-  cleanup();
   EMU_CUDA(cudaMemcpyAsync(pool_off, off.data(), 8 * (U + 1), cudaMemcpyHostToDevice, s));
   if (table_of_key) {
     EMU_LAUNCH("table_of_key", s, k_table_of_key<<<grid_for(U, 256, 1024), 256, 0, s>>>(key_phase, U, o->plane_tab[0], o->plane_tab[1], table_of_key));
@@ -1916,6 +1942,17 @@ extern "C" int emu_stats_read(unsigned long long* out32) {
   EMU_CUDA(cudaMemcpyFromSymbol(out32, emu::g_stats, sizeof(unsigned long long) * 32));
   unsigned long long z[32] = {0};
   EMU_CUDA(cudaMemcpyToSymbol(emu::g_stats, z, sizeof(z)));
+  return EMU_OK;
+}
+#endif
+
+#ifdef EMU_CHECK
+// Debug builds: number of failed device invariant checks since the last read.
+extern "C" int emu_check_read(unsigned long long* n) {
+  EMU_CUDA(cudaDeviceSynchronize());
+  EMU_CUDA(cudaMemcpyFromSymbol(n, emu::g_check_fail, sizeof(unsigned long long)));
+  unsigned long long z = 0;
+  EMU_CUDA(cudaMemcpyToSymbol(emu::g_check_fail, &z, sizeof(z)));
   return EMU_OK;
 }
 #endif

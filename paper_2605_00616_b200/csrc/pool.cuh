@@ -45,6 +45,23 @@ __device__ unsigned long long g_stats[32];
   } while (0)
 #endif
 
+// Debug-build invariant checks (build with -DEMU_CHECK; `make check`): a failed
+// check prints the key and bumps g_check_fail, read by emu_check_read().
+#ifdef EMU_CHECK
+__device__ unsigned long long g_check_fail;
+#define EMU_DCHECK(cond, ...)                 \
+  do {                                        \
+    if (!(cond)) {                            \
+      printf(__VA_ARGS__);                    \
+      atomicAdd(&::emu::g_check_fail, 1ULL);  \
+    }                                         \
+  } while (0)
+#else
+#define EMU_DCHECK(cond, ...) \
+  do {                        \
+  } while (0)
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int64_t kInfW = 1LL << 40;
 
@@ -143,6 +160,28 @@ __device__ __forceinline__ int64_t upper_bound_i32(const int32_t* a, int64_t lo,
 __device__ __forceinline__ bool cand_less(double da, int32_t ba, double db, int32_t bb) {
   return da < db || (da == db && ba < bb);
 }
+
+// Debug builds: the sorted candidates ws[0..pos) are strictly increasing in
+// (distance, bucket) and every bucket index is valid.
+template <int NT>
+__device__ __forceinline__ void check_sorted(const DevTable& T, const PoolWS& ws, int64_t pos, int64_t C, int32_t t,
+                                             int32_t c, int tag) {
+#ifdef EMU_CHECK
+  EMU_DCHECK(pos >= 0 && pos <= C && pos <= ws.cap, "CHECK pos tag=%d NT=%d key=(%d,%d) pos=%lld C=%lld cap=%lld\n",
+             tag, NT, t, c, (long long)pos, (long long)C, (long long)ws.cap);
+  for (int64_t i = Grp<NT>::rank(); i < pos; i += NT) {
+    const int32_t bb = ws.b[i];
+    EMU_DCHECK(bb >= 0 && bb < T.nb, "CHECK bucket tag=%d NT=%d key=(%d,%d) i=%lld/%lld bb=%d nb=%lld\n", tag, NT, t,
+               c, (long long)i, (long long)pos, bb, (long long)T.nb);
+    if (i > 0)
+      EMU_DCHECK(cand_less(ws.d[i - 1], ws.b[i - 1], ws.d[i], bb),
+                 "CHECK order tag=%d NT=%d key=(%d,%d) i=%lld/%lld (%.17g,%d) !< (%.17g,%d)\n", tag, NT, t, c,
+                 (long long)i, (long long)pos, ws.d[i - 1], ws.b[i - 1], ws.d[i], bb);
+  }
+  Grp<NT>::sync();
+#endif
+}
+
 
 template <int NT>
 __device__ void bitonic_sort(double* d, int32_t* b, int64_t P) {
@@ -276,14 +315,21 @@ __device__ int64_t pool_search_grow(const DevTable& T, int32_t t, int32_t c, int
       }
       carry += tot;
     }
+    check_sorted<NT>(T, ws, C, C, t, c, 3);
     if (K < 0) {
+      EMU_DCHECK(!(cov_t && cov_c) || T.ns < mfloor, "CHECK exhaustive(grow) NT=%d key=(%d,%d) C=%lld ns=%lld\n", NT, t,
+                 c, (long long)C, (long long)T.ns);
       if (cov_t && cov_c) return C;  // the table holds fewer than mfloor samples
       continue;
     }
     double et = cov_t ? __longlong_as_double(0x7ff0000000000000LL) : norm_dist(Wt + 1, 0, span_t, span_c);
     double ec = cov_c ? __longlong_as_double(0x7ff0000000000000LL) : norm_dist(0, Wc + 1, span_t, span_c);
     double d_edge = fmin(et, ec);
-    if (ws.d[K - 1] < d_edge) return K;
+    // read d_K, then sync: a faster thread returning K starts pool_finish,
+    // which overwrites ws.d with masses (WAR race -> non-uniform returns)
+    const double dK = ws.d[K - 1];
+    G::sync();
+    if (dK < d_edge) return K;
   }
   return -1;  // unreachable for a finite table
 }
@@ -494,6 +540,8 @@ __device__ int64_t prefix_k(const DevTable& T, const int32_t* sb, int64_t C, int
     long long cnt = 0;
     if (j < lim) {
       const int32_t bb = sb[j];
+      EMU_DCHECK(bb >= 0 && bb < T.nb, "CHECK prefix_k NT=%d j=%lld bb=%d nb=%lld C=%lld\n", NT, (long long)j, bb,
+                 (long long)T.nb, (long long)C);
       const int64_t o0 = T.bkt_off[bb];
       cnt = T.bkt_off[bb + 1] - o0;
       if (j < ws.ncache) {
@@ -544,6 +592,7 @@ __device__ __forceinline__ void append_cand(bool in, double d, int32_t bb, const
   }
   if (in) {
     const int o = base + __popc(m & ((1u << lane) - 1u));
+    EMU_DCHECK(o >= 0 && o < ws.cap, "CHECK append_cand NT=%d o=%d cap=%lld\n", NT, o, (long long)ws.cap);
     ws.d[o] = d;
     ws.b[o] = bb;
   }
@@ -819,14 +868,25 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
     if (P > 1) bitonic_sort<NT>(ws.d, ws.b, P);
   }
   EMU_PHASE(4);
+  check_sorted<NT>(T, ws, pos, C, t, c, 1);
   const int64_t K = prefix_k<NT>(T, ws.b, pos, mfloor, ws);
   EMU_PHASE(5);
   EMU_STAT(10, K);
   EMU_STAT(11, 1);
-  if (K < 0) return (w.cov_t && w.cov_c) ? pos : -2;
+  if (K < 0) {
+    EMU_DCHECK(!(w.cov_t && w.cov_c) || pos < mfloor || T.ns < mfloor,
+               "CHECK exhaustive(sat) NT=%d key=(%d,%d) pos=%d C=%d nb=%lld ns=%lld dmax=%g\n", NT, t, c, pos, C,
+               (long long)T.nb, (long long)T.ns, dmax);
+    return (w.cov_t && w.cov_c) ? pos : -2;
+  }
   const double et = w.cov_t ? __longlong_as_double(0x7ff0000000000000LL) : dist_tab(T, w.Wt + 1, 0, span_t, span_c);
   const double ec = w.cov_c ? __longlong_as_double(0x7ff0000000000000LL) : dist_tab(T, 0, w.Wc + 1, span_t, span_c);
-  return ws.d[K - 1] < fmin(et, ec) ? K : -2;
+  // every thread reads d_K before any returns: the caller's pool_finish
+  // overwrites ws.d (a group whose warps raced here returned non-uniformly and
+  // desynchronised its barriers -- the round-1 out-of-grid known issue)
+  const double dK = ws.d[K - 1];
+  G::sync();
+  return dK < fmin(et, ec) ? K : -2;
 }
 
 // ------------------------------------------------- thread-per-key SAT passes
@@ -1092,6 +1152,7 @@ __device__ int64_t pool_from_window(const DevTable& T, int32_t t, int32_t c, int
     bitonic_sort<32>(ws.d, ws.b, P);
   }
   EMU_PHASE(4);
+  check_sorted<32>(T, ws, pos, kw.cap, t, c, 2);
   const int64_t K = prefix_k<32>(T, ws.b, pos, mfloor, ws);
   EMU_PHASE(5);
   EMU_STAT(10, K);
@@ -1102,7 +1163,9 @@ __device__ int64_t pool_from_window(const DevTable& T, int32_t t, int32_t c, int
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   const double et = cov_t ? kInf : dist_tab(T, kw.Wt + 1, 0, span_t, span_c);
   const double ec = cov_c ? kInf : dist_tab(T, 0, kw.Wc + 1, span_t, span_c);
-  return ws.d[K - 1] < fmin(et, ec) ? K : -2;
+  const double dK = ws.d[K - 1];
+  __syncwarp();
+  return dK < fmin(et, ec) ? K : -2;
 }
 
 // Dispatcher: SAT search when the table has a grid, else (or if the SAT
@@ -1133,6 +1196,7 @@ __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, 
   PoolWS ws = ws_in;
   ws.d += sorted_off;
   ws.b += sorted_off;
+  EMU_DCHECK(K >= 1, "CHECK pool_finish NT=%d K=%lld\n", NT, (long long)K);
   const bool use_cache = cached && K <= ws.ncache;
   for (int64_t j = G::rank(); j < K; j += NT) {
     int32_t bb = ws.b[j];

@@ -449,18 +449,31 @@ def test_functional_api_cache_is_bounded():
         assert len(orc_mod._tables_cache) <= orc_mod._TABLES_CACHE_MAX
 
 
+@pytest.fixture(scope="module")
+def big_packs():
+    """1M-record GPU-built canonical packs (llama and sparse generators) + oracle tables."""
+    out = {}
+    for gen, fn in (("llama", records_llama), ("sparse", records_sparse)):
+        rec = fn(1_000_000, 3)
+        out[gen] = (build_pack_arrays(*rec, num_gpu_blocks=1000, canonical=True), O.build(*rec, canonical=True))
+    return out
+
+
+def _oog_keys(gen, n, seed):
+    rng = np.random.default_rng(seed)
+    kt = rng.integers(-10, 140_000 if gen == "sparse" else 3000, n).astype(np.int32)  # tt beyond the table on both sides
+    kc = rng.integers(-3, 300, n).astype(np.int32)
+    kp = rng.integers(0, 2, n).astype(np.uint8)
+    return kt, kc, kp
+
+
 @pytest.mark.parametrize("gen", ["llama", "sparse"])
 def test_device_search_index_matches_host_index(gen, monkeypatch):
     """The table build's search index (summed-area tables, occupancy bitmap,
     row bases, column index) is built on the device; EMU_INDEX_HOST=1 builds it
-    on the host.  Both must give bit-identical pools for 20k keys inside the grid
-    (out-of-grid batches: see test_large_out_of_grid_batches_known_issue)."""
+    on the host.  Both must give bit-identical pools for 20k keys in and out of the grid."""
     rec = (records_llama if gen == "llama" else records_sparse)(1_000_000, 3)
-    rng = np.random.default_rng(5)
-    n = 20_000
-    kt = rng.integers(1, 2049 if gen == "llama" else 131_073, n)  # keys inside the table's grid
-    kc = rng.integers(1, 257, n)
-    kp = rng.integers(0, 2, n)
+    kt, kc, kp = _oog_keys(gen, 20_000, 5)
     out = []
     for host in ("0", "1"):
         monkeypatch.setenv("EMU_INDEX_HOST", host)
@@ -471,16 +484,26 @@ def test_device_search_index_matches_host_index(gen, monkeypatch):
         assert np.array_equal(g, w)
 
 
-@pytest.mark.xfail(strict=False, reason="known issue (DESIGN.md §6): the group tier intermittently faults or "
-                                        "returns a wrong pool for keys outside the table's tt range in large "
-                                        "random pool batches")
-def test_large_out_of_grid_batches_known_issue():
-    """Runs in a subprocess: a device fault there must not poison this process's context."""
-    import subprocess
-    import sys
-
-    from conftest import ROOT
-
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "idx_repro.py")], capture_output=True, text=True,
-                       timeout=600, env={**os.environ, "IDX": "dev", "ROUNDS": "4"})
-    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-2000:]
+@pytest.mark.parametrize("gen,floor", [("llama", 32), ("sparse", 32), ("sparse", 256)])
+def test_large_out_of_grid_batches_vs_oracle(big_packs, gen, floor):
+    """Round-1 known issue, fixed: the group tier read d_K after faster warps had
+    started pool_finish (which overwrites the workspace with masses), returned
+    non-uniformly and desynchronised its barriers -- intermittent wrong pools /
+    illegal addresses for keys outside the table's range in large batches.
+    20k in/out-of-grid keys, 6 rounds, each round vs the CPU oracle (pools through
+    emu_oracle_pool, and 100k cache-path draws through emu_oracle_sample)."""
+    pack, tabs = big_packs[gen]
+    kt, kc, kp = _oog_keys(gen, 20_000, 5 + floor)
+    want = O.pools(tabs, kt, kc, kp, floor)
+    rng = np.random.default_rng(9)
+    qi = rng.integers(0, len(kt), 100_000)
+    us, ui = explicit_uniforms(len(qi), 11)
+    want_s = O.sample_batch(tabs, kt[qi], kc[qi], kp[qi], floor, mode="explicit", u_sel=us, u_idx=ui, threads=8)
+    for r in range(6):
+        orc = LatencyOracle(pack, OracleConfig(reliability_floor=floor))
+        got = orc.pools(kt, kc, kp)
+        for g, w in zip(got[:5], want[:5]):
+            assert np.array_equal(g, w), f"round {r}"
+        lat, sidx = orc.sample_batch(kt[qi], kc[qi], kp[qi], rng="explicit", u_sel=us, u_idx=ui)
+        assert np.array_equal(sidx, want_s[1]) and np.array_equal(lat, want_s[0]), f"round {r}"
+        del orc
