@@ -51,7 +51,64 @@ def parse():
     ap.add_argument("--rng", default="explicit", choices=["explicit", "philox"])
     ap.add_argument("--cpu-sample", type=int, default=100_000, help="queries in the CPU baseline sample")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / roofline / cpu / p50 legs")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher + collectives only, on CPU over gloo (no kernels): tests/test_dist.py")
     return ap.parse_args()
+
+
+def launch_ranks(args) -> bool:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec under
+    torch.distributed.run with N ranks on this node (one process per GPU,
+    rendezvous on 127.0.0.1).  Returns False when already a rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def run_dry(args):
+    """The multi-rank plumbing of run_b200 on CPU (gloo): rank env, the packed
+    table broadcast, query shards, barrier-bracketed timing with the max over
+    ranks, and rank 0's JSON line.  No kernels run (and none are claimed)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import emu_oracle as O  # stand-in table builder on CPU (test only)
+    from paper_2605_00616_b200.dist import all_reduce_max, broadcast_soas
+    from paper_2605_00616_b200.profile import TableSoA
+    from paper_2605_00616_b200.workloads import queries_llama, records_llama
+
+    rank, size, _ = env_rank()
+    if size > 1:
+        dist.init_process_group("gloo")
+    soas = None
+    if rank == 0:
+        soas = [TableSoA(t.tt, t.conc, t.off, t.samples) for t in O.build(*records_llama(args.records, 0),
+                                                                          canonical=True)]
+    got = broadcast_soas(soas, 0, "cpu") if size > 1 else None
+    nb = [int(g[0].numel()) for g in got] if got else [len(s.tt) for s in soas]
+    Q = args.queries
+    qt, _, _ = queries_llama(Q, 1 + rank)
+    if size > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        np.sort(qt)  # placeholder work per step
+    ms = all_reduce_max((time.perf_counter() - t0) * 1e3 / max(args.steps, 1), device="cpu")
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": size, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": ms, "queries_per_rank": Q, "buckets": nb, "gpu_launches": 0}), flush=True)
+    if size > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def env_rank():
@@ -324,7 +381,10 @@ def run_b200(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    launch_ranks(args)
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

@@ -2,14 +2,15 @@
 
 * Queries shard naturally: each rank owns a contiguous range
   of the query stream (or whole scenarios) -- no collective in the query loop.
-* The immutable profile table is replicated once: ``broadcast_tables`` sends
-  the three canonical tables' SoA from ``src`` with one NCCL broadcast per
-  array over NVLink.
+* The immutable profile table is replicated once: ``broadcast_tables`` packs
+  the three canonical tables' SoA into one buffer and sends it from ``src``
+  with one NCCL broadcast over NVLink (after a 96-byte size header).
 * The offline build range-partitions records on tt (``partition_by_tt`` picks
   splitters from an all-reduced tt histogram, ``exchange_records`` moves each
-  record to its owner with one all_to_all); each rank builds its tt slice and
-  ``gather_tables`` concatenates the slices in rank order, which is already
-  the global (tt, conc) order because the slices are disjoint tt ranges.
+  record to its owner with one all_to_all per column); each rank builds its tt
+  slice and ``all_gather_tables`` re-replicates the slices (one all_gather of
+  the packed payloads) in rank order, which is already the global (tt, conc)
+  order because the slices are disjoint tt ranges.
 
 The collective helpers take plain tensors so the host logic is exercised on
 CPU with the gloo backend (tests/test_dist.py); the CUDA path passes CUDA
@@ -39,24 +40,53 @@ def shard_range(n: int, rank: int, size: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def pack_arrays(arrays: list[torch.Tensor]) -> tuple[torch.Tensor, torch.Tensor]:
+    """(header, payload): element counts int64[n] and one uint8 buffer holding
+    every array's bytes, each padded to 8 B (so every slice views back aligned)."""
+    dev = arrays[0].device if arrays else torch.device("cpu")
+    header = torch.tensor([a.numel() for a in arrays], dtype=torch.int64, device=dev)
+    parts = []
+    for a in arrays:
+        if a.numel() == 0:
+            continue
+        raw = a.contiguous().reshape(-1).view(torch.uint8)
+        parts.append(raw)
+        if raw.numel() % 8:
+            parts.append(torch.zeros(8 - raw.numel() % 8, dtype=torch.uint8, device=dev))
+    payload = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.uint8, device=dev)
+    return header, payload
+
+
+def _payload_bytes(counts, dtypes) -> int:
+    return sum((int(n) * torch.empty(0, dtype=dt).element_size() + 7) // 8 * 8 for n, dt in zip(counts, dtypes))
+
+
+def unpack_arrays(counts, payload: torch.Tensor, dtypes) -> list[torch.Tensor]:
+    """Inverse of pack_arrays: zero-copy typed views into `payload`."""
+    out, o = [], 0
+    for n, dt in zip(counts, dtypes):
+        nb = int(n) * torch.empty(0, dtype=dt).element_size()
+        out.append(payload[o:o + nb].view(dt) if nb else torch.empty(0, dtype=dt, device=payload.device))
+        o += (nb + 7) // 8 * 8
+    return out
+
+
 def broadcast_arrays(arrays: list[torch.Tensor] | None, dtypes: list[torch.dtype], src: int = 0,
                      device: str | torch.device = "cuda") -> list[torch.Tensor]:
-    """Broadcast a list of 1-D tensors from `src` (receivers pass None)."""
+    """Broadcast a list of 1-D tensors from `src` (receivers pass None): one
+    broadcast of the element counts, then ONE broadcast of the packed payload."""
     rank, _ = world()
-    sizes = torch.zeros(len(dtypes), dtype=torch.int64, device=device)
+    header = torch.zeros(len(dtypes), dtype=torch.int64, device=device)
+    payload = None
     if rank == src:
-        sizes = torch.tensor([a.numel() for a in arrays], dtype=torch.int64, device=device)
-    dist.broadcast(sizes, src)
-    out = []
-    for i, dt in enumerate(dtypes):
-        if rank == src:
-            t = arrays[i].to(device=device, dtype=dt).contiguous()
-        else:
-            t = torch.empty(int(sizes[i].item()), dtype=dt, device=device)
-        if t.numel():
-            dist.broadcast(t, src)
-        out.append(t)
-    return out
+        header, payload = pack_arrays([a.to(device=device, dtype=dt) for a, dt in zip(arrays, dtypes)])
+    dist.broadcast(header, src)
+    counts = header.tolist()
+    if rank != src:
+        payload = torch.empty(_payload_bytes(counts, dtypes), dtype=torch.uint8, device=device)
+    if payload.numel():
+        dist.broadcast(payload, src)
+    return unpack_arrays(counts, payload, dtypes)
 
 
 def broadcast_soas(soas: list[TableSoA] | None, src: int = 0, device="cuda") -> list[list[torch.Tensor]]:
@@ -69,23 +99,64 @@ def broadcast_soas(soas: list[TableSoA] | None, src: int = 0, device="cuda") -> 
     return [got[4 * i:4 * i + 4] for i in range(3)]
 
 
+TABLE_DTYPES = [dt for _ in range(3) for _, dt in _FIELDS]
+
+
+def table_arrays(tables) -> list[torch.Tensor]:
+    """The 12 device arrays [tt, conc, off, samples] x (decode, mixed, combined) of a DeviceTables."""
+    arrs = [tables.device_arrays(i) for i in range(3)]
+    return [a[k] for a in arrs for k in ("bkt_tt", "bkt_conc", "bkt_off", "samples")]
+
+
 def broadcast_tables(tables, src: int = 0):
-    """Replicate a DeviceTables handle from `src` to every rank (NCCL over NVLink)."""
+    """Replicate a DeviceTables handle from `src` to every rank: the 12 arrays
+    travel as one packed payload (one NCCL broadcast over NVLink, after a
+    96-byte size header); receivers rebuild their search indexes locally."""
     from .device import DeviceTables
 
     rank, size = world()
     if size == 1:
         return tables
-    if rank == src:
-        arrs = [tables.device_arrays(i) for i in range(3)]
-        flat = [a[k] for a in arrs for k in ("bkt_tt", "bkt_conc", "bkt_off", "samples")]
-    else:
-        flat = None
-    got = broadcast_arrays(flat, [dt for _ in range(3) for _, dt in _FIELDS], src, "cuda")
+    got = broadcast_arrays(table_arrays(tables) if rank == src else None, TABLE_DTYPES, src, "cuda")
     if rank == src:
         return tables
-    torch.cuda.synchronize()
+    torch.cuda.current_stream().synchronize()
     return DeviceTables.from_device(got)
+
+
+def all_gather_tables(local: list[torch.Tensor]) -> list[torch.Tensor]:
+    """Re-replicate a range-partitioned build: every rank
+    holds the 12 arrays of its tt slice; one all_gather of the size headers and
+    one all_gather of the packed payloads give every rank all slices, which are
+    concatenated in rank order (already the global (tt, conc) order: the slices
+    are disjoint, ascending tt ranges) with bucket offsets rebased.  Works on
+    CUDA tensors (NCCL) and CPU tensors (gloo)."""
+    rank, size = world()
+    dev = local[0].device
+    header, payload = pack_arrays([a.to(dtype=dt) for a, dt in zip(local, TABLE_DTYPES)])
+    headers = torch.empty(size * len(TABLE_DTYPES), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(headers, header)
+    counts = headers.view(size, len(TABLE_DTYPES)).tolist()
+    nbytes = [_payload_bytes(c, TABLE_DTYPES) for c in counts]
+    mx = max(nbytes)
+    buf = torch.zeros(mx, dtype=torch.uint8, device=dev)
+    buf[: payload.numel()] = payload
+    allbuf = torch.empty(size * mx, dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(allbuf, buf)
+    per_rank = [unpack_arrays(counts[r], allbuf[r * mx:(r + 1) * mx], TABLE_DTYPES) for r in range(size)]
+    out = []
+    for t in range(3):
+        tt = torch.cat([p[4 * t] for p in per_rank])
+        conc = torch.cat([p[4 * t + 1] for p in per_rank])
+        smp = torch.cat([p[4 * t + 3] for p in per_rank])
+        offs, base = [], 0
+        for p in per_rank:
+            o = p[4 * t + 2]
+            offs.append(o[:-1] + base if o.numel() else o)
+            base += p[4 * t + 3].numel()
+        offs.append(torch.tensor([base], dtype=torch.int64, device=dev))
+        out += [tt, conc, torch.cat(offs), smp]
+    return out
 
 
 # ------------------------------------------------------------ range-partitioned build
@@ -101,13 +172,9 @@ def partition_by_tt(tt_local: torch.Tensor, size: int, tt_max: int | None = None
     hist = torch.bincount(t, minlength=tt_max + 1)[: tt_max + 1].to(torch.int64)
     dist.all_reduce(hist)
     cum = torch.cumsum(hist, 0)
-    total = int(cum[-1].item())
-    cuts = [0]
-    for k in range(1, size):
-        cuts.append(int(torch.searchsorted(cum, torch.tensor(total * k // size, device=cum.device),
-                                           right=True).item()))
-    cuts.append(tt_max + 1)
-    cuts = np.maximum.accumulate(np.array(cuts))
+    targets = (cum[-1] * torch.arange(1, size, device=cum.device)) // size
+    inner = torch.searchsorted(cum, targets, right=True).tolist()  # one device->host read
+    cuts = np.maximum.accumulate(np.array([0] + inner + [tt_max + 1]))
     return torch.tensor(cuts, dtype=torch.int64)
 
 
@@ -131,32 +198,15 @@ def exchange_records(cols: list[torch.Tensor], tt: torch.Tensor, splitters: torc
     return out
 
 
-def gather_soas(local: list[TableSoA]) -> list[TableSoA]:
-    """Concatenate per-rank tt-slices of the three tables in rank order
-    (all_gather of sizes, then of each array); offsets are rebased."""
-    rank, size = world()
-    res = []
-    for s in local:
-        parts = {}
-        for f, dt in _FIELDS:
-            a = torch.as_tensor(np.ascontiguousarray(getattr(s, f) if f != "off" else getattr(s, f)[:-1]))
-            n = torch.tensor([a.numel()], dtype=torch.int64)
-            ns = [torch.zeros(1, dtype=torch.int64) for _ in range(size)]
-            dist.all_gather(ns, n)
-            mx = max(int(x.item()) for x in ns)
-            pad = torch.zeros(mx, dtype=dt)
-            pad[: a.numel()] = a.to(dt)
-            bufs = [torch.zeros(mx, dtype=dt) for _ in range(size)]
-            dist.all_gather(bufs, pad)
-            parts[f] = [b[: int(k.item())] for b, k in zip(bufs, ns)]
-        counts = [int(p.numel()) for p in parts["samples"]]
-        base = np.concatenate([[0], np.cumsum(counts)])
-        off = [parts["off"][r].numpy().astype(np.int64) + base[r] for r in range(size)]
-        res.append(TableSoA(torch.cat(parts["tt"]).numpy().astype(np.int32),
-                            torch.cat(parts["conc"]).numpy().astype(np.int32),
-                            np.concatenate(off + [np.array([base[-1]], np.int64)]),
-                            torch.cat(parts["samples"]).numpy()))
-    return res
+def gather_soas(local: list[TableSoA], device=None) -> list[TableSoA]:
+    """Host-SoA wrapper of all_gather_tables (CPU tensors under gloo, CUDA under NCCL)."""
+    if device is None:
+        device = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    flat = [torch.as_tensor(np.ascontiguousarray(getattr(s, f))).to(device) for s in local for f, _ in _FIELDS]
+    got = all_gather_tables(flat)
+    return [TableSoA(got[4 * i].cpu().numpy().astype(np.int32), got[4 * i + 1].cpu().numpy().astype(np.int32),
+                     got[4 * i + 2].cpu().numpy().astype(np.int64), got[4 * i + 3].cpu().numpy())
+            for i in range(3)]
 
 
 def all_reduce_max(x: float, device="cuda") -> float:

@@ -129,3 +129,36 @@ def test_range_partitioned_build_gloo():
 
 def test_query_shards_reproduce_single_stream_gloo():
     _run(_query_shards)
+
+
+def test_pack_unpack_round_trip():
+    from paper_2605_00616_b200.dist import TABLE_DTYPES, pack_arrays, unpack_arrays
+
+    rng = np.random.default_rng(0)
+    arrs = []
+    for dt in TABLE_DTYPES:
+        n = int(rng.integers(0, 9))
+        arrs.append(torch.as_tensor(rng.integers(-5, 5, n)).to(dt))
+    header, payload = pack_arrays(arrs)
+    assert payload.numel() % 8 == 0
+    got = unpack_arrays(header.tolist(), payload, TABLE_DTYPES)
+    for g, a in zip(got, arrs):
+        assert g.dtype == a.dtype and torch.equal(g, a)
+
+
+def test_bench_launcher_spawns_ranks():
+    """`python bench.py --gpus 2` re-execs itself under torch.distributed.run
+    (2 ranks, 127.0.0.1 rendezvous); --dry-run keeps it on CPU over gloo."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2",
+                        "--warmup", "1", "--records", "20000", "--queries", "50000"], capture_output=True, text=True,
+                       timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["dry_run"] and line["buckets"][2] > 0
