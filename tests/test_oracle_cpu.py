@@ -217,3 +217,45 @@ def test_build_rejects_invalid_records():
     with pytest.raises(O.BuildError) as e:
         O.build(np.array([2, 2]), np.array([2, 2]), np.zeros(2), np.array([0.1, float("nan")]))
     assert e.value.index == 1 and e.value.code == 5
+
+
+# ----------------------------------------- bench configs: C2 and C3 (reference-made goldens)
+def _big_tables(gen, g):
+    from conftest import records_sha, soa_digest
+    from paper_2605_00616_b200.workloads import records_llama, records_sparse
+
+    rec = (records_llama if gen == "c2" else records_sparse)(1_000_000, 0)
+    assert records_sha(*rec) == str(g["records_sha256"]), "generator drifted from the golden records"
+    tabs = O.build(*rec, canonical=True)
+    assert [soa_digest(t.tt, t.conc, t.off, t.samples) for t in tabs] == [str(x) for x in g["canon_digest"]]
+    return tabs
+
+
+def test_c2_oracle_matches_reference(c2_golden):
+    """C2 (1M-record Llama-shaped pack): table digests, pools + probabilities of
+    2,000 bench-workload keys and 500 out-of-range keys, and the reference
+    LatencyOracle's 10,000-draw PCG64 stream with its final state."""
+    from conftest import check_full_pools, pool_digests
+
+    g = c2_golden
+    tabs = _big_tables("c2", g)
+    off, bkt, dist, prob, cdf, tid = O.pools(tabs, g["key_tt"], g["key_conc"], g["key_phase"], 32)
+    assert np.array_equal(pool_digests(off, bkt, dist, prob, tid, tabs), g["pool_digest"])
+    check_full_pools(off, bkt, dist, prob, tid, tabs, g, "pool_")
+    st = O.pcg64_state6(0)
+    lat, _ = O.sample_pcg64(tabs, g["seq_tt"], g["seq_conc"], g["seq_phase"], 32, state6=st)
+    assert np.array_equal(lat, g["lat_seq"])
+    assert st.tolist() == g["final_state"].tolist()
+
+
+@pytest.mark.parametrize("floor", [32, 256])
+def test_c3_oracle_matches_reference(c3_golden, floor):
+    """C3 (sparse long-context, 1M records): pools of 800 bench-workload keys and
+    200 out-of-range keys at M = 32 and 256."""
+    from conftest import check_full_pools, pool_digests
+
+    g = c3_golden
+    tabs = _big_tables("c3", g)
+    off, bkt, dist, prob, cdf, tid = O.pools(tabs, g["key_tt"], g["key_conc"], g["key_phase"], floor)
+    assert np.array_equal(pool_digests(off, bkt, dist, prob, tid, tabs), g[f"m{floor}_digest"])
+    check_full_pools(off, bkt, dist, prob, tid, tabs, g, f"m{floor}_")
