@@ -300,7 +300,8 @@ def run_b200(args):
         for _ in range(2):
             step()
         kern = {}
-        for name in ("flush", "mark", "pool_prep", "pool_warp", "pool_grp", "pool_cta", "sample"):
+        for name in ("flush", "mark", "pool_prep", "tile_bin", "scan", "tile_scatter", "pool_tile", "pool_warp", "pool_grp",
+                     "pool_cta", "sample"):
             t, n = _lib.profile_read(name)
             kern[name] = {"ms_per_launch": t / max(n, 1), "launches": n}
         _lib.profile_enable(False)

@@ -26,6 +26,7 @@
 #include "emu_internal.cuh"
 #include "prof.h"
 #include "pool.cuh"
+#include "scan.cuh"
 #include "tables.h"
 
 namespace emu {
@@ -67,6 +68,10 @@ struct BatchCtl {
   int esc2_work;
   int grp_pad;
   int bad_key[4];  // first key whose pool failed validation: claimed flag, phase, tt, conc
+  int tile_work;   // tile tier: chunk counter
+  int tile_total;  // tile tier: keys binned
+  int fb_n;        // keys handed from the tile tier to the warp tier
+  int fb_work;
 };
 
 struct Keys {
@@ -97,6 +102,11 @@ struct Cfg {
   int64_t floor;
   double p, eps;
 };
+}  // namespace emu
+
+#include "pool_tile.cuh"
+
+namespace emu {
 
 // Result of one engine step, written by k_step straight into mapped pinned
 // host memory; the host spins on `seq` (no memcpy, no stream sync).
@@ -332,7 +342,8 @@ __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t*
 template <int MODE>
 __global__ void __launch_bounds__(kWarpThreads, EMU_WARP_MINB) k_pool_warp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
                                                             const KeyWin* kw, const long long* resv, int* work,
-                                                            int* esc_list, int* esc_count) {
+                                                            int* esc_list, int* esc_count, const int* list,
+                                                            const int* list_n) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = smem + warp * kWarpBytes;
@@ -346,7 +357,8 @@ __global__ void __launch_bounds__(kWarpThreads, EMU_WARP_MINB) k_pool_warp(DevTa
   ws.o = ws.n + kWarpCap / 2;
   ws.ncache = kWarpCap / 2;
   ws.cap = kWarpCap;
-  const int64_t n = keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
+  // all new keys, or (after the tile tier) the keys it handed over
+  const int64_t n = list ? (int64_t)*list_n : keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
   int64_t w_end = 0, w = 0;
   for (;;) {
     if (w >= w_end) {  // grab keys two at a time (dynamic balance, half the atomics)
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__(kWarpThreads, EMU_WARP_MINB) k_pool_warp(DevTa
       w_end = w + 2;
     }
     if (w >= n) break;
-    const int64_t wk = w++;
+    const int64_t wk = list ? (int64_t)list[w++] : w++;
     const bool mixed = keys.ph[wk] != 0;
     const DevTable& T = mixed ? P1 : P0;
     const int64_t ent = keys.entry ? keys.entry[wk] : 0;
@@ -376,6 +388,104 @@ __global__ void __launch_bounds__(kWarpThreads, EMU_WARP_MINB) k_pool_warp(DevTa
       int e = atomicAdd(esc_count, 1);
       esc_list[e] = (int)wk;
     }
+  }
+}
+
+// Tile tier (pool_tile.cuh): a warp per 32 consecutive keys of the
+// (phase, conc, tt)-ordered new-key list, a lane per key; keys that do not fit
+// go to fb_list for the warp tier.
+template <int MODE>
+__global__ void __launch_bounds__(kTileThreads, EMU_TILE_MINB)
+    k_pool_tile(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk, TileIdx ti, const KeyWin* __restrict__ kw,
+                const long long* __restrict__ resv, const int* __restrict__ order, const int* __restrict__ off,
+                const int* __restrict__ total, int* work, int* fb_list, int* fb_n) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  TileWarp& tw = reinterpret_cast<TileWarp*>(smem)[threadIdx.x >> 5];
+  const int n0 = ti.base[1] < ti.nb ? off[ti.base[1]] : *total;
+  const int p1 = (n0 + 31) & ~31;
+  const int nslots = p1 + (*total - n0);
+  const int nch = (nslots + 31) >> 5;
+  for (;;) {
+    int ch = 0;
+    if (lane == 0) ch = atomicAdd(work, 1);
+    ch = __shfl_sync(kFull, ch, 0);
+    if (ch >= nch) break;
+    const int pos = ch * 32 + lane;
+    const int ph = ch * 32 >= p1 ? 1 : 0;  // a tile never straddles the planes
+    const DevTable& T = ph ? P1 : P0;
+    const int w = (pos < nslots && (pos < n0 || pos >= p1)) ? order[pos] : -1;
+    EMU_DCHECK(w < (keys.count_dev ? *keys.count_dev : keys.count), "CHECK tile w=%d pos=%d n0=%d p1=%d nslots=%d\n", w,
+               pos, n0, p1, nslots);
+    KeyWin k;
+    k.flags = 0;
+    int32_t t = 0, c = 0;
+    if (w >= 0) {
+      k = kw[w];
+      t = keys.tt[w];
+      c = keys.conc[w];
+    }
+    const bool has = w >= 0 && k.i0 <= k.i1 && k.j0 <= k.j1;
+    const int i0 = __reduce_min_sync(kFull, has ? k.i0 : 0x7fffffff), i1 = __reduce_max_sync(kFull, has ? k.i1 : -1);
+    const int j0 = __reduce_min_sync(kFull, has ? k.j0 : 0x7fffffff), j1 = __reduce_max_sync(kFull, has ? k.j1 : -1);
+    int Cu = 0;
+    if (i0 <= i1 && j0 <= j1) {
+      Win u;
+      u.i0 = i0;
+      u.i1 = i1;
+      u.j0 = j0;
+      u.j1 = j1;
+      Cu = sat_rect(T.bsat, (int32_t)T.gnc + 1, u);
+    }
+    EMU_STAT(16, 1);
+    EMU_STAT(17, Cu);
+    if (Cu <= kTileU && Cu > 0) Cu = tile_enum_union(T, i0, i1, j0, j1, tw);
+    if (Cu < 0 || Cu > kTileU) {  // union too wide for the tile: every key goes to the warp tier
+      if (w >= 0) EMU_LSTAT(18, 1);
+      warp_push(fb_list, fb_n, w >= 0, w);
+      continue;
+    }
+    int K = -2;
+    if (w >= 0) {
+      K = tile_search(T, t, c, k, cfg.floor, Cu, tw);
+      EMU_LSTAT(K == -2 ? 19 : K == -3 ? 20 : K == -4 ? 21 : 22, 1);
+    }
+    EMU_DCHECK(K != 0 && K <= 64, "CHECK tile K=%d w=%d Cu=%d\n", K, w, Cu);
+    warp_push(fb_list, fb_n, w >= 0 && K < 0, w);
+    if (w >= 0 && K > 0) {
+      if (MODE == 0) {
+        const long long r = resv[w];
+        long long* ep = map_entry_ptr(sk.map, keys.entry[w]);
+        if (K > cfg.floor || K > T.nb) {
+          report_bad_pool(sk, ph, t, c);
+        } else if (K == 1) {  // direct entry: the bucket itself
+          const int4 q = tw.u[tw.j[lane]];
+          *ep = make_entry_direct(T.bkt_off[q.w], q.z);
+        } else {
+          long long start = r;
+          if (start == -1) {
+            const unsigned long long tot = (unsigned long long)pool_total_slots(K);
+            const unsigned long long st = atomicAdd(sk.arena_used, tot);
+            start = (st + tot <= (unsigned long long)sk.arena_cap) ? (long long)st : -2LL;
+            if (start < 0) atomicOr(sk.flags, FLAG_ARENA);
+          }
+          if (start >= 0) {
+            const PoolPtrs pp = pool_ptrs(sk.arena, start, K);
+            tile_finish<0>(T, K, cfg, tw, &pp, nullptr, nullptr, nullptr, nullptr);
+            *ep = make_entry(K, start);
+          }
+        }
+      } else {
+        const int64_t base = (int64_t)w * sk.kmax;
+        if (K > sk.kmax) {
+          sk.x_K[w] = K + (int64_t)1000000;
+        } else {
+          tile_finish<1>(T, K, cfg, tw, nullptr, sk.x_bkt + base, sk.x_dist + base, sk.x_prob + base, sk.x_cdf + base);
+          sk.x_K[w] = K;
+        }
+      }
+    }
+    __syncwarp();  // the next tile overwrites the union list
   }
 }
 
@@ -988,6 +1098,8 @@ static int set_kernel_attrs() {
   if (g_attrs_set) return EMU_OK;
   EMU_CUDA(cudaFuncSetAttribute(k_pool_warp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpBytes * kWarpsPerCta));
   EMU_CUDA(cudaFuncSetAttribute(k_pool_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpBytes * kWarpsPerCta));
+  EMU_CUDA(cudaFuncSetAttribute(k_pool_tile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
+  EMU_CUDA(cudaFuncSetAttribute(k_pool_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
   EMU_CUDA(cudaFuncSetAttribute(k_pool_grp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGrpSmem));
   EMU_CUDA(cudaFuncSetAttribute(k_pool_grp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGrpSmem));
   EMU_CUDA(cudaFuncSetAttribute(k_pool_cta<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem));
@@ -1027,6 +1139,16 @@ struct emu_oracle_s {
   int64_t nk_cap = 0;  // allocated new-key capacity (lazy)
   KeyWin* kw = nullptr;
   long long* resv = nullptr;
+  // tile tier: ordering bins and per-key scratch (EMU_TILE=0 disables the tier)
+  bool tile_on = true;
+  TileIdx ti{};
+  int* tile_cnt = nullptr;   // ti.nb + 1
+  int* tile_off = nullptr;   // ti.nb + 1
+  int* tile_part = nullptr;  // scan partials
+  int* kbin = nullptr;
+  int* krank = nullptr;
+  int* order = nullptr;
+  int* fb_list = nullptr;
   // CTA global scratch
   double* gd = nullptr;
   int32_t* gb = nullptr;
@@ -1185,6 +1307,24 @@ int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, doubl
     emu_oracle_destroy(o);
     return rc;
   }
+  {
+    const char* tv = getenv("EMU_TILE");
+    o->tile_on = !(tv && tv[0] == '0');
+    int64_t nb = 0;
+    for (int ph = 0; ph < 2; ph++) {
+      const DevTable& T = o->plane[ph];
+      o->ti.base[ph] = nb;
+      o->ti.nbt[ph] = T.gnt > 0 ? (T.gnt + (1 << kTileRowShift) - 1) >> kTileRowShift : 0;
+      nb += o->ti.nbt[ph] * T.gnc;
+    }
+    o->ti.nb = nb;
+    if (nb == 0 || nb > (1LL << 26)) o->tile_on = false;
+    if (o->tile_on && ((rc = dalloc(&o->tile_cnt, nb + 1)) || (rc = dalloc(&o->tile_off, nb + 1)) ||
+                       (rc = dalloc(&o->tile_part, (nb + kScanTile) / kScanTile + 1)))) {
+      emu_oracle_destroy(o);
+      return rc;
+    }
+  }
   if (cudaHostAlloc((void**)&o->step_host, sizeof(StepOut), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&o->step_dev, o->step_host, 0) != cudaSuccess ||
       cudaHostAlloc((void**)&o->flags_host, sizeof(int) * 4, cudaHostAllocDefault) != cudaSuccess) {
@@ -1239,6 +1379,13 @@ void emu_oracle_destroy(emu_oracle_t o) {
   cudaFree(o->esc2);
   cudaFree(o->kw);
   cudaFree(o->resv);
+  cudaFree(o->tile_cnt);
+  cudaFree(o->tile_off);
+  cudaFree(o->tile_part);
+  cudaFree(o->kbin);
+  cudaFree(o->krank);
+  cudaFree(o->order);
+  cudaFree(o->fb_list);
   cudaFree(o->gd);
   cudaFree(o->gb);
   cudaFree(o->pcg);
@@ -1295,6 +1442,11 @@ static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
   cudaFree(o->esc2);
   cudaFree(o->kw);
   cudaFree(o->resv);
+  cudaFree(o->kbin);
+  cudaFree(o->krank);
+  cudaFree(o->order);
+  cudaFree(o->fb_list);
+  o->kbin = o->krank = o->order = o->fb_list = nullptr;
   o->nk_tt = nullptr;
   o->nk_c = nullptr;
   o->nk_p = nullptr;
@@ -1307,8 +1459,8 @@ static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
   int rc;
   if ((rc = dalloc(&o->nk_tt, need)) || (rc = dalloc(&o->nk_c, need)) || (rc = dalloc(&o->nk_p, need)) ||
       (rc = dalloc(&o->nk_e, need)) || (rc = dalloc(&o->esc, need)) || (rc = dalloc(&o->esc2, need)) ||
-      (rc = dalloc(&o->kw, need)) ||
-      (rc = dalloc(&o->resv, need)))
+      (rc = dalloc(&o->kw, need)) || (rc = dalloc(&o->resv, need)) || (rc = dalloc(&o->kbin, need)) ||
+      (rc = dalloc(&o->krank, need)) || (rc = dalloc(&o->order, need + 64)) || (rc = dalloc(&o->fb_list, need)))
     return rc;
   o->nk_cap = need;
   return EMU_OK;
@@ -1327,8 +1479,92 @@ static int grid_knob(int which, int dflt) {  // EMU_GRIDS=<prep>,<sample> CTAs p
 }
 #define kPrepGrid (kNumSMs * grid_knob(0, 4))
 
-// Build missing pools for a chunk of queries: mark -> prep (thread/key) ->
-// warp (sort, prefix, CDF) -> CTA escalation.  No host round trip.
+struct CntIn {
+  const int* c;
+  __device__ int operator()(int64_t i) const { return c[i]; }
+};
+struct OffOut {
+  int* o;
+  __device__ void operator()(int64_t i, int v) const { o[i] = v; }
+};
+
+// The pool tiers after k_mark / explicit keys: prep (thread per key: SAT window,
+// arena reservation) -> tile tier (counting sort of the keys into (phase, conc,
+// tt) bins, warp per 32 keys, lane per key) -> warp tier for the keys the tile
+// tier handed over (or all keys) -> group tier -> CTA tier.
+template <int MODE>
+static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, cudaStream_t s, bool sync_check) {
+  static const bool tile_debug = getenv("EMU_TILE_DEBUG") != nullptr;
+  auto chk = [&](const char* what) -> int {
+    EMU_CUDA(cudaGetLastError());
+    if (sync_check || tile_debug) {
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return cuda_fail(e, what);
+    }
+    if (tile_debug) {
+      BatchCtl c{};
+      EMU_CUDA(cudaMemcpy(&c, o->ctl, sizeof(c), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[emu] after %s: new %d work %d tile_work %d tile_total %d fb_n %d fb_work %d esc %d flags %d\n",
+              what, c.new_count, c.work, c.tile_work, c.tile_total, c.fb_n, c.fb_work, c.esc_count, c.flags);
+    }
+    return EMU_OK;
+  };
+  int rc;
+  EMU_LAUNCH("pool_prep", s, k_pool_prep<MODE><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
+                                                                          o->kw, o->resv));
+  if ((rc = chk("pool_prep"))) return rc;
+  const int* list = nullptr;
+  const int* list_n = nullptr;
+  int* warp_work = &o->ctl->work;
+  if (o->tile_on) {
+    EMU_CUDA(cudaMemsetAsync(o->tile_cnt, 0, sizeof(int) * o->ti.nb, s));
+    EMU_LAUNCH("tile_bin", s, k_tile_bin<MODE><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, o->ti,
+                                                                          o->kw, o->resv, o->tile_cnt, o->kbin, o->krank,
+                                                                          o->fb_list, &o->ctl->fb_n));
+    if ((rc = chk("tile_bin"))) return rc;
+    EMU_CUDA(device_excl_scan<int>(CntIn{o->tile_cnt}, OffOut{o->tile_off}, o->ti.nb, o->tile_part,
+                                   &o->ctl->tile_total, s));
+    if ((rc = chk("tile_scan"))) return rc;
+    EMU_LAUNCH("tile_scatter", s, k_tile_scatter<MODE><<<kPrepGrid, 256, 0, s>>>(keys, o->ti, o->kbin, o->krank,
+                                                                                  o->tile_off, &o->ctl->tile_total,
+                                                                                  o->order));
+    if ((rc = chk("tile_scatter"))) return rc;
+    if (getenv("EMU_TILE_DEBUG")) {
+      BatchCtl c{};
+      EMU_CUDA(cudaMemcpyAsync(&c, o->ctl, sizeof(c), cudaMemcpyDeviceToHost, s));
+      EMU_CUDA(cudaStreamSynchronize(s));
+      std::vector<int> off(o->ti.nb), ord(c.tile_total + 64);
+      EMU_CUDA(cudaMemcpy(off.data(), o->tile_off, 4 * o->ti.nb, cudaMemcpyDeviceToHost));
+      EMU_CUDA(cudaMemcpy(ord.data(), o->order, 4 * (c.tile_total + 64), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[emu] tile debug: n=%lld binned=%d fb=%d nb=%lld base1=%lld off[base1]=%d ord[0..4]=%d %d %d %d\n",
+              (long long)keys.count, c.tile_total, c.fb_n, (long long)o->ti.nb, (long long)o->ti.base[1],
+              o->ti.base[1] < o->ti.nb ? off[o->ti.base[1]] : -1, ord[0], ord[1], ord[2], ord[3]);
+    }
+    EMU_LAUNCH("pool_tile", s, k_pool_tile<MODE><<<kNumSMs * EMU_TILE_MINB, kTileThreads, kTileBytes, s>>>(
+                                   o->plane[0], o->plane[1], keys, o->cfg, sk, o->ti, o->kw, o->resv, o->order,
+                                   o->tile_off, &o->ctl->tile_total, &o->ctl->tile_work, o->fb_list, &o->ctl->fb_n));
+    if ((rc = chk("pool_tile"))) return rc;
+    list = o->fb_list;
+    list_n = &o->ctl->fb_n;
+    warp_work = &o->ctl->fb_work;
+  }
+  EMU_LAUNCH("pool_warp", s, k_pool_warp<MODE><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
+                                 o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, warp_work, o->esc,
+                                 &o->ctl->esc_count, list, list_n));
+  if ((rc = chk("pool_warp"))) return rc;
+  EMU_LAUNCH("pool_grp", s, k_pool_grp<MODE><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(o->plane[0], o->plane[1], keys,
+                                                                                     o->cfg, sk, &o->ctl->esc_work,
+                                                                                     o->esc, &o->ctl->esc_count, o->esc2,
+                                                                                     &o->ctl->esc2_count));
+  if ((rc = chk("pool_grp"))) return rc;
+  EMU_LAUNCH("pool_cta", s, k_pool_cta<MODE><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys,
+                                                                                     o->cfg, sk, &o->ctl->esc2_work,
+                                                                                     o->esc2, &o->ctl->esc2_count, o->gd,
+                                                                                     o->gb, o->gcap));
+  return chk("pool_cta");
+}
+
+// Build missing pools for a chunk of queries: mark -> the pool tiers.  No host round trip.
 static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t Q,
                          cudaStream_t s) {
   int rc = ensure_key_capacity(o, std::min<int64_t>(Q, map_entries(o)));
@@ -1361,24 +1597,19 @@ static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, c
   }
   EMU_CUDA(cudaGetLastError());
   Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
-  Sink sk = make_sink(o);
-  EMU_LAUNCH("pool_prep", s, k_pool_prep<0><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw,
-                                                                      o->resv));
-  EMU_CUDA(cudaGetLastError());
-  EMU_LAUNCH("pool_warp", s, k_pool_warp<0><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
-                                 o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, &o->ctl->work, o->esc, &o->ctl->esc_count));
-  EMU_CUDA(cudaGetLastError());
-  EMU_LAUNCH("pool_grp", s, k_pool_grp<0><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg,
-                                                                                  sk, &o->ctl->esc_work, o->esc,
-                                                                                  &o->ctl->esc_count, o->esc2,
-                                                                                  &o->ctl->esc2_count));
-  EMU_CUDA(cudaGetLastError());
-  EMU_LAUNCH("pool_cta", s, k_pool_cta<0><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys, o->cfg,
-                                                                                  sk, &o->ctl->esc2_work, o->esc2,
-                                                                                  &o->ctl->esc2_count, o->gd, o->gb,
-                                                                                  o->gcap));
-  EMU_CUDA(cudaGetLastError());
-  return EMU_OK;
+  rc = launch_pool_tiers<0>(o, keys, make_sink(o), s, false);
+  static const bool tile_stats = [] {
+    const char* v = getenv("EMU_TILE_STATS");
+    return v && v[0] == '1';
+  }();
+  if (!rc && tile_stats) {  // tuning aid: how many new keys each tier took
+    BatchCtl c{};
+    EMU_CUDA(cudaMemcpyAsync(&c, o->ctl, sizeof(c), cudaMemcpyDeviceToHost, s));
+    EMU_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "[emu] new keys %d  tile-binned %d  to warp tier %d  to group tier %d  to CTA tier %d\n",
+            c.new_count, c.tile_total, o->tile_on ? c.fb_n : c.new_count, c.esc_count, c.esc2_count);
+  }
+  return rc;
 }
 
 static int read_flags(emu_oracle_t o, cudaStream_t s, int* flags) {
@@ -1875,38 +2106,7 @@ int emu_oracle_pool(emu_oracle_t o, const int32_t* key_tt, const int32_t* key_co
     sk.x_prob = xp;
     sk.x_cdf = xc;
     sk.x_K = xK;
-    EMU_LAUNCH("pool_prep", s, k_pool_prep<1><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
-                                                                        o->kw, o->resv));
-    EMU_CUDA(cudaGetLastError());
-    if (sync_check) {
-      const cudaError_t e_ = cudaStreamSynchronize(s);
-      if (e_ != cudaSuccess) return cuda_fail(e_, "emu_oracle_pool after pool_prep");
-    }
-    EMU_LAUNCH("pool_warp", s, k_pool_warp<1><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
-                                   o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, &o->ctl->work, o->esc, &o->ctl->esc_count));
-    EMU_CUDA(cudaGetLastError());
-    if (sync_check) {
-      const cudaError_t e_ = cudaStreamSynchronize(s);
-      if (e_ != cudaSuccess) return cuda_fail(e_, "emu_oracle_pool after pool_warp");
-    }
-    EMU_LAUNCH("pool_grp", s, k_pool_grp<1><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(o->plane[0], o->plane[1], keys,
-                                                                                    o->cfg, sk, &o->ctl->esc_work,
-                                                                                    o->esc, &o->ctl->esc_count, o->esc2,
-                                                                                    &o->ctl->esc2_count));
-    EMU_CUDA(cudaGetLastError());
-    if (sync_check) {
-      const cudaError_t e_ = cudaStreamSynchronize(s);
-      if (e_ != cudaSuccess) return cuda_fail(e_, "emu_oracle_pool after pool_grp");
-    }
-    EMU_LAUNCH("pool_cta", s, k_pool_cta<1><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys,
-                                                                                    o->cfg, sk, &o->ctl->esc2_work,
-                                                                                    o->esc2, &o->ctl->esc2_count, o->gd,
-                                                                                    o->gb, o->gcap));
-    EMU_CUDA(cudaGetLastError());
-    if (sync_check) {
-      const cudaError_t e_ = cudaStreamSynchronize(s);
-      if (e_ != cudaSuccess) return cuda_fail(e_, "emu_oracle_pool after pool_cta");
-    }
+    if ((rc = launch_pool_tiers<1>(o, keys, sk, s, sync_check))) return rc;
     EMU_CUDA(cudaMemcpyAsync(hK.data(), xK, 8 * n, cudaMemcpyDeviceToHost, s));
     EMU_CUDA(cudaStreamSynchronize(s));
     for (int64_t u = 0; u < n; u++) {

@@ -33,6 +33,7 @@ __device__ unsigned long long g_stats[32];
   } while (0)
 #define EMU_STAT(i, v) \
   do { if ((threadIdx.x & 31) == 0) atomicAdd(&::emu::g_stats[i], (unsigned long long)(v)); } while (0)
+#define EMU_LSTAT(i, v) atomicAdd(&::emu::g_stats[i], (unsigned long long)(v))
 #else
 #define EMU_PHASE_BEGIN() \
   do {                    \
@@ -42,6 +43,9 @@ __device__ unsigned long long g_stats[32];
   } while (0)
 #define EMU_STAT(i, v) \
   do {                 \
+  } while (0)
+#define EMU_LSTAT(i, v) \
+  do {                  \
   } while (0)
 #endif
 

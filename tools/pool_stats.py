@@ -24,3 +24,8 @@ print("keys", keys, "avg C_sat %.1f  avg pos %.1f  avg K %.1f" % (buf[8] / keys,
 tot = sum(int(buf[i]) for i in range(7))
 for i, n in enumerate(names):
     print(f"{n:10s} {buf[i] / keys:9.0f} cycles/key  {100 * int(buf[i]) / tot:5.1f}%")
+tiles, cu = int(buf[16]), int(buf[17])
+if tiles:
+    tk = int(buf[22]) + int(buf[19]) + int(buf[20]) + int(buf[21]) + int(buf[18])
+    print("tile tier: tiles %d  avg union %.1f  keys %d  ok %d  fallback: union %d  list %d  prefix %d  window %d  avg list %.1f"
+          % (tiles, cu / tiles, tk, buf[22], buf[18], buf[19], buf[20], buf[21], buf[23] / max(1, tk - int(buf[18]))))
