@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kTileThreads, EMU_TILE_MINB)
         if (K > cfg.floor || K > T.nb) {
           report_bad_pool(sk, ph, t, c);
         } else if (K == 1) {  // direct entry: the bucket itself
-          const int4 q = tw.u[tw.j[lane]];
+          const int4 q = tw.u[tw.j[tw.perm[lane] * 32 + lane]];
           *ep = make_entry_direct(T.bkt_off[q.w], q.z);
         } else {
           long long start = r;

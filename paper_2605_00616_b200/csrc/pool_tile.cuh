@@ -33,7 +33,7 @@
 namespace emu {
 
 constexpr int kTileU = 256;       // union candidates per tile
-constexpr int kTileL = 44;        // exact candidates per key (after the pivot)
+constexpr int kTileL = 36;        // exact candidates per key (after the pivot)
 constexpr int kTileWarps = 2;
 constexpr int kTileThreads = 32 * kTileWarps;
 constexpr int kTileRowShift = 4;  // ordering bins: 16 grid rows of one conc column
@@ -44,9 +44,11 @@ constexpr int kTileRowPath = 512; // union boxes up to this many grid rows enume
 #endif
 
 struct TileWarp {
-  int4 u[kTileU];          // union candidates in BUCKET order: (tt, conc, count, bucket)
-  double d[kTileL * 32];   // per-lane list, entry e of lane l at [e * 32 + l] (staging for the union sort)
-  uint8_t j[kTileL * 32];  // union index of that entry (= bucket order: ties in d break on it)
+  int4 u[kTileU];             // union candidates in BUCKET order: (tt, conc, count, bucket)
+  double d[kTileL * 32];      // per-lane list, entry e of lane l at [e * 32 + l] (staging for the union sort)
+  uint8_t j[kTileL * 32];     // union index of that entry (= bucket order: ties in d break on it)
+  uint8_t perm[kTileL * 32];  // sorted order: the e-th smallest entry of lane l is perm[e * 32 + l]
+  uint16_t h[32 * 32];        // per lane: pivot histogram (16 bins), then distance-bin counts (32 bins)
 };
 static_assert(kTileL * 32 * 8 >= kTileU * 16, "the union staging area lives in TileWarp::d");
 constexpr int kTileBytes = (int)sizeof(TileWarp) * kTileWarps;
@@ -256,8 +258,8 @@ __device__ __forceinline__ int tile_enum_union(const DevTable& T, int32_t i0, in
 }
 
 // Lane l of a warp handles key w (or none: w < 0).  Returns K >= 1 with the
-// lane's sorted pool in tw.d / tw.j entries [0, K), or a negative reason for
-// the warp tier (-2 list overflow, -3 prefix, -4 window test).
+// lane's pool: sorted entry e (< K) is list slot tw.perm[e * 32 + lane]; or a
+// negative reason for the warp tier (-2 list overflow, -3 prefix, -4 window test).
 __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t c, const KeyWin& k, int64_t mfloor,
                                            int Cu, TileWarp& tw) {
   const int lane = threadIdx.x & 31;
@@ -265,47 +267,70 @@ __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t
   const float inv_t = span_t ? 1.0f / (float)span_t : 0.0f, inv_c = span_c ? 1.0f / (float)span_c : 0.0f;
   const int32_t Wt = (int32_t)min(k.Wt, (int64_t)0x3fffffff), Wc = (int32_t)min(k.Wc, (int64_t)0x3fffffff);
   const bool exhaust = !(k.dmax < 1e300);
-  // r1 = r2 / sqrt(2) / (1 + 1e-9): the 8 pivots r1 (1 + (sqrt(2) - 1)(l + 1) / 8), l = 0..7
-  const double r1 = exhaust ? 0.0 : k.dmax / (1.4142135623730951 * (1.0 + 1e-9) * (1.0 + 1e-9));
   const float dmax2 = exhaust ? 3.0e38f : (float)(k.dmax * k.dmax) * (1.0f + 4e-5f);
-  const float inv_r1 = exhaust ? 0.0f : (float)(1.0 / r1);
-  const int32_t cap = (int32_t)min(mfloor, (int64_t)0x7fffff);
-  // ---- 1. membership bitmask + conservative cumulative pivot counts (uniform loop)
-  int32_t pc[8];
-#pragma unroll
-  for (int l = 0; l < 8; l++) pc[l] = 0;
+  uint16_t* h = tw.h + lane;  // lane-strided
+  // ---- 1. membership bitmask: own window and float distance <= dmax (uniform loop over the union)
   uint32_t mask[kTileU / 32];
 #pragma unroll
   for (int wd = 0; wd < kTileU / 32; wd++) {
     uint32_t mw = 0;
     if (wd * 32 < Cu) {
       const int lim = min(32, Cu - wd * 32);
-      for (int bi = 0; bi < lim; bi++) {
-        const int4 q = tw.u[wd * 32 + bi];
-        const int32_t dt = t - q.x, dc = c - q.y;
-        const float ft = (float)dt * inv_t, fc = (float)dc * inv_c;
-        const float sf = ft * ft + fc * fc;
-        const bool in = abs(dt) <= Wt && abs(dc) <= Wc && sf <= dmax2;
-        mw |= (in ? 1u : 0u) << bi;
-        // bin of a value >= the exact distance: counts in bins <= l are certainly within pivot l
-        const float v = sqrtf(sf) * (1.0f + 4e-5f) * inv_r1;
-        const int lb = v <= 1.0f ? 0 : (int)fminf(ceilf((v - 1.0f) * 19.313708498984761f) - 1.0f, 8.0f);
-        const int32_t z = in ? min(q.z, cap) : 0;
+      for (int b0 = 0; b0 < lim; b0 += 4) {
 #pragma unroll
-        for (int l = 0; l < 8; l++) pc[l] += lb <= l ? z : 0;
+        for (int x = 0; x < 4; x++) {
+          const int bi = b0 + x;
+          const int4 q = tw.u[wd * 32 + bi];  // entries past Cu hold stale data; masked below
+          const int32_t dt = t - q.x, dc = c - q.y;
+          const float ft = (float)dt * inv_t, fc = (float)dc * inv_c;
+          const bool in = bi < lim && abs(dt) <= Wt && abs(dc) <= Wc && ft * ft + fc * fc <= dmax2;
+          mw |= (in ? 1u : 0u) << bi;
+        }
       }
     }
     mask[wd] = mw;
   }
-  // ---- 2. pivot radius, exact distances of the members within it
+  // ---- 2. pool radius bound: 16 pivots in squared distance, r1^2 (1 + (l + 1) / 16);
+  // the smallest whose disc certainly holds >= floor samples bounds d_K.  The
+  // counts use a float squared distance inflated past any rounding (never an
+  // overcount); 16-bit counters packed two per register.
   double piv = k.dmax;
   if (!exhaust) {
+    const double r1 = k.dmax / (1.4142135623730951 * (1.0 + 1e-9) * (1.0 + 1e-9));  // r2 / sqrt(2) / (1 + 1e-9)
+    const float inv_r1sq = (float)(1.0 / (r1 * r1)) * (1.0f + 4e-5f);
+    const uint32_t cap = (uint32_t)min(mfloor, (int64_t)1024);
+    uint32_t hc[8];
 #pragma unroll
-    for (int l = 7; l >= 0; l--)
-      if (pc[l] >= mfloor) piv = r1 * (1.0 + 0.41421356237309515 * (double)(l + 1) * 0.125);
-    piv = fmin(piv, k.dmax);
+    for (int r = 0; r < 8; r++) hc[r] = 0;
+#pragma unroll
+    for (int wd = 0; wd < kTileU / 32; wd++) {
+      uint32_t mw = mask[wd];
+      while (mw) {
+        const int bi = __ffs(mw) - 1;
+        mw &= mw - 1u;
+        const int4 q = tw.u[wd * 32 + bi];
+        const float ft = (float)(t - q.x) * inv_t, fc = (float)(c - q.y) * inv_c;
+        const float v = (ft * ft + fc * fc) * inv_r1sq;  // >= (exact d / r1)^2
+        const int lb = v <= 1.0f ? 0 : (int)fminf(ceilf((v - 1.0f) * 16.0f) - 1.0f, 16.0f);
+        const uint32_t z = min((uint32_t)q.z, cap) << ((lb & 1) * 16);
+#pragma unroll
+        for (int r = 0; r < 8; r++) hc[r] += (lb >> 1) == r ? z : 0u;
+      }
+    }
+    uint32_t cum = 0;
+    int lp = -1;
+#pragma unroll
+    for (int l = 0; l < 16; l++) {
+      cum += (hc[l >> 1] >> ((l & 1) * 16)) & 0xffffu;
+      if (lp < 0 && cum >= (uint32_t)mfloor) lp = l;
+    }
+    if (lp >= 0) piv = fmin(k.dmax, r1 * sqrt(1.0 + (double)(lp + 1) * 0.0625) * (1.0 + 1e-12));
   }
+  // ---- 3. members within the bound (float filter), then their exact distances
+  // (norm_dist's IEEE ops via the squared-delta tables), two at a time, counted
+  // into 32 distance bins
   const float piv2 = exhaust ? 3.0e38f : (float)(piv * piv) * (1.0f + 4e-5f);
+  const double scale = (piv > 0.0 && piv < 1e300) ? 32.0 / piv : 0.0;  // bin(d) = floor(d * scale): monotone in d
   int m = 0;
   bool ovf = false;
 #pragma unroll
@@ -316,45 +341,79 @@ __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t
       mw &= mw - 1u;
       const int jj = wd * 32 + bi;
       const int4 q = tw.u[jj];
-      const int32_t dt = t - q.x, dc = c - q.y;
-      const float ft = (float)dt * inv_t, fc = (float)dc * inv_c;
+      const float ft = (float)(t - q.x) * inv_t, fc = (float)(c - q.y) * inv_c;
       if (ft * ft + fc * fc > piv2) continue;
-      const double d = dist_tab(T, dt, dc, span_t, span_c);
-      if (!(d <= piv)) continue;
       if (m == kTileL) {
         ovf = true;
         break;
       }
-      tw.d[m * 32 + lane] = d;
       tw.j[m * 32 + lane] = (uint8_t)jj;
       m++;
     }
   }
+#pragma unroll
+  for (int l = 0; l < 32; l++) h[l * 32] = 0;
+  int m2 = 0;  // entries kept after the exact test (compacted in place)
+  for (int e = 0; e < m; e += 2) {
+    const bool two = e + 1 < m;
+    const int ja = tw.j[e * 32 + lane], jb = two ? tw.j[(e + 1) * 32 + lane] : ja;
+    const int4 qa = tw.u[ja], qb = tw.u[jb];
+    const double da = dist_tab(T, t - qa.x, c - qa.y, span_t, span_c);
+    const double db = dist_tab(T, t - qb.x, c - qb.y, span_t, span_c);
+    if (da <= piv) {
+      tw.d[m2 * 32 + lane] = da;
+      tw.j[m2 * 32 + lane] = (uint8_t)ja;
+      h[min(31, (int)(da * scale)) * 32] += 1;
+      m2++;
+    }
+    if (two && db <= piv) {
+      tw.d[m2 * 32 + lane] = db;
+      tw.j[m2 * 32 + lane] = (uint8_t)jb;
+      h[min(31, (int)(db * scale)) * 32] += 1;
+      m2++;
+    }
+  }
+  m = m2;
   EMU_LSTAT(23, m);
   if (ovf) return -2;
-  // ---- 3. selection sort by (d, bucket) until the prefix holds >= floor samples;
-  // the union is in bucket order, so the union index breaks distance ties
+  // ---- 4. bucket sort by (d, bucket): bins in order, then an insertion pass
+  // that only moves entries within a bin (an earlier bin's d is strictly
+  // smaller); the union is in bucket order, so the union index breaks ties
+  {
+    int st = 0;
+#pragma unroll
+    for (int l = 0; l < 32; l++) {
+      const int cnt = h[l * 32];
+      h[l * 32] = (uint16_t)st;
+      st += cnt;
+    }
+  }
+  for (int e = 0; e < m; e++) {
+    const int bn = min(31, (int)(tw.d[e * 32 + lane] * scale));
+    const int p = h[bn * 32];
+    h[bn * 32] = (uint16_t)(p + 1);
+    tw.perm[p * 32 + lane] = (uint8_t)e;
+  }
+  for (int p = 1; p < m; p++) {
+    const int x = tw.perm[p * 32 + lane];
+    const double dx = tw.d[x * 32 + lane];
+    int q = p;
+    while (q > 0) {
+      const int y = tw.perm[(q - 1) * 32 + lane];
+      const double dy = tw.d[y * 32 + lane];
+      if (!(dx < dy || (dx == dy && tw.j[x * 32 + lane] < tw.j[y * 32 + lane]))) break;
+      tw.perm[q * 32 + lane] = (uint8_t)y;
+      q--;
+    }
+    tw.perm[q * 32 + lane] = (uint8_t)x;
+  }
+  // ---- 5. the shortest prefix holding >= floor samples
   int64_t cum = 0;
   int K = -1;
-  for (int kk = 0; kk < m; kk++) {
-    int best = kk;
-    double bd = tw.d[kk * 32 + lane];
-    int bj = tw.j[kk * 32 + lane];
-    for (int e = kk + 1; e < m; e++) {
-      const double de = tw.d[e * 32 + lane];
-      const int je = tw.j[e * 32 + lane];
-      const bool less = de < bd || (de == bd && je < bj);
-      best = less ? e : best;
-      bd = less ? de : bd;
-      bj = less ? je : bj;
-    }
-    tw.d[best * 32 + lane] = tw.d[kk * 32 + lane];
-    tw.j[best * 32 + lane] = tw.j[kk * 32 + lane];
-    tw.d[kk * 32 + lane] = bd;
-    tw.j[kk * 32 + lane] = (uint8_t)bj;
-    cum += tw.u[bj].z;
+  for (int e = 0; e < m; e++) {
+    cum += tw.u[tw.j[tw.perm[e * 32 + lane] * 32 + lane]].z;
     if (cum >= mfloor) {
-      K = kk + 1;
+      K = e + 1;
       break;
     }
   }
@@ -363,46 +422,66 @@ __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t
     if (!(cov_t && cov_c) || !exhaust || m == 0) return -3;
     K = m;  // the table holds fewer than floor samples: every bucket (sorted above)
   }
-  // ---- 4. the exact window test (as pool_from_window)
+  // ---- 6. the exact window test (as pool_from_window)
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   const double et = cov_t ? kInf : dist_tab(T, k.Wt + 1, 0, span_t, span_c);
   const double ec = cov_c ? kInf : dist_tab(T, 0, k.Wc + 1, span_t, span_c);
-  return tw.d[(K - 1) * 32 + lane] < fmin(et, ec) ? K : -4;
+  return tw.d[tw.perm[(K - 1) * 32 + lane] * 32 + lane] < fmin(et, ec) ? K : -4;
 }
 
 // Shepard weights -> probabilities -> cdf of the lane's pool, pool_finish's
 // operation order; writes cache slots (MODE 0) or explicit outputs (MODE 1).
 template <int MODE>
 __device__ __forceinline__ void tile_finish(const DevTable& T, int K, const Cfg& cfg, TileWarp& tw, const PoolPtrs* pp,
-                                            int32_t* o_bkt,
-                                            double* o_dist, double* o_prob, double* o_cdf) {
+                                            int32_t* o_bkt, double* o_dist, double* o_prob, double* o_cdf) {
   const int lane = threadIdx.x & 31;
-  double* a = tw.d + lane;
+  double* a = tw.d + lane;              // slot s of this lane at a[s * 32]
+  const uint8_t* pm = tw.perm + lane;   // e-th smallest -> slot pm[e * 32]
   for (int e = 0; e < K; e++) {
-    const double d = a[e * 32];
-    const int4 q = tw.u[tw.j[e * 32 + lane]];
+    const int sl = pm[e * 32];
+    const double d = a[sl * 32];
+    const int4 q = tw.u[tw.j[sl * 32 + lane]];
     if (MODE == 1) {
       o_bkt[e] = q.w;
       o_dist[e] = d;
     }
     const double x = d > cfg.eps ? d : cfg.eps;
-    a[e * 32] = __dmul_rn(__ddiv_rn(1.0, shepard_pow(x, cfg.p)), (double)q.z);
+    a[sl * 32] = __dmul_rn(__ddiv_rn(1.0, shepard_pow(x, cfg.p)), (double)q.z);  // mass
   }
-  const double S = K <= 128 ? pairwise_leaf_lane(a, K) : 0.0;  // K <= floor <= 32
+  // numpy's pairwise sum (K <= floor <= 32: the 8-accumulator leaf), in sorted order
+  double S;
+  if (K < 8) {
+    S = 0.0;
+    for (int e = 0; e < K; e++) S = __dadd_rn(S, a[pm[e * 32] * 32]);
+  } else {
+    double r[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) r[q] = a[pm[q * 32] * 32];
+    int i = 8;
+    for (; i < K - (K % 8); i += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) r[q] = __dadd_rn(r[q], a[pm[(i + q) * 32] * 32]);
+    }
+    S = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                  __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < K; i++) S = __dadd_rn(S, a[pm[i * 32] * 32]);
+  }
   double acc = 0.0;
   for (int e = 0; e < K; e++) {
-    const double pr = __ddiv_rn(a[e * 32], S);
+    const int sl = pm[e * 32];
+    const double pr = __ddiv_rn(a[sl * 32], S);
     if (MODE == 1) o_prob[e] = pr;
-    acc = e == 0 ? pr : __dadd_rn(acc, pr);
-    a[e * 32] = acc;
+    acc = e == 0 ? pr : __dadd_rn(acc, pr);  // np.cumsum: sequential
+    a[sl * 32] = acc;
   }
   const double last = acc;
   for (int e = 0; e < K; e++) {
-    const double cdf = __ddiv_rn(a[e * 32], last);
+    const int sl = pm[e * 32];
+    const double cdf = __ddiv_rn(a[sl * 32], last);
     if (MODE == 1) {
       o_cdf[e] = cdf;
     } else {
-      const int4 q = tw.u[tw.j[e * 32 + lane]];
+      const int4 q = tw.u[tw.j[sl * 32 + lane]];
       pp->cdf[e] = cdf;
       pp->data[e] = make_int2((int32_t)T.bkt_off[q.w], q.z);
       if (pp->header && (e % kGroupSlots) == kGroupSlots - 1 && e < K - 1) pp->header[e / kGroupSlots] = cdf;
