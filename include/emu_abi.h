@@ -188,6 +188,12 @@ int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q
 int emu_oracle_seed_pcg64(emu_oracle_t o, const uint64_t* pcg_state6);
 int emu_oracle_get_pcg64(emu_oracle_t o, uint64_t* pcg_state6);
 int emu_oracle_step(emu_oracle_t o, int32_t tt, int32_t conc, int32_t phase, double* out_lat);
+/* emu_oracle_step is served by a resident one-warp kernel that stays up for
+ * EMU_STEP_SERVER_IDLE_US (default 100000) after the last step, so calls at the
+ * engine's cadence (engine.py:565 sleeps the sampled latency) skip the kernel
+ * launch.  A foreign device-wide synchronize waits for that timeout; park the
+ * server first (it exits on its next poll; the next step relaunches it). */
+int emu_oracle_park(emu_oracle_t o);
 
 /* Build (without drawing) the pools of n keys [dev] not cached yet -- the
  * warm-up half of emu_oracle_sample (the lazy cache of _pooled, oracle.py:200-222). */

@@ -59,6 +59,7 @@ SIGNATURES = {
     "emu_oracle_seed_pcg64": (c_int, [c_vp, c_vp]),
     "emu_oracle_get_pcg64": (c_int, [c_vp, c_vp]),
     "emu_oracle_step": (c_int, [c_vp, c_i32, c_i32, c_i32, ctypes.POINTER(c_dbl)]),
+    "emu_oracle_park": (c_int, [c_vp]),
     "emu_oracle_stats": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "emu_distance": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "emu_token_fill": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),

@@ -58,16 +58,18 @@ constexpr int kQPT = 4;  // queries per thread, interleaved for memory-level par
 constexpr int64_t kHostChunk = 1 << 20;  // queries per pipelined chunk of emu_oracle_sample_host
 
 struct BatchCtl {
+  int flags;
+  int bad_key[4];  // first key whose pool failed validation: claimed flag, phase, tt, conc
+  int ctl_pad[3];
+  // per-pass counters from here on (reset_counters): a chunk's passes keep the flags
   unsigned long long cand_used;  // candidate scratch bump pointer
   int new_count;
+  int miss_count;  // k_sweep: queries left for k_sample_list (read with new_count in one copy)
   int work;
   int esc_count;
   int esc_work;
-  int flags;
   int esc2_count;  // keys too big for the 128-thread group tier -> CTA tier
   int esc2_work;
-  int grp_pad;
-  int bad_key[4];  // first key whose pool failed validation: claimed flag, phase, tt, conc
   int tile_work;   // tile tier: chunk counter
   int tile_total;  // tile tier: keys binned
   int fb_n;        // keys handed from the tile tier to the warp tier
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 :
     uint64_t us[QPT];
     uint32_t w0[QPT];
     uint4 px[QPT];
-    double u[QPT];
+    uint64_t u[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       px[j] = make_uint4(0, 0, 0, 0);
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 :
         us[j] = (uint64_t)px[j].x | ((uint64_t)px[j].y << 32);
         w0[j] = px[j].z;
       }
-      u[j] = unit_double(us[j]);
+      u[j] = unit_k53(us[j]);
     }
     // two-level inverse-CDF lookup (header split, then one 8-slot group)
     PoolPick sl[QPT];
@@ -672,6 +674,133 @@ __global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 :
         st_stream(out_lat + i[j], lat[j], HINT);
         st_stream(out_sidx + i[j], sidx[j], HINT);
       }
+    }
+  }
+}
+
+// One query's draw from its (built) map entry e: the inverse-CDF pick and the
+// Lemire index, exactly as k_sample; writes lat / sidx of query i.
+template <int RNG>
+__device__ __forceinline__ void draw_query(const Slot* __restrict__ arena, const double* __restrict__ s0,
+                                           const double* __restrict__ s1, long long e, int ph, int64_t i,
+                                           const uint64_t* __restrict__ usel, const uint32_t* __restrict__ uidx,
+                                           uint2 key, uint64_t ctr_base, double* __restrict__ out_lat,
+                                           int32_t* __restrict__ out_sidx, bool hint) {
+  uint64_t us;
+  uint32_t w0;
+  uint4 px = make_uint4(0, 0, 0, 0);
+  if (RNG == EMU_RNG_EXPLICIT) {
+    us = ld_stream(usel + i, hint);
+    w0 = ld_stream(uidx + i, hint);
+  } else {
+    const uint64_t qid = ctr_base + (uint64_t)i;
+    px = philox4x32_10(make_uint4((uint32_t)qid, (uint32_t)(qid >> 32), 0u, 0u), key);
+    us = (uint64_t)px.x | ((uint64_t)px.y << 32);
+    w0 = px.z;
+  }
+  const PoolPick sl = pool_pick(arena, e, unit_k53(us));
+  const uint32_t k = draw_index<RNG>((uint32_t)sl.n, w0, px, ctr_base + (uint64_t)i, key);
+  const int32_t sidx = sl.soff + (int32_t)k;
+  st_stream(out_lat + i, (ph ? s1 : s0)[sidx], hint);
+  st_stream(out_sidx + i, sidx, hint);
+}
+
+// Streaming sweep for a cache that already holds most keys: ONE pass over the
+// queries.  A query whose pool is built is drawn at once; any other query is
+// appended to the miss list (and its key claimed and appended to the new-key
+// list, as k_mark does).  After the pool tiers, k_sample_list draws the misses
+// only, so each key / uniform is read from HBM once (41 B/query explicit).
+template <int RNG>
+__global__ void __launch_bounds__(kSampleThreads, 8) k_sweep(MapView m, const Slot* __restrict__ arena,
+                                                             const double* __restrict__ s0,
+                                                             const double* __restrict__ s1,
+                                                             const int32_t* __restrict__ qt,
+                                                             const int32_t* __restrict__ qc,
+                                                             const uint8_t* __restrict__ qp, int64_t Q,
+                                                             const uint64_t* __restrict__ usel,
+                                                             const uint32_t* __restrict__ uidx, uint64_t seed,
+                                                             uint64_t ctr_base, double* __restrict__ out_lat,
+                                                             int32_t* __restrict__ out_sidx, int32_t* nk_tt,
+                                                             int32_t* nk_c, uint8_t* nk_p, int64_t* nk_e, int* miss,
+                                                             BatchCtl* ctl) {
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < Q; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;  // warp-uniform trip count: every ballot has all lanes
+    const bool v = i < Q;
+    int ph = 0;
+    int32_t t = 0, c = 0;
+    if (v) {
+      ph = __ldcs(qp + i) ? 1 : 0;
+      t = __ldcs(qt + i);
+      c = __ldcs(qc + i);
+    }
+    const int64_t idx = v ? map_find<true>(m, ph, t, c) : -2;
+    const long long e = idx >= 0 ? *map_entry_ptr(m, idx) : -1;
+    if (idx == -1) atomicOr(&ctl->flags, FLAG_HASH);
+    const bool hit = e > 0;
+    if (hit) draw_query<RNG>(arena, s0, s1, e, ph, i, usel, uidx, key, ctr_base, out_lat, out_sidx, true);
+    // claim empty entries: one CAS per distinct key per warp
+    const bool cand = idx >= 0 && e == kEntryEmpty;
+    bool won = false;
+    if (__any_sync(kFull, cand)) {
+      const unsigned peers =
+          __match_any_sync(kFull, cand ? (unsigned long long)idx : (0xffffffff00000000ULL | (unsigned)lane));
+      if (cand && (__ffs(peers) - 1) == lane)
+        won = atomicCAS((unsigned long long*)map_entry_ptr(m, idx), 0ULL, (unsigned long long)kEntryPending) == 0ULL;
+    }
+    const unsigned mb = __ballot_sync(kFull, v && !hit);
+    if (mb) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&ctl->miss_count, __popc(mb));
+      base = __shfl_sync(kFull, base, 0);
+      if (v && !hit) miss[base + __popc(mb & lt)] = (int)i;
+    }
+    const unsigned wb = __ballot_sync(kFull, won);
+    if (wb) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&ctl->new_count, __popc(wb));
+      base = __shfl_sync(kFull, base, 0);
+      if (won) {
+        const int pos = base + __popc(wb & lt);
+        nk_tt[pos] = t;
+        nk_c[pos] = c;
+        nk_p[pos] = (uint8_t)ph;
+        nk_e[pos] = idx;
+      }
+    }
+  }
+}
+
+// The misses of k_sweep, after the pool tiers built their pools (gathered by
+// query index; the list is a small fraction of the sweep on a warm cache).
+template <int RNG>
+__global__ void __launch_bounds__(kSampleThreads, 8) k_sample_list(MapView m, const Slot* __restrict__ arena,
+                                                                   const double* __restrict__ s0,
+                                                                   const double* __restrict__ s1,
+                                                                   const int32_t* __restrict__ qt,
+                                                                   const int32_t* __restrict__ qc,
+                                                                   const uint8_t* __restrict__ qp,
+                                                                   const int* __restrict__ list,
+                                                                   const int* __restrict__ list_n,
+                                                                   const uint64_t* __restrict__ usel,
+                                                                   const uint32_t* __restrict__ uidx, uint64_t seed,
+                                                                   uint64_t ctr_base, double* __restrict__ out_lat,
+                                                                   int32_t* __restrict__ out_sidx, int* flags) {
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const int n = *list_n;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int64_t i = list[j];
+    const int ph = qp[i] ? 1 : 0;
+    const int64_t idx = map_find<false>(m, ph, qt[i], qc[i]);
+    const long long e = idx >= 0 ? *map_entry_ptr(m, idx) : 0;
+    if (e > 0) {
+      draw_query<RNG>(arena, s0, s1, e, ph, i, usel, uidx, key, ctr_base, out_lat, out_sidx, false);
+    } else {
+      out_lat[i] = __longlong_as_double(0x7ff8000000000000LL);
+      out_sidx[i] = -1;
+      atomicOr(flags, FLAG_MISSING);
     }
   }
 }
@@ -760,7 +889,7 @@ __global__ void __launch_bounds__(256) k_sample_c(MapView m, const Slot* __restr
       const PendingDraw P = wq[k];
       const int64_t i = tb + (P.rel & 0x3fffffff);
       const int ph = P.rel >> 30;
-      const PoolPick pk = pool_pick(arena, P.e, unit_double(P.us));
+      const PoolPick pk = pool_pick(arena, P.e, unit_k53(P.us));
       const uint32_t kk = draw_index<RNG>((uint32_t)pk.n, P.w0, make_uint4(0, 0, 0, P.pw), ctr_base + (uint64_t)i, key);
       const int32_t sidx = pk.soff + (int32_t)kk;
       __stcs(out_lat + i, (ph ? s1 : s0)[sidx]);
@@ -827,7 +956,7 @@ __global__ void __launch_bounds__(kSampleThreads, 8) k_sample_pf(MapView m, cons
       w0 = px.z;
     }
     if (e > 0) {
-      const PoolPick pk = pool_pick(arena, e, unit_double(us));
+      const PoolPick pk = pool_pick(arena, e, unit_k53(us));
       const uint32_t k = draw_index<RNG>((uint32_t)pk.n, w0, px, ctr_base + (uint64_t)i, key);
       const int32_t sidx = pk.soff + (int32_t)k;
       __stcs(out_lat + i, (ph ? s1 : s0)[sidx]);
@@ -868,8 +997,7 @@ __device__ __forceinline__ void store_pcg(uint64_t* st6, const Pcg64& g) {
 // One draw of LatencyOracle.sample on the PCG64 stream: choice() draws one
 // double; integers(n) draws buffered u32 words only when n > 1.
 __device__ __forceinline__ int32_t pcg_draw(Pcg64& g, const Slot* arena, long long e) {
-  const double u = unit_double(pcg64_next64(g));
-  const PoolPick s = pool_pick(arena, e, u);
+  const PoolPick s = pool_pick(arena, e, unit_k53(pcg64_next64(g)));
   uint32_t j = 0;
   if (s.n > 1) {
     uint32_t w0 = pcg64_next32(g);
@@ -979,14 +1107,21 @@ __global__ void k_step_hit(MapView m, const Slot* __restrict__ arena, const doub
 // a request into mapped pinned memory, lane 0 sees it over PCIe, serves it
 // exactly like k_step_hit (cached keys; misses go back to the host, which
 // launches k_step) and writes the result back into mapped memory.  It exits
-// after `idle_ns` without a request (device-wide syncs then wait at most that
-// long) or after `max_ns`; the host relaunches it on demand.  Requests carry a
-// sequence number; a (re)started server first serves any request it has not
-// served yet, so a request written while the server was exiting is never lost.
+// after `idle_ns` without a request or after `max_ns`; the host relaunches it
+// on demand.  The idle timeout (EMU_STEP_SERVER_IDLE_US, default 100 ms) is
+// longer than the engine's step cadence (it sleeps the sampled latency between
+// calls, engine.py:565: ms), so the server survives the gaps; whenever the
+// library itself needs the server gone (reallocation, destroy) or the caller
+// wants a prompt device-wide sync (emu_oracle_park), the host sets the park
+// bit in the request's phase word and the server exits on its next poll.
+// Requests carry a sequence number; a (re)started server first serves any
+// request it has not served yet, so a request written while the server was
+// exiting is never lost.
 struct __align__(16) StepReq {
   uint32_t seq;
-  int32_t tt, conc, phase;
+  int32_t tt, conc, phase;  // phase bit 31: park (exit now) when no request is pending
 };
+constexpr uint32_t kParkBit = 0x80000000u;
 
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
@@ -1009,7 +1144,7 @@ __global__ void k_step_server(MapView m, const Slot* __restrict__ arena, const d
                  : "=r"(sq), "=r"(ut), "=r"(uc), "=r"(up)
                  : "l"(req));
     if (sq != served) {
-      const int32_t t = (int32_t)ut, c = (int32_t)uc, ph = up ? 1 : 0;
+      const int32_t t = (int32_t)ut, c = (int32_t)uc, ph = (up & ~kParkBit) ? 1 : 0;
       const int64_t idx = map_find<false>(m, ph, t, c);
       const long long e = idx >= 0 ? __ldcg(map_entry_ptr(m, idx)) : 0;
       if (e <= 0) {
@@ -1022,8 +1157,7 @@ __global__ void k_step_server(MapView m, const Slot* __restrict__ arena, const d
         g.i_lo = __ldcg(st6 + 3);
         g.has_u32 = (uint32_t)__ldcg(st6 + 4);
         g.u32 = (uint32_t)__ldcg(st6 + 5);
-        const double u = unit_double(pcg64_next64(g));
-        const PoolPick pk = pool_pick<true>(arena, e, u);
+        const PoolPick pk = pool_pick<true>(arena, e, unit_k53(pcg64_next64(g)));
         uint32_t j = 0;
         if (pk.n > 1) {
           const uint32_t w0 = pcg64_next32(g);
@@ -1045,7 +1179,7 @@ __global__ void k_step_server(MapView m, const Slot* __restrict__ arena, const d
       continue;
     }
     const uint64_t now = global_ns();
-    if (now - t_last > idle_ns || now - t0 > max_ns) break;
+    if ((up & kParkBit) || now - t_last > idle_ns || now - t0 > max_ns) break;
   }
   __threadfence();
   *alive = 0;
@@ -1135,6 +1269,9 @@ struct emu_oracle_s {
   int* esc = nullptr;
   int* esc2 = nullptr;
   int64_t chunk_cap = 0;
+  bool cold = true;          // cache flushed since the last batch: the head of the next batch takes the mark path
+  int* miss = nullptr;       // k_sweep miss list (query indices)
+  int64_t miss_cap = 0;
   int64_t arena_max = 0;  // growth limit for the pool arena (slots)
   int64_t nk_cap = 0;  // allocated new-key capacity (lazy)
   KeyWin* kw = nullptr;
@@ -1170,6 +1307,7 @@ struct emu_oracle_s {
   StepOut* step_host = nullptr;  // pinned, mapped
   uint32_t step_seq = 0;
   int* flags_host = nullptr;
+  BatchCtl* ctl_host = nullptr;  // pinned: the head of BatchCtl after a k_sweep
   // host staging for emu_oracle_sample_host (pipelined: copy-in stream,
   // compute on the caller's stream, copy-out stream; one event pair per chunk)
   void* stage = nullptr;
@@ -1204,6 +1342,7 @@ static int bad_pool_error(emu_oracle_t o, cudaStream_t s) {
 }
 
 static int oracle_flush(emu_oracle_t o, cudaStream_t s) {
+  o->cold = true;
   int64_t D = 2LL * o->map.dom_tt * o->map.dom_conc;
   EMU_CUDA(cudaMemsetAsync(o->map.dense, 0, sizeof(long long) * D, s));
   EMU_LAUNCH("flush", s, k_fill_u64<<<grid_for(2 * o->map.hcap, 256, 4096), 256, 0, s>>>(o->map.hkeys, 2 * o->map.hcap, kHashEmpty));
@@ -1225,10 +1364,16 @@ int oracle_views(emu_oracle_t o, MapView* m, const Slot** arena, const double** 
 }
 }  // namespace emu
 
-// Wait for the step server to exit (<= its idle timeout) before the arrays it
-// was launched with are reallocated.
+// Park the step server (it exits on its next poll) and wait for it, before the
+// arrays it was launched with are reallocated or freed.
 static void quiesce_server(emu_oracle_t o) {
-  if (o->srv_stream) cudaStreamSynchronize(o->srv_stream);
+  if (!o->srv_stream) return;
+  if (o->req_host) {
+    volatile StepReq* rq = o->req_host;
+    rq->phase = (int32_t)kParkBit;  // seq unchanged: no request pending
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+  }
+  cudaStreamSynchronize(o->srv_stream);
 }
 
 static int alloc_hash(emu_oracle_t o, int64_t hcap) {
@@ -1327,7 +1472,8 @@ int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, doubl
   }
   if (cudaHostAlloc((void**)&o->step_host, sizeof(StepOut), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&o->step_dev, o->step_host, 0) != cudaSuccess ||
-      cudaHostAlloc((void**)&o->flags_host, sizeof(int) * 4, cudaHostAllocDefault) != cudaSuccess) {
+      cudaHostAlloc((void**)&o->flags_host, sizeof(int) * 4, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void**)&o->ctl_host, sizeof(BatchCtl), cudaHostAllocDefault) != cudaSuccess) {
     emu_oracle_destroy(o);
     return fail(EMU_ERR_CUDA, "cudaHostAlloc failed");
   }
@@ -1364,6 +1510,7 @@ int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, doubl
 }
 
 void emu_oracle_destroy(emu_oracle_t o) {
+  if (o) cudaFree(o->miss);
   if (!o) return;
   cudaFree(o->map.dense);
   cudaFree(o->map.hkeys);
@@ -1397,7 +1544,7 @@ void emu_oracle_destroy(emu_oracle_t o) {
   if (o->cp_out) cudaStreamDestroy(o->cp_out);
   cudaFree(o->flag_log);
   if (o->flag_log_host) cudaFreeHost(o->flag_log_host);
-  if (o->srv_stream) cudaStreamSynchronize(o->srv_stream);  // the server exits after its idle timeout
+  quiesce_server(o);
   if (o->srv_stream) cudaStreamDestroy(o->srv_stream);
   if (o->srv_done) cudaEventDestroy(o->srv_done);
   if (o->async_done) cudaEventDestroy(o->async_done);
@@ -1406,6 +1553,7 @@ void emu_oracle_destroy(emu_oracle_t o) {
   if (o->alive_host) cudaFreeHost(o->alive_host);
   if (o->step_host) cudaFreeHost(o->step_host);
   if (o->flags_host) cudaFreeHost(o->flags_host);
+  if (o->ctl_host) cudaFreeHost(o->ctl_host);
   delete o;
 }
 
@@ -1564,12 +1712,20 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
   return chk("pool_cta");
 }
 
+// Zero the per-pass counters of BatchCtl (the flags and bad key survive: one
+// chunk's passes report together; callers zero the whole block per chunk).
+static cudaError_t reset_counters(emu_oracle_t o, cudaStream_t s) {
+  constexpr size_t off = offsetof(BatchCtl, cand_used);
+  return cudaMemsetAsync(reinterpret_cast<char*>(o->ctl) + off, 0, sizeof(BatchCtl) - off, s);
+}
+
 // Build missing pools for a chunk of queries: mark -> the pool tiers.  No host round trip.
 static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t Q,
                          cudaStream_t s) {
   int rc = ensure_key_capacity(o, std::min<int64_t>(Q, map_entries(o)));
   if (rc) return rc;
-  EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
+  o->cold = false;
+  EMU_CUDA(reset_counters(o, s));
   {
     // EMU_MARK=<qpt>,<ctas per SM> (tuning knob).  Default 2 queries per
     // thread, up to 8 CTAs per SM: 0.124 ms per 10M-query cold sweep vs 0.153
@@ -1621,7 +1777,10 @@ static int read_flags(emu_oracle_t o, cudaStream_t s, int* flags) {
 
 // Handle a failed chunk: grow the hash on overflow; always flush the cache.
 // Returns the (possibly reduced) chunk size to retry with, or -1 if hopeless.
-static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s, int* rc) {
+// started_cold: the failed chunk began on an empty cache.  A chunk that
+// overflowed a cache filled by earlier chunks is retried whole after the flush;
+// only one that overflowed on its own is halved (bounded below by what always fits).
+static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s, int* rc, bool started_cold) {
   *rc = EMU_OK;
   if (flags & FLAG_HASH) {
     if ((*rc = alloc_hash(o, o->map.hcap * 4))) return -1;
@@ -1637,7 +1796,8 @@ static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s,
   }
   if ((*rc = oracle_flush(o, s))) return -1;
   if (flags & FLAG_ARENA) {
-    int64_t fit = std::max<int64_t>(1, o->arena_cap / std::max<int64_t>(1, o->kmax));
+    int64_t fit = std::max<int64_t>(1, o->arena_cap / std::max<int64_t>(1, pool_total_slots(o->kmax)));
+    if (!started_cold) return chunk;
     if (chunk <= 1 && fit <= 1) return -1;
     return std::min(chunk / 2 > 0 ? chunk / 2 : 1, fit);
   }
@@ -1718,6 +1878,89 @@ static int launch_sample(emu_oracle_t o, int rng_mode, const int32_t* qt, const 
   return EMU_OK;
 }
 
+// Queries of a batch on a COLD cache that take the two-pass path (k_mark ->
+// tiers -> k_sample) before the rest streams through k_sweep.  Default: all of
+// them -- splitting a cold batch's distinct keys over two tier passes costs more
+// than the second read of the key stream saves (C2 cold step 1.29 ms at a 25 %
+// head vs 0.88 ms two-pass).  EMU_SWEEP_HEAD=<fraction, %> (0: sweep everything).
+static int64_t cold_head(int64_t n) {
+  static const int pct = [] {
+    const char* v = getenv("EMU_SWEEP_HEAD");
+    return v ? std::max(0, std::min(100, atoi(v))) : 100;
+  }();
+  return std::min<int64_t>(n, (n * pct + 99) / 100);
+}
+
+// One chunk of a batch, device-resident, no host round trip: pools for the
+// keys not cached yet, then every query's draw.  Flags accumulate in ctl.
+// may_sync: the caller allows one host round trip after k_sweep, so the pool
+// tiers and k_sample_list are only launched when there are new keys / misses
+// (a warm sweep then costs one kernel, not a dozen near-empty ones); the
+// pipelined host path passes false to keep its copies overlapped.
+// *flags_out (if given): the chunk's final flags when that round trip already
+// read them (nothing launched after k_sweep), else -1.
+static int draw_chunk(emu_oracle_t o, int rng_mode, const int32_t* qt, const int32_t* qc, const uint8_t* qp,
+                      int64_t n, const uint64_t* us, const uint32_t* ui, uint64_t seed, uint64_t ctr, double* lat,
+                      int32_t* sidx, cudaStream_t s, bool may_sync, int* flags_out = nullptr) {
+  if (flags_out) *flags_out = -1;
+  const int64_t head = o->cold ? cold_head(n) : 0;
+  const int64_t m = n - head;
+  o->cold = false;
+  int rc;
+  // scratch first: reallocating after the head pass is enqueued would stall on it
+  if ((rc = ensure_key_capacity(o, std::min<int64_t>(n, map_entries(o))))) return rc;
+  if (m > o->miss_cap) {
+    cudaFree(o->miss);
+    o->miss = nullptr;
+    o->miss_cap = 0;
+    if ((rc = dalloc(&o->miss, pow2_at_least(m)))) return rc;
+    o->miss_cap = pow2_at_least(m);
+  }
+  if (head > 0) {
+    if ((rc = build_missing(o, qt, qc, qp, head, s))) return rc;
+    if ((rc = launch_sample(o, rng_mode, qt, qc, qp, head, us, ui, seed, ctr, lat, sidx, s))) return rc;
+  }
+  if (m <= 0) return EMU_OK;
+  qt += head, qc += head, qp += head, lat += head, sidx += head, ctr += (uint64_t)head;
+  if (us) us += head, ui += head;
+  EMU_CUDA(reset_counters(o, s));
+  const int grid = grid_for(m, kSampleThreads, kNumSMs * 8);
+  const uint64_t sd = seed;
+  if (rng_mode == EMU_RNG_EXPLICIT)
+    EMU_LAUNCH("sweep", s, k_sweep<EMU_RNG_EXPLICIT><<<grid, kSampleThreads, 0, s>>>(
+                               o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, m, us, ui, sd,
+                               ctr, lat, sidx, o->nk_tt, o->nk_c, o->nk_p, o->nk_e, o->miss, o->ctl));
+  else
+    EMU_LAUNCH("sweep", s, k_sweep<EMU_RNG_PHILOX><<<grid, kSampleThreads, 0, s>>>(
+                               o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, m, us, ui, sd,
+                               ctr, lat, sidx, o->nk_tt, o->nk_c, o->nk_p, o->nk_e, o->miss, o->ctl));
+  EMU_CUDA(cudaGetLastError());
+  int lgrid = kNumSMs * 4;
+  if (may_sync) {  // flags .. miss_count in one copy
+    EMU_CUDA(cudaMemcpyAsync(o->ctl_host, o->ctl, offsetof(BatchCtl, miss_count) + sizeof(int), cudaMemcpyDeviceToHost,
+                             s));
+    EMU_CUDA(cudaStreamSynchronize(s));
+    if (o->ctl_host->miss_count == 0) {  // every query was drawn in the pass
+      if (flags_out) *flags_out = o->ctl_host->flags;
+      return EMU_OK;
+    }
+    lgrid = grid_for(o->ctl_host->miss_count, kSampleThreads, kNumSMs * 4);
+  }
+  Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
+  if ((!may_sync || o->ctl_host->new_count > 0) && (rc = launch_pool_tiers<0>(o, keys, make_sink(o), s, false)))
+    return rc;
+  if (rng_mode == EMU_RNG_EXPLICIT)
+    EMU_LAUNCH("sample_list", s, k_sample_list<EMU_RNG_EXPLICIT><<<lgrid, kSampleThreads, 0, s>>>(
+                                     o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, o->miss,
+                                     &o->ctl->miss_count, us, ui, sd, ctr, lat, sidx, &o->ctl->flags));
+  else
+    EMU_LAUNCH("sample_list", s, k_sample_list<EMU_RNG_PHILOX><<<lgrid, kSampleThreads, 0, s>>>(
+                                     o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, o->miss,
+                                     &o->ctl->miss_count, us, ui, sd, ctr, lat, sidx, &o->ctl->flags));
+  EMU_CUDA(cudaGetLastError());
+  return EMU_OK;
+}
+
 extern "C" {
 
 int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc, const uint8_t* q_phase, int64_t Q,
@@ -1735,21 +1978,22 @@ int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc
   int attempts = 0;
   while (done < Q) {
     const int64_t n = std::min(chunk, Q - done);
-    int rc = build_missing(o, q_tt + done, q_conc + done, q_phase + done, n, s);
-    if (rc) return rc;
-    rc = launch_sample(o, rng_mode, q_tt + done, q_conc + done, q_phase + done, n, u_sel ? u_sel + done : nullptr,
-                       u_idx ? u_idx + done : nullptr, seed, ctr_base + (uint64_t)done, out_lat + done,
-                       out_sidx + done, s);
+    const bool cold0 = o->cold;
+    int fk = -1;
+    EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
+    int rc = draw_chunk(o, rng_mode, q_tt + done, q_conc + done, q_phase + done, n, u_sel ? u_sel + done : nullptr,
+                        u_idx ? u_idx + done : nullptr, seed, ctr_base + (uint64_t)done, out_lat + done,
+                        out_sidx + done, s, true, &fk);
     if (rc) return rc;
     EMU_CUDA(cudaGetLastError());
-    int flags = 0;
-    if ((rc = read_flags(o, s, &flags))) return rc;
+    int flags = fk;
+    if (fk < 0 && (rc = read_flags(o, s, &flags))) return rc;
     if (flags) {
       if (++attempts > 16) return fail(EMU_ERR_CUDA, "oracle could not fit a chunk after 16 retries");
       if (flags & FLAG_BADPOOL) return bad_pool_error(o, s);
       if (!(flags & (FLAG_ARENA | FLAG_HASH)))
         return fail(EMU_ERR_CUDA, "internal error: pool missing after build (flags=" + std::to_string(flags) + ")");
-      chunk = recover(o, flags, n, s, &rc);
+      chunk = recover(o, flags, n, s, &rc, cold0);
       if (rc) return rc;
       if (chunk < 0) return fail(EMU_ERR_CAPACITY, "pool arena too small for a single query's pool");
       continue;
@@ -1772,6 +2016,8 @@ int emu_oracle_sample_pcg64(emu_oracle_t o, const int32_t* q_tt, const int32_t* 
   int attempts = 0;
   while (done < Q) {
     const int64_t n = std::min(chunk, Q - done);
+    const bool cold0 = o->cold;
+    EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
     int rc = build_missing(o, q_tt + done, q_conc + done, q_phase + done, n, s);
     if (rc) return rc;
     EMU_LAUNCH("sample_pcg", s, k_sample_pcg<<<1, 32, 0, s>>>(o->map, o->arena, o->plane[0].samples, o->plane[1].samples, q_tt + done,
@@ -1785,7 +2031,7 @@ int emu_oracle_sample_pcg64(emu_oracle_t o, const int32_t* q_tt, const int32_t* 
       if (flags & FLAG_BADPOOL) return bad_pool_error(o, s);
       if (!(flags & (FLAG_ARENA | FLAG_HASH)))
         return fail(EMU_ERR_CUDA, "internal error: pool missing after build (flags=" + std::to_string(flags) + ")");
-      chunk = recover(o, flags, n, s, &rc);
+      chunk = recover(o, flags, n, s, &rc, cold0);
       if (rc) return rc;
       if (chunk < 0) return fail(EMU_ERR_CAPACITY, "pool arena too small for a single query's pool");
       continue;
@@ -1874,10 +2120,9 @@ int emu_oracle_sample_host(emu_oracle_t o, const int32_t* q_tt, const int32_t* q
     }
     EMU_CUDA(cudaEventRecord(o->ev_in[i], o->cp_in));
     EMU_CUDA(cudaStreamWaitEvent(s, o->ev_in[i], 0));
-    int rc = build_missing(o, d_qt + a, d_qc + a, d_qp + a, n, s);
-    if (rc) return rc;
-    rc = launch_sample(o, rng_mode, d_qt + a, d_qc + a, d_qp + a, n, ex ? d_us + a : nullptr, ex ? d_ui + a : nullptr,
-                       seed, ctr_base + (uint64_t)a, d_lat + a, d_si + a, s);
+    EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
+    int rc = draw_chunk(o, rng_mode, d_qt + a, d_qc + a, d_qp + a, n, ex ? d_us + a : nullptr, ex ? d_ui + a : nullptr,
+                        seed, ctr_base + (uint64_t)a, d_lat + a, d_si + a, s, false);
     if (rc) return rc;
     EMU_CUDA(cudaMemcpyAsync(o->flag_log + i, &o->ctl->flags, sizeof(int), cudaMemcpyDeviceToDevice, s));
     EMU_CUDA(cudaEventRecord(o->ev_cmp[i], s));
@@ -1916,13 +2161,14 @@ int emu_oracle_prefetch(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_co
   if (!o->has_data) return fail(EMU_ERR_NO_DATA, "profile pack has no samples in any table");
   cudaStream_t s = as_stream(stream);
   for (int attempt = 0; attempt < 16; attempt++) {
+    EMU_CUDA(cudaMemsetAsync(o->ctl, 0, sizeof(BatchCtl), s));
     int rc = build_missing(o, q_tt, q_conc, q_phase, n, s);
     if (rc) return rc;
     int flags = 0;
     if ((rc = read_flags(o, s, &flags))) return rc;
     if (flags & FLAG_BADPOOL) return bad_pool_error(o, s);
     if (!(flags & (FLAG_ARENA | FLAG_HASH))) return EMU_OK;
-    recover(o, flags, n, s, &rc);
+    recover(o, flags, n, s, &rc, true);
     if (rc) return rc;
   }
   return fail(EMU_ERR_CAPACITY, "oracle could not place the pools of the pending keys");
@@ -1943,8 +2189,24 @@ int emu_oracle_get_pcg64(emu_oracle_t o, uint64_t* st6) {
   return EMU_OK;
 }
 
-static constexpr uint64_t kServerIdleNs = 200000;      // exit after 200 us without a step
-static constexpr uint64_t kServerMaxNs = 2000000000ULL;  // and after 2 s in any case
+static constexpr uint64_t kServerMaxNs = 2000000000ULL;  // relaunched at least every 2 s
+// exit after this long without a step (EMU_STEP_SERVER_IDLE_US, default 100 ms:
+// longer than the engine's inter-step sleeps, so cadence calls find it resident)
+static uint64_t server_idle_ns() {
+  static const uint64_t v = [] {
+    const char* e = getenv("EMU_STEP_SERVER_IDLE_US");
+    const long long us = e ? atoll(e) : 100000;
+    return (uint64_t)std::max<long long>(us, 1) * 1000ULL;
+  }();
+  return v;
+}
+
+int emu_oracle_park(emu_oracle_t o) {
+  if (!o) return fail(EMU_ERR_INVALID, "NULL oracle");
+  quiesce_server(o);
+  EMU_CUDA(cudaGetLastError());
+  return EMU_OK;
+}
 
 static int launch_server(emu_oracle_t o) {
   *(volatile int*)o->alive_host = 1;
@@ -1952,7 +2214,7 @@ static int launch_server(emu_oracle_t o) {
   EMU_LAUNCH("step_server", o->srv_stream,
              k_step_server<<<1, 32, 0, o->srv_stream>>>(o->map, o->arena, o->plane[0].samples, o->plane[1].samples,
                                                         o->pcg, o->req_dev, o->step_dev, o->served_dev,
-                                                        o->alive_dev, kServerIdleNs, kServerMaxNs));
+                                                        o->alive_dev, server_idle_ns(), kServerMaxNs));
   EMU_CUDA(cudaGetLastError());
   EMU_CUDA(cudaEventRecord(o->srv_done, o->srv_stream));
   return EMU_OK;
@@ -1970,7 +2232,7 @@ static int step_via_server(emu_oracle_t o, int32_t tt, int32_t conc, int ph, dou
   const uint32_t seq = ++o->step_seq;
   rq->tt = tt;
   rq->conc = conc;
-  rq->phase = ph;
+  rq->phase = ph;  // clears the park bit
   std::atomic_thread_fence(std::memory_order_seq_cst);
   rq->seq = seq;
   std::atomic_thread_fence(std::memory_order_seq_cst);

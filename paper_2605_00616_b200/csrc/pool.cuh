@@ -1269,9 +1269,7 @@ __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, 
         dv.x = (int32_t)o0;
         dv.y = (int32_t)(T.bkt_off[bb + 1] - o0);
       }
-      slots->cdf[j] = cdf;
-      slots->data[j] = dv;
-      if (slots->header && (j % kGroupSlots) == kGroupSlots - 1 && j < K - 1) slots->header[j / kGroupSlots] = cdf;
+      pool_put(*slots, (int32_t)j, cdf, dv);
     }
   }
   G::sync();

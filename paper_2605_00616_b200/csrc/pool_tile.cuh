@@ -482,9 +482,7 @@ __device__ __forceinline__ void tile_finish(const DevTable& T, int K, const Cfg&
       o_cdf[e] = cdf;
     } else {
       const int4 q = tw.u[tw.j[sl * 32 + lane]];
-      pp->cdf[e] = cdf;
-      pp->data[e] = make_int2((int32_t)T.bkt_off[q.w], q.z);
-      if (pp->header && (e % kGroupSlots) == kGroupSlots - 1 && e < K - 1) pp->header[e / kGroupSlots] = cdf;
+      pool_put(*pp, e, cdf, make_int2((int32_t)T.bkt_off[q.w], q.z));
     }
   }
 }

@@ -425,8 +425,7 @@ __device__ __forceinline__ Pcg64 load_pcg(const uint64_t* p) {
 // The oracle draw of a step whose pool entry `e` exists (LatencyOracle._draw,
 // oracle.py:130-135): choice over the pool CDF, then the sample index.
 __device__ __forceinline__ double oracle_draw(const SchedArgs& A, long long e, int ph, Pcg64& g) {
-  const double u = unit_double(pcg64_next64(g));
-  const PoolPick pk = pool_pick<true>(A.arena, e, u);
+  const PoolPick pk = pool_pick<true>(A.arena, e, unit_k53(pcg64_next64(g)));
   uint32_t j = 0;
   if (pk.n > 1) {
     const uint32_t w0 = pcg64_next32(g);

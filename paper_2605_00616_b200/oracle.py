@@ -405,6 +405,12 @@ class LatencyOracle:
         """Drop every cached pool."""
         _check(_lib.lib().emu_oracle_flush(self._h, _lib.stream_ptr()))
 
+    def park(self) -> None:
+        """Stop the resident step server now (it otherwise stays up for
+        EMU_STEP_SERVER_IDLE_US after the last step, so a device-wide
+        synchronize would wait that long); the next step relaunches it."""
+        _check(_lib.lib().emu_oracle_park(self._h))
+
     def cached_slots(self) -> int:
         n_pools, n_slots = ctypes.c_int64(), ctypes.c_int64()
         _check(_lib.lib().emu_oracle_stats(self._h, ctypes.byref(n_pools), ctypes.byref(n_slots)))

@@ -241,6 +241,33 @@ def test_batched_modes_match_oracle(c1_pack, mode):
     assert np.array_equal(sidx_h, sidx_o)
 
 
+@pytest.mark.parametrize("mode", ["explicit", "philox"])
+def test_sweep_paths_match_oracle(c1_pack, mode):
+    """Every cache state a batch can meet: cold (k_mark + k_sample head, k_sweep
+    tail with its miss list), partly warm (k_sweep: hits drawn in the pass,
+    misses built then drawn by k_sample_list) and fully warm (one k_sweep)."""
+    tabs = to_oracle_tables(c1_pack)
+    qt, qc, qp = queries_llama(300_000, 41)
+    us, ui = explicit_uniforms(len(qt), 42)
+    orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32))
+    for a, b in ((0, 40_000), (0, 300_000), (0, 300_000), (150_000, 300_000)):
+        lat, sidx = orc.sample_batch(dev(qt[a:b]), dev(qc[a:b]), dev(qp[a:b]), rng=mode,
+                                     u_sel=dev(us[a:b].view(np.int64)), u_idx=dev(ui[a:b].view(np.int32)),
+                                     seed=3, ctr_base=a)
+        lat_o, sidx_o = O.sample_batch(tabs, qt[a:b], qc[a:b], qp[a:b], 32, mode=mode, u_sel=us[a:b],
+                                       u_idx=ui[a:b], seed=3, ctr_base=a, threads=8)
+        assert np.array_equal(sidx.cpu().numpy(), sidx_o), (a, b)
+        assert np.array_equal(lat.cpu().numpy(), lat_o), (a, b)
+    # out-of-domain keys (hash map) arriving on a warm cache
+    qt2 = qt[:20_000].copy()
+    qt2[::7] += 5000
+    lat, sidx = orc.sample_batch(dev(qt2), dev(qc[:20_000]), dev(qp[:20_000]), rng=mode,
+                                 u_sel=dev(us[:20_000].view(np.int64)), u_idx=dev(ui[:20_000].view(np.int32)), seed=3)
+    lat_o, sidx_o = O.sample_batch(tabs, qt2, qc[:20_000], qp[:20_000], 32, mode=mode, u_sel=us[:20_000],
+                                   u_idx=ui[:20_000], seed=3, threads=8)
+    assert np.array_equal(sidx.cpu().numpy(), sidx_o)
+
+
 def test_rejection_words_explicit_mode():
     """Force Lemire rejections: a bucket with n = 3*2^30 is impossible, so use
     words that land below the threshold for a small n and compare to the oracle."""
@@ -335,8 +362,13 @@ def test_step_server_matches_launch_path(c1_pack, c1_trace, monkeypatch):
     for server in ("1", "0"):
         monkeypatch.setenv("EMU_STEP_SERVER", server)
         orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32, rng_seed=5))
-        out = [orc(*k) for k in keys[:200]]
-        _time.sleep(0.002)  # > idle timeout: the server exits, the next call relaunches it
+        out = [orc(*k) for k in keys[:100]]
+        _time.sleep(0.15)  # > idle timeout (100 ms): the server exits, the next call relaunches it
+        out += [orc(*k) for k in keys[100:150]]
+        _time.sleep(0.005)  # engine-cadence gap: the server stays resident
+        out += [orc(*k) for k in keys[150:200]]
+        orc.park()  # exits on its next poll; the next call relaunches it
+        torch.cuda.synchronize()
         out += [orc(*k) for k in keys[200:300]]
         orc.flush()
         out += [orc(*k) for k in keys[300:400]]

@@ -20,5 +20,7 @@ us = torch.as_tensor(us.view(np.int64), device="cuda"); ui = torch.as_tensor(ui.
 for _ in range(sweeps):
     orc.flush()
     lat, sidx = orc.sample_batch(qt, qc, qp, rng=rng, u_sel=us, u_idx=ui, seed=1)
+for _ in range(int(os.environ.get("WARM", 0))):  # warm sweeps (no flush): one k_sweep pass each
+    lat, sidx = orc.sample_batch(qt, qc, qp, rng=rng, u_sel=us, u_idx=ui, seed=1)
 torch.cuda.synchronize()
 print("slots used", orc.cached_slots())
