@@ -136,7 +136,8 @@ def c3(args):
         ms = timed(sweep, max(1, args.steps // 2), warmup=1)
         _lib.profile_enable(True)
         sweep()
-        kern = {k: round(_lib.profile_read(k)[0], 4) for k in ("mark", "pool_prep", "pool_warp", "pool_grp", "pool_cta", "sample")}
+        kern = {k: round(_lib.profile_read(k)[0], 4) for k in ("mark", "pool_prep", "tile_bin", "scan", "tile_scatter",
+                                                                "pool_tile", "pool_warp", "pool_grp", "pool_cta", "sample")}
         _lib.profile_enable(False)
         n = 2_000
         t0 = time.perf_counter()

@@ -204,10 +204,10 @@ __device__ void emit_pool(const DevTable& T, int64_t w, int64_t K, int64_t entry
 // for this workspace.
 template <int NT, int MODE>
 __device__ bool process_key(const DevTable& T, int64_t w, int ph, int32_t t, int32_t c, int64_t entry_idx,
-                            const Cfg& cfg, const PoolWS& ws, const Sink& sk) {
+                            const Cfg& cfg, const PoolWS& ws, const Sink& sk, const KeyWin* kwin = nullptr) {
   int64_t soff = 0;
   bool cached = false;
-  const int64_t K = pool_search<NT>(T, t, c, cfg.floor, ws, soff, cached);
+  const int64_t K = pool_search<NT>(T, t, c, cfg.floor, ws, soff, cached, kwin);
   if (K < 0) return false;
   emit_pool<NT, MODE>(T, w, K, entry_idx, soff, cached, -1, cfg, ws, sk, ph, t, c);
   return true;
@@ -233,7 +233,8 @@ __device__ __forceinline__ long long warp_alloc(unsigned long long* counter, lon
 // pool's arena reservation min(floor, window buckets), one atomic per warp.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk, KeyWin* kw,
-                                                   long long* resv) {
+                                                   long long* resv, int* esc_list, int* esc_count, int* wl,
+                                                   int* wl_n) {
   const int64_t n = keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
@@ -243,11 +244,14 @@ __global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Key
     k.flags = 0;
     k.cap = 0;
     bool ready = false;
+    bool win = false;
     if (valid) {
       const DevTable& T = keys.ph[w] ? P1 : P0;
-      ready = key_window(T, keys.tt[w], keys.conc[w], cfg.floor, k) && k.cap <= kWarpCap;
+      win = key_window(T, keys.tt[w], keys.conc[w], cfg.floor, k);
+      ready = win && k.cap <= kWarpCap;
     }
-    if (!ready) k.flags = 0;
+    // too big for a warp: keep the window for the group tier (kWinBig), no reservation
+    if (!ready) k.flags = win ? ((k.flags & ~kWinReady) | kWinBig) : 0;
     long long r = -1;
     if (MODE == 0) {
       const long long need = ready ? pool_total_slots(k.cap < cfg.floor ? k.cap : cfg.floor) : 0;
@@ -261,6 +265,11 @@ __global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Key
       kw[w] = k;
       resv[w] = r;
     }
+    // windows too big for a warp go straight onto the group tier's list; without
+    // the tile tier the others form the warp tier's list (wl)
+    const bool big = valid && (k.flags & kWinBig);
+    warp_push(esc_list, esc_count, big, (int)w);
+    if (wl) warp_push(wl, wl_n, valid && !big, (int)w);
   }
 }
 
@@ -385,6 +394,7 @@ __global__ void __launch_bounds__(kWarpThreads, EMU_WARP_MINB) k_pool_warp(DevTa
       }
       __syncwarp();
     }
+    if (k.flags & kWinBig) continue;  // k_pool_prep put it on the group tier's list
     const bool ok = process_key<32, MODE>(T, wk, mixed ? 1 : 0, keys.tt[wk], keys.conc[wk], ent, cfg, ws, sk);
     if (!ok && lane == 0) {
       int e = atomicAdd(esc_count, 1);
@@ -496,7 +506,8 @@ __global__ void __launch_bounds__(kTileThreads, EMU_TILE_MINB)
 // still overflow go on to the CTA tier.
 template <int MODE>
 __global__ void __launch_bounds__(kGrpThreads, EMU_GRP_MINB) k_pool_grp(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk,
-                                                          int* work, const int* esc_list, const int* esc_count,
+                                                          const KeyWin* __restrict__ kw, int* work,
+                                                          const int* esc_list, const int* esc_count,
                                                           int* esc2_list, int* esc2_count) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ long long scr[40];
@@ -516,7 +527,9 @@ __global__ void __launch_bounds__(kGrpThreads, EMU_GRP_MINB) k_pool_grp(DevTable
     const int w = esc_list[i];
     const DevTable& T = keys.ph[w] ? P1 : P0;
     const int64_t ent = keys.entry ? keys.entry[w] : 0;
-    const bool ok = process_key<kGrpThreads, MODE>(T, w, keys.ph[w] ? 1 : 0, keys.tt[w], keys.conc[w], ent, cfg, ws, sk);
+    const KeyWin k = kw[w];
+    const bool ok = process_key<kGrpThreads, MODE>(T, w, keys.ph[w] ? 1 : 0, keys.tt[w], keys.conc[w], ent, cfg, ws,
+                                                   sk, (k.flags & kWinBig) ? &k : nullptr);
     if (!ok && threadIdx.x == 0) esc2_list[atomicAdd(esc2_count, 1)] = w;
   }
 }
@@ -1658,12 +1671,13 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
     return EMU_OK;
   };
   int rc;
-  EMU_LAUNCH("pool_prep", s, k_pool_prep<MODE><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, sk,
-                                                                          o->kw, o->resv));
+  EMU_LAUNCH("pool_prep", s, k_pool_prep<MODE><<<kPrepGrid, 256, 0, s>>>(
+                                 o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, o->esc,
+                                 &o->ctl->esc_count, o->tile_on ? nullptr : o->fb_list, &o->ctl->fb_n));
   if ((rc = chk("pool_prep"))) return rc;
-  const int* list = nullptr;
-  const int* list_n = nullptr;
-  int* warp_work = &o->ctl->work;
+  const int* list = o->fb_list;  // the warp tier's keys: from prep, or handed over by the tile tier
+  const int* list_n = &o->ctl->fb_n;
+  int* warp_work = &o->ctl->fb_work;
   if (o->tile_on) {
     EMU_CUDA(cudaMemsetAsync(o->tile_cnt, 0, sizeof(int) * o->ti.nb, s));
     EMU_LAUNCH("tile_bin", s, k_tile_bin<MODE><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, o->ti,
@@ -1692,16 +1706,13 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
                                    o->plane[0], o->plane[1], keys, o->cfg, sk, o->ti, o->kw, o->resv, o->order,
                                    o->tile_off, &o->ctl->tile_total, &o->ctl->tile_work, o->fb_list, &o->ctl->fb_n));
     if ((rc = chk("pool_tile"))) return rc;
-    list = o->fb_list;
-    list_n = &o->ctl->fb_n;
-    warp_work = &o->ctl->fb_work;
   }
   EMU_LAUNCH("pool_warp", s, k_pool_warp<MODE><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
                                  o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, warp_work, o->esc,
                                  &o->ctl->esc_count, list, list_n));
   if ((rc = chk("pool_warp"))) return rc;
   EMU_LAUNCH("pool_grp", s, k_pool_grp<MODE><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(o->plane[0], o->plane[1], keys,
-                                                                                     o->cfg, sk, &o->ctl->esc_work,
+                                                                                     o->cfg, sk, o->kw, &o->ctl->esc_work,
                                                                                      o->esc, &o->ctl->esc_count, o->esc2,
                                                                                      &o->ctl->esc2_count));
   if ((rc = chk("pool_grp"))) return rc;

@@ -386,6 +386,18 @@ __device__ __forceinline__ int sat_rect(const int32_t* __restrict__ S, int32_t s
   return S[r1 + w.j1 + 1] - S[r0 + w.j1 + 1] - S[r1 + w.j0] + S[r0 + w.j0];
 }
 
+// Column j's slice [lo, lo + cnt) of the column index (buckets ordered by
+// (conc, tt)) over grid rows [i0, i1], from the bucket SAT: four loads instead
+// of two binary searches over the column (rows [0, i) hold S[i][j+1] - S[i][j]).
+__device__ __forceinline__ void col_range(const DevTable& T, int32_t i0, int32_t i1, int32_t j, int32_t& lo,
+                                          int32_t& cnt) {
+  const int32_t st = (int32_t)T.gnc + 1;
+  const int32_t a = i0 * st + j, b = (i1 + 1) * st + j;
+  const int32_t before = T.bsat[a + 1] - T.bsat[a];
+  lo = T.col_start[j] + before;
+  cnt = T.bsat[b + 1] - T.bsat[b] - before;
+}
+
 // 2^((l - 8) / 4): the radius grid of the SAT probe.
 __constant__ double kRadiusStep[32] = {
     0.25, 0.29730177875068026, 0.3535533905932738, 0.42044820762685725, 0.5, 0.5946035575013605,
@@ -531,6 +543,96 @@ __device__ __forceinline__ bool grp_sort_runs(const PoolWS& ws, int64_t pos) {
   return true;
 }
 
+// Multi-warp groups, up to 4 candidates per thread: bucket sort by d^2 (1024
+// bins over [0, max d^2]: monotone in d, so bins are in distance order), then
+// each bin's few entries ordered by (d, bucket) in place.  Elements travel in
+// registers, bin counts live in the ncache arrays (free until prefix_k).  Four
+// barriers and O(pos) work instead of sorting networks; returns false (caller
+// sorts otherwise) when it does not apply.
+template <int NT>
+__device__ __forceinline__ bool grp_bucket_sort(const PoolWS& ws, int64_t pos) {
+  constexpr int E = 4, NB = 1024;
+  using G = Grp<NT>;
+  if (NT <= 32 || pos > (int64_t)E * NT || 2 * ws.ncache < NB + NB / 32) return false;
+  const int r = G::rank(), lane = r & 31;
+  int* cnt = ws.n;  // NB + NB/32 ints, skewed (ws.o follows: 2 * ncache ints in all)
+  auto at = [](int b) { return b + (b >> 5); };  // bin b's slot: conflict-free per-thread runs
+  double d[E];
+  int32_t b[E];
+  double mx = 0.0;
+#pragma unroll
+  for (int q = 0; q < E; q++) {
+    const int i = q * NT + r;
+    d[q] = 0.0;
+    b[q] = 0;
+    if (i < pos) {
+      d[q] = ws.d[i];
+      b[q] = ws.b[i];
+      mx = fmax(mx, d[q]);
+    }
+  }
+  for (int i = r; i < NB + NB / 32; i += NT) cnt[i] = 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  if (lane == 0) ws.dsh[r >> 5] = mx;
+  G::sync();
+  mx = ws.dsh[0];
+#pragma unroll
+  for (int q = 1; q < NT / 32; q++) mx = fmax(mx, ws.dsh[q]);
+  const double sc = mx > 0.0 && mx < 1e300 ? (double)NB / __dmul_rn(mx, mx) : 0.0;
+  int bin[E], rk[E];
+#pragma unroll
+  for (int q = 0; q < E; q++) {
+    bin[q] = -1;
+    if (q * NT + r < pos) {
+      const double v = __dmul_rn(__dmul_rn(d[q], d[q]), sc);
+      bin[q] = v < (double)(NB - 1) ? (int)v : NB - 1;
+      rk[q] = atomicAdd(&cnt[at(bin[q])], 1);
+    }
+  }
+  G::sync();
+  // exclusive scan of the bin counts: NB / NT consecutive bins per thread
+  constexpr int PER = NB / NT;
+  int loc[PER];
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    loc[k] = sum;
+    sum += cnt[at(r * PER + k)];
+  }
+  long long tot;
+  const int ex = (int)G::excl_scan(sum, tot, ws.scr);
+#pragma unroll
+  for (int k = 0; k < PER; k++) cnt[at(r * PER + k)] = ex + loc[k];
+  G::sync();
+#pragma unroll
+  for (int q = 0; q < E; q++)
+    if (bin[q] >= 0) {
+      const int p = cnt[at(bin[q])] + rk[q];
+      ws.d[p] = d[q];
+      ws.b[p] = b[q];
+    }
+  G::sync();
+  // entries sharing a bin: insertion sort by (d, bucket)
+  for (int bn = r; bn < NB; bn += NT) {
+    const int s0 = cnt[at(bn)], s1 = bn + 1 < NB ? cnt[at(bn + 1)] : (int)pos;
+    for (int x = s0 + 1; x < s1; x++) {
+      const double dx = ws.d[x];
+      const int32_t bx = ws.b[x];
+      int y = x;
+      while (y > s0 && cand_less(dx, bx, ws.d[y - 1], ws.b[y - 1])) {
+        ws.d[y] = ws.d[y - 1];
+        ws.b[y] = ws.b[y - 1];
+        y--;
+      }
+      ws.d[y] = dx;
+      ws.b[y] = bx;
+    }
+  }
+  G::sync();
+  return true;
+}
+
 // Shortest prefix of the sorted candidates (sd, sb)[0..C) reaching the floor,
 // or -1 if the C candidates hold fewer than mfloor samples.  Caches each
 // scanned candidate's sample count / first sample in ws.n / ws.o.
@@ -602,20 +704,50 @@ __device__ __forceinline__ void append_cand(bool in, double d, int32_t bb, const
   }
 }
 
+// Precomputed search window of one key (k_pool_prep, thread per key).
+struct KeyWin {
+  int64_t Wt, Wc;          // r2 window half-widths (kInfW = unbounded)
+  double dmax;             // candidates farther than this cannot be pooled
+  int32_t i0, i1, j0, j1;  // r2 window in grid coordinates
+  int32_t off, cap;        // candidate scratch slice [off, off + cap)
+  int32_t pos;             // candidates written (<= cap)
+  int32_t flags;           // kWinReady | kWinCovT | kWinCovC
+};
+// kWinBig: the window was computed but holds more than a warp workspace (the
+// group tier takes it as is, without its own radius search).
+constexpr int32_t kWinReady = 1, kWinCovT = 2, kWinCovC = 4, kWinBig = 8;
+
 template <int NT>
 __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws,
-                                   int64_t& sorted_off) {
+                                   int64_t& sorted_off, const KeyWin* kwin = nullptr) {
   using G = Grp<NT>;
   EMU_PHASE_BEGIN();
   const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
   const int32_t st = (int32_t)T.gnc + 1;
+  Win w;
+  double r1, dmax;
+  int C;
+  if (kwin) {  // the window k_pool_prep found (same rules: r1 search on the SAT, r2 = sqrt(2) r1)
+    w.Wt = kwin->Wt;
+    w.Wc = kwin->Wc;
+    w.i0 = kwin->i0;
+    w.i1 = kwin->i1;
+    w.j0 = kwin->j0;
+    w.j1 = kwin->j1;
+    w.cov_t = kwin->flags & kWinCovT;
+    w.cov_c = kwin->flags & kWinCovC;
+    dmax = kwin->dmax;
+    r1 = dmax < 1e300 ? dmax / (1.4142135623730951 * (1.0 + 1e-9) * (1.0 + 1e-9)) : dmax;
+    C = kwin->cap;
+  } else {
   double gtd = 0.0, gcd = 0.0;
   if (span_t) gtd = (double)max(max((int64_t)T.tt_lo - t, (int64_t)t - T.tt_hi), (int64_t)0) / (double)span_t;
   if (span_c) gcd = (double)max(max((int64_t)T.c_lo - c, (int64_t)c - T.c_hi), (int64_t)0) / (double)span_c;
   const double rb = fmax(gtd, gcd);
   const double r0 = initial_radius(T, mfloor);
   // ---- 1. radius search
-  double r1 = -1.0, rmiss = -1.0;
+  double rmiss = -1.0;
+  r1 = -1.0;
   double scale = 1.0;
   for (int round = 0; round < 10 && r1 < 0.0; round++, scale *= 256.0) {
     bool ok = true;
@@ -672,11 +804,12 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
   EMU_PHASE(1);
   // ---- 2. the guaranteed window; pool members lie within dmax of the query
   const double r2 = r1 * 1.4142135623730951 * (1.0 + 1e-9);
-  const Win w = make_win(T, t, c, radius_to_w(r2, span_t), radius_to_w(r2, span_c));
+  w = make_win(T, t, c, radius_to_w(r2, span_t), radius_to_w(r2, span_c));
   const Win w1 = make_win(T, t, c, radius_to_w(r1, span_t), radius_to_w(r1, span_c));
   const bool exhaust = w1.cov_t && w1.cov_c && sat_rect(T.ssat, st, w1) < mfloor;
-  const double dmax = exhaust ? __longlong_as_double(0x7ff0000000000000LL) : r2 * (1.0 + 1e-9);
-  const int C = sat_rect(T.bsat, st, w);
+  dmax = exhaust ? __longlong_as_double(0x7ff0000000000000LL) : r2 * (1.0 + 1e-9);
+  C = sat_rect(T.bsat, st, w);
+  }
   EMU_STAT(8, C);
   EMU_PHASE(2);
   if (C > ws.cap) return -1;
@@ -696,9 +829,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
       const int r = G::rank();
       int32_t lo = 0, cnt = 0;
       if (r < ncj) {
-        const int32_t s0 = T.col_start[w.j0 + r], s1 = T.col_start[w.j0 + r + 1];
-        lo = (int32_t)lower_bound_i32(T.col_tt, s0, s1, tlo);
-        cnt = (int32_t)upper_bound_i32(T.col_tt, lo, s1, thi) - lo;
+        col_range(T, w.i0, w.i1, w.j0 + r, lo, cnt);
       }
       long long tot;
       const int ex = (int)G::excl_scan(cnt, tot, ws.scr);
@@ -861,7 +992,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
       warp_sort_ws<2>(ws, pos);
     else
       warp_sort_ws<4>(ws, pos);
-  } else if (!grp_sort_runs<NT>(ws, pos)) {
+  } else if (!grp_bucket_sort<NT>(ws, pos) && !grp_sort_runs<NT>(ws, pos)) {
     int64_t P = 1;
     while (P < pos) P <<= 1;
     for (int64_t i = pos + G::rank(); i < P; i += NT) {
@@ -897,15 +1028,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
 // The scalar parts of the SAT search run one key per THREAD (k_pool_win /
 // k_pool_enum); the warp kernel then only sorts, takes the prefix and builds
 // the CDF.  Same window rules as pool_search_sat (see its comment).
-struct KeyWin {
-  int64_t Wt, Wc;          // r2 window half-widths (kInfW = unbounded)
-  double dmax;             // candidates farther than this cannot be pooled
-  int32_t i0, i1, j0, j1;  // r2 window in grid coordinates
-  int32_t off, cap;        // candidate scratch slice [off, off + cap)
-  int32_t pos;             // candidates written (<= cap)
-  int32_t flags;           // kWinReady | kWinCovT | kWinCovC
-};
-constexpr int32_t kWinReady = 1, kWinCovT = 2, kWinCovC = 4;
+
 
 __device__ __forceinline__ bool win_ok(const DevTable& T, int32_t t, int32_t c, double r, int64_t span_t,
                                        int64_t span_c, int32_t st, int64_t mfloor) {
@@ -937,7 +1060,13 @@ __device__ bool key_window(const DevTable& T, int32_t t, int32_t c, int64_t mflo
       hi = rb + step;
       if (++guard > 200) return false;
     }
-    for (int it = 0; it < 12; it++) {
+    // Bisection until the windows of lo (too small) and hi (enough samples)
+    // differ by one step of one axis: hi's window is then the minimal one, and
+    // r1 = the smallest radius that still yields it (its breakpoint).
+    for (int it = 0; it < 40; it++) {
+      const int64_t dwt = radius_to_w(hi, span_t) - radius_to_w(lo, span_t);
+      const int64_t dwc = radius_to_w(hi, span_c) - radius_to_w(lo, span_c);
+      if ((span_t ? dwt : 0) + (span_c ? dwc : 0) <= 1) break;
       const double mid = 0.5 * (lo + hi);
       if (win_ok(T, t, c, mid, span_t, span_c, st, mfloor))
         hi = mid;
@@ -945,6 +1074,17 @@ __device__ bool key_window(const DevTable& T, int32_t t, int32_t c, int64_t mflo
         lo = mid;
     }
     r1 = hi;
+    {
+      const int64_t wt = radius_to_w(hi, span_t), wc = radius_to_w(hi, span_c);
+      double rb2 = 0.0;
+      if (span_t) rb2 = fmax(rb2, (double)wt / (double)span_t);
+      if (span_c) rb2 = fmax(rb2, (double)wc / (double)span_c);
+      for (int k = 0; k < 4 && rb2 < hi; k++, rb2 = nextafter(rb2, 1e300))
+        if (radius_to_w(rb2, span_t) == wt && radius_to_w(rb2, span_c) == wc) {
+          r1 = fmax(rb2, rb);
+          break;
+        }
+    }
   }
   const double r2 = r1 * 1.4142135623730951 * (1.0 + 1e-9);
   const Win w = make_win(T, t, c, radius_to_w(r2, span_t), radius_to_w(r2, span_c));
@@ -985,9 +1125,7 @@ __device__ int warp_enumerate(const DevTable& T, int32_t t, int32_t c, const Key
       const int32_t j = cbase + lane;
       int32_t lo = 0, cnt = 0;
       if (j <= kw.j1) {
-        const int32_t s0 = T.col_start[j], s1 = T.col_start[j + 1];
-        lo = (int32_t)lower_bound_i32(T.col_tt, s0, s1, tlo);
-        cnt = (int32_t)upper_bound_i32(T.col_tt, lo, s1, thi) - lo;
+        col_range(T, kw.i0, kw.i1, j, lo, cnt);
       }
       int x = cnt;
 #pragma unroll
@@ -1177,11 +1315,11 @@ __device__ int64_t pool_from_window(const DevTable& T, int32_t t, int32_t c, int
 // is at ws.d/ws.b + sorted_off.
 template <int NT>
 __device__ int64_t pool_search(const DevTable& T, int32_t t, int32_t c, int64_t mfloor, const PoolWS& ws,
-                               int64_t& sorted_off, bool& cached) {
+                               int64_t& sorted_off, bool& cached, const KeyWin* kwin = nullptr) {
   sorted_off = 0;
   cached = true;
   if (T.gnt > 0) {
-    const int64_t K = pool_search_sat<NT>(T, t, c, mfloor, ws, sorted_off);
+    const int64_t K = pool_search_sat<NT>(T, t, c, mfloor, ws, sorted_off, kwin);
     if (K != -2) return K;
     Grp<NT>::sync();
     sorted_off = 0;
@@ -1235,6 +1373,36 @@ __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, 
       }
       ws.dsh[0] = res;
     }
+  } else if (NT >= 128 && K <= 256) {
+    // numpy's recursion for 128 < K <= 256: A = [0, n2), n2 = K/2 - (K/2)%8, and
+    // B = [n2, K), itself split the same way when longer than 128.  Each leaf
+    // (<= 128) is one warp's 8-accumulator block; S = A + B (or A + (B1 + B2)).
+    double* part = reinterpret_cast<double*>(ws.scr);  // 3 leaves x 8 partial accumulators
+    const int64_t n2 = (K / 2) - (K / 2) % 8, m = K - n2;
+    const int64_t m2 = m > 128 ? (m / 2) - (m / 2) % 8 : m;
+    const int64_t lb3[3] = {0, n2, n2 + m2}, ln3[3] = {n2, m2, m - m2};
+    const int nleaf = m > 128 ? 3 : 2;
+    const int g = G::rank() >> 5, q = G::rank() & 31;
+    if (g < nleaf && q < 8) {
+      const int64_t lb = lb3[g], ln = ln3[g];
+      const int64_t body = ln - (ln % 8);
+      double r = ws.d[lb + q];
+      for (int64_t i = 8 + q; i < body; i += 8) r = __dadd_rn(r, ws.d[lb + i]);
+      part[g * 8 + q] = r;
+    }
+    G::sync();
+    if (G::rank() == 0) {
+      double leaf[3];
+      for (int h = 0; h < nleaf; h++) {
+        const double* r = part + h * 8;
+        const int64_t lb = lb3[h], ln = ln3[h];
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (int64_t i = ln - (ln % 8); i < ln; i++) res = __dadd_rn(res, ws.d[lb + i]);
+        leaf[h] = res;
+      }
+      ws.dsh[0] = __dadd_rn(leaf[0], nleaf == 3 ? __dadd_rn(leaf[1], leaf[2]) : leaf[1]);
+    }
   } else if (G::rank() == 0) {
     ws.dsh[0] = pairwise_sum(ws.d, K);
   }
@@ -1246,9 +1414,20 @@ __device__ void pool_finish(const DevTable& T, int64_t K, double p, double eps, 
     if (o_prob) o_prob[j] = pr;
   }
   G::sync();
-  if (G::rank() == 0) {  // np.cumsum: strictly sequential
+  if (G::rank() == 0) {  // np.cumsum: strictly sequential (loads hoisted 8 at a time)
     double acc = ws.d[0];
-    for (int64_t j = 1; j < K; j++) {
+    int64_t j = 1;
+    for (; j + 8 <= K; j += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) v[q] = ws.d[j + q];
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        acc = __dadd_rn(acc, v[q]);
+        ws.d[j + q] = acc;
+      }
+    }
+    for (; j < K; j++) {
       acc = __dadd_rn(acc, ws.d[j]);
       ws.d[j] = acc;
     }

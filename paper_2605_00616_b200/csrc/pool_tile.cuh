@@ -33,7 +33,10 @@
 namespace emu {
 
 constexpr int kTileU = 256;       // union candidates per tile
-constexpr int kTileL = 36;        // exact candidates per key (after the pivot)
+#ifndef EMU_TILE_L
+#define EMU_TILE_L 36
+#endif
+constexpr int kTileL = EMU_TILE_L;  // exact candidates per key (after the pivot)
 constexpr int kTileWarps = 2;
 constexpr int kTileThreads = 32 * kTileWarps;
 constexpr int kTileRowShift = 4;  // ordering bins: 16 grid rows of one conc column
@@ -48,7 +51,7 @@ struct TileWarp {
   double d[kTileL * 32];      // per-lane list, entry e of lane l at [e * 32 + l] (staging for the union sort)
   uint8_t j[kTileL * 32];     // union index of that entry (= bucket order: ties in d break on it)
   uint8_t perm[kTileL * 32];  // sorted order: the e-th smallest entry of lane l is perm[e * 32 + l]
-  uint16_t h[32 * 32];        // per lane: pivot histogram (16 bins), then distance-bin counts (32 bins)
+  uint8_t h[32 * 32];         // per lane: distance-bin counts (32 bins, <= kTileL each), then bin starts
 };
 static_assert(kTileL * 32 * 8 >= kTileU * 16, "the union staging area lives in TileWarp::d");
 constexpr int kTileBytes = (int)sizeof(TileWarp) * kTileWarps;
@@ -95,6 +98,7 @@ __global__ void __launch_bounds__(256) k_tile_bin(DevTable P0, DevTable P1, Keys
       bin = (MODE == 0 && resv[w] == -2) ? -2 : tile_bin(ph ? P1 : P0, ti, ph, keys.tt[w], keys.conc[w], k, cfg.floor);
       if (bin >= 0) krank[w] = atomicAdd(&cnt[bin], 1);
       kbin[w] = (int)bin;
+      if (k.flags & kWinBig) bin = -4;  // already on the group tier's list (k_pool_prep)
     }
     warp_push(fb_list, fb_n, bin == -1, (int)w);
   }
@@ -196,9 +200,7 @@ __device__ __forceinline__ int tile_enum_union(const DevTable& T, int32_t i0, in
   const int32_t j = j0 + lane;
   int32_t lo = 0, cnt = 0;
   if (j <= j1) {
-    const int32_t s0 = T.col_start[j], s1 = T.col_start[j + 1];
-    lo = (int32_t)lower_bound_i32(T.col_tt, s0, s1, tlo);
-    cnt = (int32_t)upper_bound_i32(T.col_tt, lo, s1, thi) - lo;
+    col_range(T, i0, i1, j, lo, cnt);
   }
   int x = cnt;
 #pragma unroll
@@ -268,7 +270,7 @@ __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t
   const int32_t Wt = (int32_t)min(k.Wt, (int64_t)0x3fffffff), Wc = (int32_t)min(k.Wc, (int64_t)0x3fffffff);
   const bool exhaust = !(k.dmax < 1e300);
   const float dmax2 = exhaust ? 3.0e38f : (float)(k.dmax * k.dmax) * (1.0f + 4e-5f);
-  uint16_t* h = tw.h + lane;  // lane-strided
+  uint8_t* h = tw.h + lane;  // lane-strided
   // ---- 1. membership bitmask: own window and float distance <= dmax (uniform loop over the union)
   uint32_t mask[kTileU / 32];
 #pragma unroll
@@ -384,14 +386,14 @@ __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t
 #pragma unroll
     for (int l = 0; l < 32; l++) {
       const int cnt = h[l * 32];
-      h[l * 32] = (uint16_t)st;
+      h[l * 32] = (uint8_t)st;
       st += cnt;
     }
   }
   for (int e = 0; e < m; e++) {
     const int bn = min(31, (int)(tw.d[e * 32 + lane] * scale));
     const int p = h[bn * 32];
-    h[bn * 32] = (uint16_t)(p + 1);
+    h[bn * 32] = (uint8_t)(p + 1);
     tw.perm[p * 32 + lane] = (uint8_t)e;
   }
   for (int p = 1; p < m; p++) {

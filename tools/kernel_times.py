@@ -33,7 +33,8 @@ for _ in range(sweeps):
 e1.record()
 torch.cuda.synchronize()
 out = {"step_ms": e0.elapsed_time(e1) / sweeps}
-for k in ("flush", "mark", "pool_prep", "pool_warp", "pool_grp", "pool_cta", "sample"):
+for k in ("flush", "mark", "pool_prep", "tile_bin", "scan", "tile_scatter", "pool_tile", "pool_warp", "pool_grp",
+          "pool_cta", "sample", "sweep", "sample_list"):
     ms, n = _lib.profile_read(k)
     out[k] = round(ms / max(n, 1), 4)
 print(os.environ.get("TAG", ""), out, flush=True)
