@@ -238,10 +238,9 @@ def c4(args):
     _lib.profile_enable(True)
     t = DeviceTables.build(*dev, canonical=True)
     nb = sum(t.info(i)["n_buckets"] for i in range(3))
-    sc_ms, passes = _lib.profile_read("radix_scatter")
-    up_ms, _ = _lib.profile_read("radix_up")
-    scan_ms, _ = _lib.profile_read("scan")
+    kern = _lib.profile_all()
     _lib.profile_enable(False)
+    sc_ms, passes = kern.get("onesweep", (0.0, 0))
     del t
     algo_bytes = 33 * n + 48 * nb / 3
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
@@ -256,9 +255,10 @@ def c4(args):
                          "frac": algo_bytes / (ms / 1e3) / 1e9 / peak,
                          "bytes": "33 B/record + 48 B/bucket (SURVEY 8d); multi-pass sort moves more"},
             "device_generation_s": gen_s,
-            "radix_sort": {"passes": passes, "scatter_ms": sc_ms, "upsweep_ms": up_ms, "scan_ms": scan_ms,
-                           "scatter_GBps": 40 * n * passes / (sc_ms / 1e3) / 1e9,
-                           "note": "each pass reads key 8 B + (hi, lo) 16 B and writes 16 B per record"},
+            "radix_sort": {"passes": passes, "onesweep_ms": sc_ms,
+                           "pass_GBps": 24 * n * passes / (sc_ms / 1e3) / 1e9 if sc_ms else None,
+                           "note": "onesweep LSD: each pass reads (hi u32, lo u64) 12 B and writes 12 B per record"},
+            "kernels_ms": {k: [round(v[0], 3), v[1]] for k, v in sorted(kern.items(), key=lambda kv: -kv[1][0])},
             "cpu_baseline": {"value": cpu, "unit": "records/s", "cores": 1, "kind": "port",
                              "sample": f"oracle qsort build of the first {m} records"}}
 

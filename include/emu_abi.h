@@ -110,6 +110,10 @@ int emu_tables_create(const emu_table_view* decode, const emu_table_view* mixed,
 int emu_tables_build(const int32_t* tt, const int32_t* conc, const uint8_t* phase,
                      const double* lat, const int64_t* step, int64_t n, int canonical,
                      void* stream, emu_tables_t* out, int64_t* bad_index, int32_t* bad_code);
+/* Builds run one at a time per process and bump-allocate their scratch (key
+ * and sort buffers) from one persistent device buffer sized to the largest
+ * build so far; this frees it. */
+int emu_build_scratch_release(void);
 
 int emu_tables_info(emu_tables_t t, int table_id, emu_table_info* out);
 /* Device views of the handle-owned arrays (for copies out / NCCL broadcast). */
@@ -324,6 +328,8 @@ int emu_trace_parse_jsonl(const char* text, int64_t len, int n_threads, int64_t 
  * pending event pairs of `kernel` (e.g. "sample", "pool_warp", "mark") into
  * (*total_ms, *launches) and resets that kernel's accumulator. */
 int64_t emu_launch_count(void);
+/* Newline-separated names of the kernels with recorded launches (truncated to cap - 1 bytes). */
+int emu_profile_names(char* buf, int64_t cap);
 int emu_profile_enable(int on);
 int emu_profile_read(const char* kernel, double* total_ms, int64_t* launches);
 

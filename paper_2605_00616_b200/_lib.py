@@ -88,6 +88,8 @@ SIGNATURES = {
     "emu_launch_count": (c_i64, []),
     "emu_profile_enable": (c_int, [c_int]),
     "emu_profile_read": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
+    "emu_profile_names": (c_int, [ctypes.c_char_p, c_i64]),
+    "emu_build_scratch_release": (c_int, []),
     "emu_last_error": (ctypes.c_char_p, []),
     "emu_version": (c_int, []),
 }
@@ -194,3 +196,10 @@ def profile_read(kernel: str) -> tuple[float, int]:
     ms, n = ctypes.c_double(), ctypes.c_int64()
     check(lib().emu_profile_read(kernel.encode(), ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
+
+
+def profile_all() -> dict:
+    """{kernel name: (total ms, launches)} for every kernel recorded since the last read."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    check(lib().emu_profile_names(buf, len(buf)))
+    return {k: profile_read(k) for k in buf.value.decode().split("\n") if k}

@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -79,10 +81,30 @@ __global__ void k_validate(RecIn r, unsigned long long* first_bad, int* maxv) {
   }
 }
 
-__global__ void k_make_keys(RecIn r, int cbits, uint64_t* __restrict__ hi, uint64_t* __restrict__ lo) {
+template <typename H>
+__global__ void k_make_keys(RecIn r, int cbits, H* __restrict__ hi, uint64_t* __restrict__ lo) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n; i += (int64_t)gridDim.x * blockDim.x) {
-    hi[i] = ((uint64_t)(uint32_t)(r.tt[i] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[i] - 1);
+    hi[i] = (H)(((uint64_t)(uint32_t)(r.tt[i] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[i] - 1));
     lo[i] = ((uint64_t)__double_as_longlong(r.lat[i]) << 1) | (r.ph[i] ? 1ULL : 0ULL);
+  }
+}
+
+// Record count of every (phase, bucket key) over the dense key domain
+// [0, 2^kb) per phase, from the SORTED records: a warp's 32 consecutive
+// records share one or two keys, so one atomic per distinct key per warp is
+// cheap (counting before the sort hammers the hot decode keys).  The tables'
+// buckets and offsets then come from scans over the domain (segment_dense)
+// instead of scans over the records.
+template <typename H>
+__global__ void k_dense_count(const H* __restrict__ hi, const uint64_t* __restrict__ lo, int64_t n, int kb,
+                              unsigned int* __restrict__ dcnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;  // warp-uniform trip count (match_any below)
+    const bool v = i < n;
+    const unsigned key = v ? ((unsigned)(lo[i] & 1ULL) << kb) | (unsigned)hi[i] : 0xffffffffu - (unsigned)lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (v && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&dcnt[key], (unsigned)__popc(peers));
   }
 }
 
@@ -93,13 +115,14 @@ struct PassSet {
 };
 
 // Histograms of every candidate digit position in one read of the keys.
-__global__ void k_digit_hist(const uint64_t* __restrict__ hi, const uint64_t* __restrict__ lo, int64_t n, PassSet ps,
+template <typename H>
+__global__ void k_digit_hist(const H* __restrict__ hi, const uint64_t* __restrict__ lo, int64_t n, PassSet ps,
                              unsigned int* hist) {
   extern __shared__ unsigned int sh[];
   for (int i = threadIdx.x; i < ps.n * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t h = hi[i], l = lo[i];
+    const uint64_t h = (uint64_t)hi[i], l = lo[i];
     for (int p = 0; p < ps.n; p++) {
       const uint64_t w = ps.word[p] ? h : l;
       atomicAdd(&sh[p * 256 + (int)((w >> ps.shift[p]) & 255u)], 1u);
@@ -212,17 +235,152 @@ __global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __r
   }
 }
 
+// One LSD pass without an up-sweep ("onesweep"): every pass's global digit
+// starts come from the single all-digits histogram (k_digit_hist); a tile's
+// offset inside each digit bucket comes from a decoupled look-back over the
+// tiles before it.  Tiles take their index from an atomic counter in launch
+// order, so a tile only ever waits on tiles that are already running.
+// Per record and pass: the (hi, lo) pair is read once and written once
+// (12 B each way with 32-bit bucket keys) -- no separate counting pass.
+// look[t * 256 + d] = flag << 30 | value: flag 1 = tile t's own count of digit
+// d, flag 2 = inclusive prefix over tiles <= t (values < 2^30: n < 2^30).
+constexpr unsigned kLookAgg = 1u << 30, kLookPre = 2u << 30, kLookVal = (1u << 30) - 1u;
+template <typename H>
+__global__ void __launch_bounds__(kRThreads) k_onesweep(const H* __restrict__ a_hi, const uint64_t* __restrict__ a_lo,
+                                                       H* __restrict__ b_hi, uint64_t* __restrict__ b_lo, int64_t n,
+                                                       int shift, int key_is_hi, const unsigned int* __restrict__ gstart,
+                                                       unsigned int* look, unsigned int* tile_ctr) {
+  constexpr int kWarpItems = kRTile / kRWarps;  // 512 consecutive records per warp
+  extern __shared__ __align__(16) unsigned char osm[];
+  uint64_t* s_lo = reinterpret_cast<uint64_t*>(osm);
+  H* s_hi = reinterpret_cast<H*>(osm + (size_t)kRTile * 8);
+  __shared__ unsigned short wcnt[kRWarps][256];  // per-warp digit counts, then each warp's offset in the digit
+  __shared__ unsigned int tstart[256];
+  __shared__ unsigned int gofs[256];  // gstart[d] + this tile's exclusive prefix
+  __shared__ unsigned int wsum[kRWarps];
+  __shared__ unsigned int s_tile;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) s_tile = atomicAdd(tile_ctr, 1u);
+#pragma unroll
+  for (int q = 0; q < kRWarps; q++) wcnt[q][t] = 0;
+  __syncthreads();
+  const unsigned tile = s_tile;
+  const int64_t base = (int64_t)tile * kRTile;
+  const int cnt_tile = (int)min((int64_t)kRTile, n - base);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // ---- load: warp w owns records [w*512, (w+1)*512) of the tile, 32 per round (coalesced)
+  H h[kRRounds];
+  uint64_t l[kRRounds];
+  unsigned rk[kRRounds / 2];  // warp-local ranks (< 512), two per register
+#pragma unroll
+  for (int k = 0; k < kRRounds; k++) {
+    const int li = w * kWarpItems + k * 32 + lane;
+    h[k] = 0;
+    l[k] = 0;
+    if (li < cnt_tile) {
+      h[k] = a_hi[base + li];
+      l[k] = a_lo[base + li];
+    }
+  }
+  // ---- warp-private ranking (no block barriers): rank = the warp's running
+  // count of the digit + this round's rank among equal digits
+#pragma unroll
+  for (int k = 0; k < kRRounds; k++) {
+    const bool valid = w * kWarpItems + k * 32 + lane < cnt_tile;
+    const unsigned d = valid ? (unsigned)(((key_is_hi ? (uint64_t)h[k] : l[k]) >> shift) & 255u) : 256u + (unsigned)lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned r = __popc(peers & lt_mask);
+    const unsigned before = valid ? wcnt[w][d] : 0u;
+    if (k & 1)
+      rk[k >> 1] |= (before + r) << 16;
+    else
+      rk[k >> 1] = before + r;
+    __syncwarp();
+    if (valid && r == 0) wcnt[w][d] = (unsigned short)(before + __popc(peers));
+    __syncwarp();
+  }
+  __syncthreads();
+  // ---- per digit: the tile's count and each warp's offset inside the digit
+  unsigned c = 0;
+#pragma unroll
+  for (int q = 0; q < kRWarps; q++) {
+    const unsigned cq = wcnt[q][t];
+    wcnt[q][t] = (unsigned short)c;
+    c += cq;
+  }
+  if (tile == 0)
+    atomicExch(&look[t], kLookPre | c);
+  else
+    atomicExch(&look[(size_t)tile * 256 + t], kLookAgg | c);
+  unsigned x = c;  // exclusive scan of the 256 counts -> tile-local digit starts
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  unsigned wb = 0;
+  for (int q = 0; q < w; q++) wb += wsum[q];
+  tstart[t] = wb + x - c;
+  __syncthreads();
+  // ---- stage the tile in digit order
+#pragma unroll
+  for (int k = 0; k < kRRounds; k++) {
+    if (w * kWarpItems + k * 32 + lane < cnt_tile) {
+      const unsigned d = (unsigned)(((key_is_hi ? (uint64_t)h[k] : l[k]) >> shift) & 255u);
+      const unsigned lp = tstart[d] + wcnt[w][d] + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
+      s_hi[lp] = h[k];
+      s_lo[lp] = l[k];
+    }
+  }
+  // ---- look back for the tile's exclusive prefix in every digit bucket:
+  // 16 predecessors per step are read at once (independent loads), so the
+  // dependent chain is ~1/16 of the distance to the nearest inclusive prefix
+  unsigned excl = 0;
+  if (tile > 0) {
+    constexpr int kLB = 16;
+    bool done = false;
+    for (int64_t q0 = (int64_t)tile - 1; !done; q0 -= kLB) {
+      unsigned v[kLB];
+#pragma unroll
+      for (int i = 0; i < kLB; i++)
+        v[i] = q0 - i >= 0 ? *(volatile unsigned int*)&look[(size_t)(q0 - i) * 256 + t] : (2u << 30);  // before tile 0: prefix 0
+#pragma unroll
+      for (int i = 0; i < kLB; i++) {
+        if (done) break;
+        while ((v[i] & ~kLookVal) == 0) v[i] = *(volatile unsigned int*)&look[(size_t)(q0 - i) * 256 + t];
+        excl += v[i] & kLookVal;
+        done = (v[i] & ~kLookVal) == kLookPre;
+      }
+    }
+    atomicExch(&look[(size_t)tile * 256 + t], kLookPre | (excl + c));
+  }
+  gofs[t] = gstart[t] + excl;
+  __syncthreads();
+  // ---- write every digit's run of the tile out contiguously
+  for (int j = t; j < cnt_tile; j += kRThreads) {
+    const H hv = s_hi[j];
+    const uint64_t lv = s_lo[j];
+    const unsigned d = (unsigned)(((key_is_hi ? (uint64_t)hv : lv) >> shift) & 255u);
+    const unsigned pos = gofs[d] + (unsigned)j - tstart[d];
+    b_hi[pos] = hv;
+    b_lo[pos] = lv;
+  }
+}
+
 // Stable partition by phase bit (lo & 1): decode (0) records first.
 struct PhaseIn {
   const uint64_t* lo;
   __device__ uint32_t operator()(int64_t i) const { return (lo[i] & 1ULL) ? 0u : 1u; }
 };
+template <typename H>
 struct PhaseOut {
-  const uint64_t* hi;
+  const H* hi;
   const uint64_t* lo;
-  uint64_t* d_hi;
+  H* d_hi;
   uint64_t* d_lo;
-  uint64_t* m_hi;
+  H* m_hi;
   uint64_t* m_lo;
   __device__ void operator()(int64_t i, uint32_t ex) const {
     if (lo[i] & 1ULL) {
@@ -237,12 +395,14 @@ struct PhaseOut {
 };
 
 // Segmenting a sorted run into buckets.
+template <typename H>
 struct HeadIn {
-  const uint64_t* hi;
+  const H* hi;
   __device__ uint32_t operator()(int64_t i) const { return (i == 0 || hi[i] != hi[i - 1]) ? 1u : 0u; }
 };
+template <typename H>
 struct HeadOut {
-  const uint64_t* hi;
+  const H* hi;
   const uint64_t* lo;
   int cbits;
   int32_t* bkt_tt;
@@ -250,8 +410,8 @@ struct HeadOut {
   int64_t* bkt_off;
   double* samples;
   __device__ void operator()(int64_t i, uint32_t ex) const {
-    const uint64_t h = hi[i];
-    if (i == 0 || h != hi[i - 1]) {
+    const uint64_t h = (uint64_t)hi[i];
+    if (i == 0 || h != (uint64_t)hi[i - 1]) {
       bkt_tt[ex] = (int32_t)(h >> cbits) + 1;
       bkt_conc[ex] = (int32_t)(h & ((1ULL << cbits) - 1ULL)) + 1;
       bkt_off[ex] = i;
@@ -276,6 +436,53 @@ struct RowOut {
   }
 };
 
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+// Dense-domain segmentation: table j (0 decode, 1 mixed, 2 combined) over the
+// key domain; a scan element packs (1 bucket << 32 | records) for a key with
+// records, so one 64-bit exclusive scan gives each bucket's index and offset.
+struct DenseIn {
+  const unsigned int* c0;  // decode counts per key
+  const unsigned int* c1;  // mixed counts per key
+  int j;
+  __device__ unsigned int cnt(int64_t k) const { return j == 0 ? c0[k] : j == 1 ? c1[k] : c0[k] + c1[k]; }
+  __device__ uint64_t operator()(int64_t k) const {
+    const unsigned int c = cnt(k);
+    return c ? ((1ULL << 32) | c) : 0ULL;
+  }
+};
+struct DenseOut {
+  DenseIn in;
+  int cbits;
+  int32_t* bkt_tt;
+  int32_t* bkt_conc;
+  int64_t* bkt_off;
+  __device__ void operator()(int64_t k, uint64_t ex) const {
+    if (!in.cnt(k)) return;
+    const int64_t b = (int64_t)(ex >> 32);
+    bkt_tt[b] = (int32_t)(k >> cbits) + 1;
+    bkt_conc[b] = (int32_t)(k & ((1LL << cbits) - 1)) + 1;
+    bkt_off[b] = (int64_t)(ex & 0xffffffffULL);
+  }
+};
+// The samples of all three tables in one pass over the sorted records: the
+// combined table is the sorted run, the phase tables its stable partition.
+struct SampleOut {
+  const uint64_t* lo;
+  double* comb;
+  double* dec;
+  double* mix;
+  __device__ void operator()(int64_t i, uint32_t ex) const {
+    const uint64_t l = lo[i];
+    const double v = __longlong_as_double((long long)(l >> 1));
+    comb[i] = v;
+    if (l & 1ULL)
+      mix[i - (int64_t)ex] = v;
+    else
+      dec[ex] = v;
+  }
+};
+
 __global__ void k_conc_range(const int32_t* c, int64_t n, int* mm) {
   int lo = 0x7fffffff, hi = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -294,28 +501,56 @@ __global__ void k_conc_range(const int32_t* c, int64_t n, int* mm) {
 }
 
 
-// Build scratch comes from the device's stream-ordered memory pool, kept
-// reserved between builds (release threshold = max): repeated builds reuse it
-// instead of mapping and unmapping GBs with cudaMalloc / cudaFree.
-static cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
-  static bool pool_set = false;
-  if (!pool_set) {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ULL;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    pool_set = true;
+static cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) { return table_alloc(p, bytes, s); }
+
+// Build scratch (key arrays, sort buffers, look-back flags, staged host
+// inputs) is bump-allocated from one persistent device buffer: no allocator
+// calls inside a build, so its time does not depend on what the pool did
+// last.  A build that needs more takes the excess from the pool and the
+// buffer is regrown to the peak for the next one.  Builds hold g_build_mu
+// (one at a time per process); emu_build_scratch_release frees the buffer.
+struct BuildScratch {
+  char* base = nullptr;
+  size_t cap = 0, used = 0, peak = 0;
+};
+static BuildScratch g_scratch;
+static std::mutex g_build_mu;
+
+static cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s, std::vector<void*>* spill) {
+  const size_t sz = ((bytes > 0 ? bytes : 1) + 255) & ~(size_t)255;
+  g_scratch.peak = std::max(g_scratch.peak, g_scratch.used + sz);
+  if (g_scratch.used + sz <= g_scratch.cap) {
+    *p = g_scratch.base + g_scratch.used;
+    g_scratch.used += sz;
+    return cudaSuccess;
   }
-  return cudaMallocAsync(p, bytes > 0 ? bytes : 1, s);
+  g_scratch.used += sz;
+  const cudaError_t e = pool_alloc(p, sz, s);
+  if (e == cudaSuccess) spill->push_back(*p);
+  return e;
 }
 
-// Table outputs from the same pool (TableBuf::release frees them with cudaFree).
+// After a build (stream synchronized): grow the buffer to the peak it needed.
+static void scratch_settle() {
+  if (g_scratch.peak > g_scratch.cap) {
+    cudaFree(g_scratch.base);
+    g_scratch.base = nullptr;
+    g_scratch.cap = 0;
+    const size_t want = g_scratch.peak + (g_scratch.peak >> 4);
+    if (cudaMalloc((void**)&g_scratch.base, want) == cudaSuccess)
+      g_scratch.cap = want;
+    else
+      cudaGetLastError();
+  }
+  g_scratch.used = 0;
+  g_scratch.peak = 0;
+}
+
+// Table outputs (TableBuf::release returns them to the pool).
 template <typename T>
 static int palloc(cudaStream_t s, T** p, int64_t n) {
   *p = nullptr;
-  EMU_CUDA(scratch_alloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), s));
+  EMU_CUDA(pool_alloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), s));
   return EMU_OK;
 }
 
@@ -331,7 +566,11 @@ static int bits_for(int64_t maxval_minus1) {
 }
 
 // Segment one sorted run of m records into a TableBuf.
-static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits, unsigned int* partial,
+static int segment_finish(TableBuf& tb, int64_t nb, int64_t m, unsigned int* partial, unsigned int* total_dev,
+                          int* mm_dev, cudaStream_t s);
+
+template <typename H>
+static int segment(const H* hi, const uint64_t* lo, int64_t m, int cbits, unsigned int* partial,
                    unsigned int* total_dev, int* mm_dev, cudaStream_t s, TableBuf& tb) {
   tb = TableBuf();
   int rc;
@@ -344,7 +583,7 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
     return EMU_OK;
   }
   // pass 1: count buckets
-  EMU_CUDA(device_excl_scan<unsigned int>(HeadIn{hi}, [] __device__(int64_t, unsigned int) {}, m, partial, total_dev, s));
+  EMU_CUDA(device_excl_scan<unsigned int>(HeadIn<H>{hi}, [] __device__(int64_t, unsigned int) {}, m, partial, total_dev, s));
   unsigned int nb_u = 0;
   EMU_CUDA(cudaMemcpyAsync(&nb_u, total_dev, 4, cudaMemcpyDeviceToHost, s));
   EMU_CUDA(cudaStreamSynchronize(s));
@@ -352,9 +591,17 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
   if ((rc = palloc(s, &tb.bkt_tt, nb)) || (rc = palloc(s, &tb.bkt_conc, nb)) || (rc = palloc(s, &tb.bkt_off, nb + 1)) ||
       (rc = palloc(s, &tb.samples, m)))
     return rc;
-  HeadOut ho{hi, lo, cbits, tb.bkt_tt, tb.bkt_conc, tb.bkt_off, tb.samples};
-  EMU_CUDA(device_excl_scan<unsigned int>(HeadIn{hi}, ho, m, partial, total_dev, s));
+  HeadOut<H> ho{hi, lo, cbits, tb.bkt_tt, tb.bkt_conc, tb.bkt_off, tb.samples};
+  EMU_CUDA(device_excl_scan<unsigned int>(HeadIn<H>{hi}, ho, m, partial, total_dev, s));
   EMU_CUDA(cudaMemcpyAsync(tb.bkt_off + nb, &m, 8, cudaMemcpyHostToDevice, s));
+  return segment_finish(tb, nb, m, partial, total_dev, mm_dev, s);
+}
+
+// Rows (distinct tt), key ranges and the search index of a table whose bucket
+// arrays and samples are written.
+static int segment_finish(TableBuf& tb, int64_t nb, int64_t m, unsigned int* partial, unsigned int* total_dev,
+                          int* mm_dev, cudaStream_t s) {
+  int rc;
   // rows
   EMU_CUDA(device_excl_scan<unsigned int>(RowIn{tb.bkt_tt}, [] __device__(int64_t, unsigned int) {}, nb, partial,
                                           total_dev, s));
@@ -394,6 +641,49 @@ static int segment(const uint64_t* hi, const uint64_t* lo, int64_t m, int cbits,
   return build_search_index(tb, htt.data(), hcc.data(), hoff.data(), s);
 }
 
+// The three tables from the dense per-(phase, key) counts and the sorted
+// records: one packed scan over the key domain per table (buckets, offsets),
+// one scan over the records for all samples, then rows / ranges / index.
+template <typename H>
+static int segment_dense(const uint64_t* lo, int64_t n, int cbits, int kb, const unsigned int* dcnt,
+                         uint64_t* part64, uint64_t* tot64, unsigned int* partial, unsigned int* total_dev,
+                         int* mm_dev, cudaStream_t s, TableBuf* tab) {
+  const int64_t D = 1LL << kb;
+  const int64_t np = (D + kScanTile - 1) / kScanTile + 1;
+  int rc;
+  for (int j = 0; j < 3; j++)
+    EMU_CUDA(device_excl_scan<uint64_t>(DenseIn{dcnt, dcnt + D, j}, [] __device__(int64_t, uint64_t) {}, D,
+                                        part64 + j * np, tot64 + j, s));
+  uint64_t tot[3];
+  EMU_CUDA(cudaMemcpyAsync(tot, tot64, sizeof(tot), cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  for (int j = 0; j < 3; j++) {
+    TableBuf& tb = tab[j];
+    tb = TableBuf();
+    const int64_t nb = (int64_t)(tot[j] >> 32), m = (int64_t)(tot[j] & 0xffffffffULL);
+    if ((rc = palloc(s, &tb.bkt_tt, nb)) || (rc = palloc(s, &tb.bkt_conc, nb)) ||
+        (rc = palloc(s, &tb.bkt_off, nb + 1)) || (rc = palloc(s, &tb.samples, m)))
+      return rc;
+    EMU_CUDA(device_excl_scan<uint64_t>(DenseIn{dcnt, dcnt + D, j},
+                                        DenseOut{DenseIn{dcnt, dcnt + D, j}, cbits, tb.bkt_tt, tb.bkt_conc, tb.bkt_off},
+                                        D, part64 + j * np, tot64 + j, s));
+    int64_t* off_end = tb.bkt_off + nb;
+    EMU_LAUNCH("fill_end", s, k_set_i64<<<1, 1, 0, s>>>(off_end, m));
+  }
+  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn{lo}, SampleOut{lo, tab[2].samples, tab[0].samples, tab[1].samples},
+                                          n, partial, total_dev, s));
+  for (int j = 0; j < 3; j++) {
+    const int64_t nb = (int64_t)(tot[j] >> 32), m = (int64_t)(tot[j] & 0xffffffffULL);
+    if (nb == 0) {  // empty table (e.g. no mixed records): the shapes segment() gives it
+      if ((rc = palloc(s, &tab[j].row_tt, 0)) || (rc = palloc(s, &tab[j].row_start, 1))) return rc;
+      EMU_CUDA(cudaMemsetAsync(tab[j].row_start, 0, 8, s));
+      continue;
+    }
+    if ((rc = segment_finish(tab[j], nb, m, partial, total_dev, mm_dev, s))) return rc;
+  }
+  return EMU_OK;
+}
+
 static bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;
@@ -402,6 +692,129 @@ static bool is_device_ptr(const void* p) {
     return false;
   }
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace emu
+
+namespace emu {
+
+// Steps 2-5 of emu_tables_build for bucket keys of type H (uint32_t when
+// (tt-1) << cbits | (conc-1) fits, else uint64_t).  Scratch comes from salloc
+// (freed by the caller); the three tables are written to tab[0..2].
+template <typename H>
+static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits, int tbits, cudaStream_t s,
+                            TableBuf* tab, const std::function<int(void**, size_t)>& alloc, unsigned int* total_dev,
+                            int* small, const std::function<void(const char*)>& mark) {
+  int rc;
+  auto salloc = [&](auto** p, int64_t count) -> int {
+    return alloc(reinterpret_cast<void**>(p), sizeof(**p) * (size_t)(count > 0 ? count : 1));
+  };
+  H *hi0, *hi1;
+  uint64_t *lo0, *lo1;
+  unsigned int *counts = nullptr, *hist = nullptr, *partial = nullptr, *gst = nullptr, *look = nullptr,
+               *tile_ctr = nullptr;
+  const int64_t nblk = (n + kRTile - 1) / kRTile;
+  // EMU_ONESWEEP=0 (64-bit keys only): the up-sweep + scan + scatter passes instead
+  const char* os_env = getenv("EMU_ONESWEEP");
+  const bool onesweep = n < (1LL << 30) && !(os_env && os_env[0] == '0' && sizeof(H) == 8);
+  const int64_t ncount = onesweep ? 1 : 256 * nblk;
+  const int64_t npart = std::max<int64_t>((ncount + kScanTile - 1) / kScanTile, (n + kScanTile - 1) / kScanTile) + 1;
+  if ((rc = salloc(&hi0, n)) || (rc = salloc(&lo0, n)) || (rc = salloc(&hi1, n)) || (rc = salloc(&lo1, n)) ||
+      (rc = salloc(&counts, ncount)) || (rc = salloc(&hist, 16 * 256)) || (rc = salloc(&partial, npart)) ||
+      (rc = salloc(&gst, 16 * 256)) || (rc = salloc(&look, onesweep ? 256 * nblk : 1)) ||
+      (rc = salloc(&tile_ctr, 16)))
+    return rc;
+  // key domains up to 2^24 per phase: dense counts -> segment_dense (no scans over the records)
+  const int kb = tbits + cbits;
+  const bool dense = kb <= 24 && getenv("EMU_DENSE_SEGMENT") == nullptr;
+  const int64_t D = dense ? (1LL << kb) : 0;
+  const int64_t np64 = (D + kScanTile - 1) / kScanTile + 1;
+  unsigned int* dcnt = nullptr;
+  uint64_t *part64 = nullptr, *tot64 = nullptr;
+  if (dense) {
+    if ((rc = salloc(&dcnt, 2 * D)) || (rc = salloc(&part64, 3 * np64)) || (rc = salloc(&tot64, 4))) return rc;
+    EMU_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned int) * 2 * D, s));
+  }
+  EMU_LAUNCH("make_keys", s, k_make_keys<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, cbits, hi0, lo0));
+  // which digit positions actually vary
+  PassSet ps{};
+  if (canonical)
+    for (int sft = 0; sft < 64; sft += 8) {
+      ps.word[ps.n] = 0;
+      ps.shift[ps.n++] = sft;
+    }
+  for (int sft = 0; sft < tbits + cbits; sft += 8) {
+    ps.word[ps.n] = 1;
+    ps.shift[ps.n++] = sft;
+  }
+  EMU_CUDA(cudaMemsetAsync(hist, 0, 4 * 16 * 256, s));
+  EMU_LAUNCH("digit_hist", s,
+             k_digit_hist<H><<<grid_of(n, 256, kNumSMs * 4), 256, ps.n * 256 * 4, s>>>(hi0, lo0, n, ps, hist));
+  std::vector<unsigned int> hh(16 * 256), gs(16 * 256);
+  EMU_CUDA(cudaMemcpyAsync(hh.data(), hist, 4 * 16 * 256, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  for (int p = 0; p < ps.n; p++) {  // global digit starts of every pass
+    unsigned acc = 0;
+    for (int d = 0; d < 256; d++) {
+      gs[p * 256 + d] = acc;
+      acc += hh[p * 256 + d];
+    }
+  }
+  EMU_CUDA(cudaMemcpyAsync(gst, gs.data(), 4 * 16 * 256, cudaMemcpyHostToDevice, s));
+  EMU_CUDA(cudaMemsetAsync(tile_ctr, 0, 4 * 16, s));
+  mark("keys+hist");
+  // LSD passes
+  const size_t osmem = (size_t)kRTile * (8 + sizeof(H));
+  if (onesweep) {
+    EMU_CUDA(cudaFuncSetAttribute(k_onesweep<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem));
+  } else {
+    EMU_CUDA(cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem));
+  }
+  for (int p = 0; p < ps.n; p++) {
+    const unsigned int mx = *std::max_element(hh.begin() + p * 256, hh.begin() + (p + 1) * 256);
+    if ((int64_t)mx == n) continue;  // all records share this digit: pass is the identity
+    if (onesweep) {
+      EMU_CUDA(cudaMemsetAsync(look, 0, sizeof(unsigned int) * 256 * nblk, s));
+      EMU_LAUNCH("onesweep", s, k_onesweep<H><<<(unsigned)nblk, kRThreads, osmem, s>>>(
+                                    hi0, lo0, hi1, lo1, n, ps.shift[p], ps.word[p], gst + p * 256, look, tile_ctr + p));
+    } else {
+      if constexpr (std::is_same<H, uint64_t>::value) {
+        const uint64_t* key = ps.word[p] ? hi0 : lo0;
+        EMU_LAUNCH("radix_up", s, k_radix_up<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], n, nblk, counts));
+        EMU_CUDA(device_excl_scan<unsigned int>(
+            [counts] __device__(int64_t i) { return counts[i]; },
+            [counts] __device__(int64_t i, unsigned int ex) { counts[i] = ex; }, ncount, partial, total_dev, s));
+        EMU_LAUNCH("radix_scatter", s, k_radix_scatter<<<(unsigned)nblk, kRThreads, kRSmem, s>>>(
+                                           key, ps.shift[p], ps.word[p], hi0, lo0, hi1, lo1, n, nblk, counts));
+      } else {
+        return fail(EMU_ERR_INVALID, "internal: 32-bit keys need the onesweep sort");
+      }
+    }
+    std::swap(hi0, hi1);
+    std::swap(lo0, lo1);
+  }
+  EMU_CUDA(cudaGetLastError());
+  mark("radix sort");
+  if (dense) {
+    EMU_LAUNCH("dense_count", s, k_dense_count<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(hi0, lo0, n, kb, dcnt));
+    rc = segment_dense<H>(lo0, n, cbits, kb, dcnt, part64, tot64, partial, total_dev, small + 2, s, tab);
+    mark("segment (dense)");
+    return rc;
+  }
+  // combined table = sorted run; decode/mixed = stable partition by phase
+  if ((rc = segment<H>(hi0, lo0, n, cbits, partial, total_dev, small + 2, s, tab[2]))) return rc;
+  mark("segment combined");
+  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn{lo0}, [] __device__(int64_t, unsigned int) {}, n, partial,
+                                          total_dev, s));
+  unsigned int n_dec = 0;
+  EMU_CUDA(cudaMemcpyAsync(&n_dec, total_dev, 4, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn{lo0}, PhaseOut<H>{hi0, lo0, hi1, lo1, hi1 + n_dec, lo1 + n_dec}, n,
+                                          partial, total_dev, s));
+  mark("phase partition");
+  if ((rc = segment<H>(hi1, lo1, n_dec, cbits, partial, total_dev, small + 2, s, tab[0]))) return rc;
+  mark("segment decode");
+  return segment<H>(hi1 + n_dec, lo1 + n_dec, n - n_dec, cbits, partial, total_dev, small + 2, s, tab[1]);
 }
 
 }  // namespace emu
@@ -426,16 +839,18 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     fprintf(stderr, "[emu build] %-24s %8.3f ms\n", what, ms);
   };
+  std::lock_guard<std::mutex> build_lock(g_build_mu);
+  g_scratch.used = 0;
+  g_scratch.peak = 0;
   // Stage host inputs on the device (device inputs are used in place).
-  std::vector<void*> owned;
+  std::vector<void*> owned;  // scratch that did not fit the persistent buffer
   auto stage = [&](const void* src, size_t bytes, const void** dst) -> int {
     if (!src || bytes == 0 || is_device_ptr(src)) {
       *dst = src;
       return EMU_OK;
     }
     void* d = nullptr;
-    EMU_CUDA(scratch_alloc(&d, bytes, s));
-    owned.push_back(d);
+    EMU_CUDA(scratch_alloc(&d, bytes, s, &owned));
     EMU_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
     *dst = d;
     return EMU_OK;
@@ -443,14 +858,14 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   auto free_owned = [&]() {
     for (void* p : owned) cudaFreeAsync(p, s);
     owned.clear();
+    if (cudaStreamSynchronize(s) == cudaSuccess) scratch_settle();
   };
   auto salloc = [&](auto** p, int64_t count) -> int {
     using T = std::remove_pointer_t<std::remove_reference_t<decltype(p)>>;
     *p = nullptr;
     void* q = nullptr;
-    EMU_CUDA(scratch_alloc(&q, sizeof(**p) * (size_t)(count > 0 ? count : 1), s));
+    EMU_CUDA(scratch_alloc(&q, sizeof(**p) * (size_t)(count > 0 ? count : 1), s, &owned));
     *p = (decltype(*p))q;
-    owned.push_back(q);
     (void)sizeof(T);
     return EMU_OK;
   };
@@ -479,7 +894,7 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   };
   if (n == 0) {
     for (int j = 0; j < 3; j++)
-      if ((rc = segment(nullptr, nullptr, 0, 1, nullptr, nullptr, nullptr, s, t->tab[j]))) return bail(rc);
+      if ((rc = segment<uint64_t>(nullptr, nullptr, 0, 1, nullptr, nullptr, nullptr, s, t->tab[j]))) return bail(rc);
     if (cudaStreamSynchronize(s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "build sync"));
     free_owned();
     *out = t;
@@ -507,75 +922,29 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
   mark("validate");
   const int cbits = bits_for((int64_t)mv[1] - 1);
   const int tbits = bits_for((int64_t)mv[0] - 1);
-  // 2. keys (double buffered)
-  uint64_t *hi0, *lo0, *hi1, *lo1;
-  unsigned int *counts = nullptr, *hist = nullptr, *partial = nullptr;
-  const int64_t nblk = (n + kRTile - 1) / kRTile;
-  const int64_t ncount = 256 * nblk;
-  const int64_t npart = std::max<int64_t>((ncount + kScanTile - 1) / kScanTile, (n + kScanTile - 1) / kScanTile) + 1;
-  if ((rc = salloc(&hi0, n)) || (rc = salloc(&lo0, n)) || (rc = salloc(&hi1, n)) || (rc = salloc(&lo1, n)) ||
-      (rc = salloc(&counts, ncount)) || (rc = salloc(&hist, 16 * 256)) || (rc = salloc(&partial, npart)))
-    return bail(rc);
-  EMU_LAUNCH("make_keys", s, k_make_keys<<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, cbits, hi0, lo0));
-  // 3. which digit positions actually vary
-  PassSet ps{};
-  if (canonical)
-    for (int sft = 0; sft < 64; sft += 8) {
-      ps.word[ps.n] = 0;
-      ps.shift[ps.n++] = sft;
-    }
-  for (int sft = 0; sft < tbits + cbits; sft += 8) {
-    ps.word[ps.n] = 1;
-    ps.shift[ps.n++] = sft;
-  }
-  if (cudaMemsetAsync(hist, 0, 4 * 16 * 256, s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "memset"));
-  EMU_LAUNCH("digit_hist", s, k_digit_hist<<<grid_of(n, 256, kNumSMs * 4), 256, ps.n * 256 * 4, s>>>(hi0, lo0, n, ps, hist));
-  std::vector<unsigned int> hh(16 * 256);
-  if (cudaMemcpyAsync(hh.data(), hist, 4 * 16 * 256, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess)
-    return bail(cuda_fail(cudaGetLastError(), "k_digit_hist"));
-  mark("keys+hist");
-  // 4. LSD passes
-  if (cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem) != cudaSuccess)
-    return bail(cuda_fail(cudaGetLastError(), "radix smem attribute"));
-  for (int p = 0; p < ps.n; p++) {
-    unsigned int mx = *std::max_element(hh.begin() + p * 256, hh.begin() + (p + 1) * 256);
-    if ((int64_t)mx == n) continue;  // all records share this digit: pass is the identity
-    const uint64_t* key = ps.word[p] ? hi0 : lo0;
-    EMU_LAUNCH("radix_up", s, k_radix_up<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], n, nblk, counts));
-    cudaError_t e = device_excl_scan<unsigned int>(
-        [counts] __device__(int64_t i) { return counts[i]; },
-        [counts] __device__(int64_t i, unsigned int ex) { counts[i] = ex; }, ncount, partial, total_dev, s);
-    if (e != cudaSuccess) return bail(cuda_fail(e, "radix scan"));
-    EMU_LAUNCH("radix_scatter", s, k_radix_scatter<<<(unsigned)nblk, kRThreads, kRSmem, s>>>(
-                                       key, ps.shift[p], ps.word[p], hi0, lo0, hi1, lo1, n, nblk, counts));
-    std::swap(hi0, hi1);
-    std::swap(lo0, lo1);
-  }
-  if (cudaGetLastError() != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "radix sort"));
-  mark("radix sort");
-  // 5. combined table = sorted run; decode/mixed = stable partition by phase
-  if ((rc = segment(hi0, lo0, n, cbits, partial, total_dev, small + 2, s, t->tab[2]))) return bail(rc);
-  mark("segment combined");
-  cudaError_t e = device_excl_scan<unsigned int>(PhaseIn{lo0}, [] __device__(int64_t, unsigned int) {}, n, partial,
-                                                 total_dev, s);
-  if (e != cudaSuccess) return bail(cuda_fail(e, "phase partition count"));
-  unsigned int n_dec = 0;
-  if (cudaMemcpyAsync(&n_dec, total_dev, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess)
-    return bail(cuda_fail(cudaGetLastError(), "phase partition"));
-  e = device_excl_scan<unsigned int>(PhaseIn{lo0}, PhaseOut{hi0, lo0, hi1, lo1, hi1 + n_dec, lo1 + n_dec}, n, partial,
-                                     total_dev, s);
-  if (e != cudaSuccess) return bail(cuda_fail(e, "phase partition"));
-  mark("phase partition");
-  if ((rc = segment(hi1, lo1, n_dec, cbits, partial, total_dev, small + 2, s, t->tab[0]))) return bail(rc);
-  mark("segment decode");
-  if ((rc = segment(hi1 + n_dec, lo1 + n_dec, n - n_dec, cbits, partial, total_dev, small + 2, s, t->tab[1])))
-    return bail(rc);
+  // 2.-5. keys, sort, partition, segment: 32-bit bucket keys when they fit
+  const std::function<int(void**, size_t)> alloc_fn = [&](void** p, size_t bytes) -> int {
+    *p = nullptr;
+    EMU_CUDA(scratch_alloc(p, bytes, s, &owned));
+    return EMU_OK;
+  };
+  const std::function<void(const char*)> mark_fn = mark;
+  if (tbits + cbits <= 32 && n < (1LL << 30))
+    rc = sort_and_segment<uint32_t>(r, n, canonical != 0, cbits, tbits, s, t->tab, alloc_fn, total_dev, small, mark_fn);
+  else
+    rc = sort_and_segment<uint64_t>(r, n, canonical != 0, cbits, tbits, s, t->tab, alloc_fn, total_dev, small, mark_fn);
+  if (rc) return bail(rc);
   if (cudaStreamSynchronize(s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "build"));
   mark("segment mixed");
   free_owned();
   mark("free");
   *out = t;
+  return EMU_OK;
+}
+
+extern "C" int emu_build_scratch_release(void) {
+  std::lock_guard<std::mutex> lk(g_build_mu);
+  EMU_CUDA(cudaFree(g_scratch.base));
+  g_scratch = BuildScratch();
   return EMU_OK;
 }

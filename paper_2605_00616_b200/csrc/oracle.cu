@@ -46,7 +46,14 @@ constexpr int kCtaCap = 8192;  // candidates in shared memory per CTA
 constexpr int kCtaSmem = kCtaCap * 12;
 constexpr int kCtaCache = 1024;  // cached counts/offsets per CTA workspace
 constexpr int kGrpThreads = 128;  // middle tier: one 4-warp group per key
-constexpr int kGrpCap = 2048;
+#ifndef EMU_GRP_CAP
+#define EMU_GRP_CAP 2048
+#endif
+#ifndef EMU_GRP_CACHE
+#define EMU_GRP_CACHE 1024
+#endif
+constexpr int kGrpCap = EMU_GRP_CAP;      // candidates per group workspace (bigger windows: CTA tier)
+constexpr int kGrpCache = EMU_GRP_CACHE;  // cached counts/offsets per group
 constexpr int kGrpSmem = kGrpCap * 12;
 #ifndef EMU_GRP_MINB
 #define EMU_GRP_MINB 8  // 4-warp groups per SM in the grid (C3 M=256: 84 vs 96 ms at 4)
@@ -514,9 +521,9 @@ __global__ void __launch_bounds__(kGrpThreads, EMU_GRP_MINB) k_pool_grp(DevTable
   __shared__ double dsh[10];
   __shared__ int s_w;
   __shared__ int32_t rows[3 * kGrpThreads];
-  __shared__ int32_t ncache[2 * kCtaCache];
-  PoolWS ws{(double*)smem, (int32_t*)(smem + kGrpCap * 8), kGrpCap, scr, dsh, rows, ncache, ncache + kCtaCache,
-            kCtaCache};
+  __shared__ int32_t ncache[2 * kGrpCache];
+  PoolWS ws{(double*)smem, (int32_t*)(smem + kGrpCap * 8), kGrpCap, scr, dsh, rows, ncache, ncache + kGrpCache,
+            kGrpCache};
   const int n = *esc_count;
   for (;;) {
     if (threadIdx.x == 0) s_w = atomicAdd(work, 1);

@@ -543,7 +543,7 @@ __device__ __forceinline__ bool grp_sort_runs(const PoolWS& ws, int64_t pos) {
   return true;
 }
 
-// Multi-warp groups, up to 4 candidates per thread: bucket sort by d^2 (1024
+// Multi-warp groups, up to 4 candidates per thread: bucket sort by d^2 (512
 // bins over [0, max d^2]: monotone in d, so bins are in distance order), then
 // each bin's few entries ordered by (d, bucket) in place.  Elements travel in
 // registers, bin counts live in the ncache arrays (free until prefix_k).  Four
@@ -551,7 +551,7 @@ __device__ __forceinline__ bool grp_sort_runs(const PoolWS& ws, int64_t pos) {
 // sorts otherwise) when it does not apply.
 template <int NT>
 __device__ __forceinline__ bool grp_bucket_sort(const PoolWS& ws, int64_t pos) {
-  constexpr int E = 4, NB = 1024;
+  constexpr int E = 4, NB = 512;
   using G = Grp<NT>;
   if (NT <= 32 || pos > (int64_t)E * NT || 2 * ws.ncache < NB + NB / 32) return false;
   const int r = G::rank(), lane = r & 31;
@@ -813,7 +813,23 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
   EMU_STAT(8, C);
   EMU_PHASE(2);
   if (C > ws.cap) return -1;
-  // ---- 3. enumerate (candidates beyond dmax cannot be pooled and are dropped)
+  // ---- 3. enumerate (candidates beyond dmax cannot be pooled and are dropped).
+  // Group tiers also count, per thread, the samples within each of the 8 pivot
+  // radii of step 3b while the candidate's bucket is at hand.
+  const bool pivots = NT > 32 && dmax < 1e300;
+  double pv[8];
+  unsigned long long pacc[8];
+#pragma unroll
+  for (int l = 0; l < 8; l++) {
+    pv[l] = r1 * (1.0 + 0.41421356237309515 * (double)(l + 1) * 0.125);
+    pacc[l] = 0;
+  }
+  auto pivot_count = [&](bool in, double d, int32_t bb) {
+    if (!pivots || !in) return;
+    const unsigned long long cn = (unsigned long long)min((int64_t)(T.bkt_off[bb + 1] - T.bkt_off[bb]), mfloor);
+#pragma unroll
+    for (int l = 0; l < 8; l++) pacc[l] += d <= pv[l] ? cn : 0ULL;
+  };
   int pos = 0;
   int* acnt = reinterpret_cast<int*>(ws.scr + 32);  // group tiers: append counter
   if (NT > 32) {
@@ -855,6 +871,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
           d = dist_tab(T, (int64_t)t - T.col_tt[idx], (int64_t)c - (T.c_lo + w.j0 + l0), span_t, span_c);
           in = d <= dmax;
         }
+        pivot_count(in, d, bb);
         append_cand<NT>(in, d, bb, ws, pos, acnt);
       }
       G::sync();
@@ -871,6 +888,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
             in = d <= dmax;
           }
         }
+        pivot_count(in, d, b);
         append_cand<NT>(in, d, b, ws, pos, acnt);
       }
     } else {  // row by row: bsat gives each row's conc sub-range
@@ -909,6 +927,7 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
             d = dist_tab(T, ws.rows[2 * NT + lo_r], (int64_t)c - T.bkt_conc[bb], span_t, span_c);
             in = d <= dmax;
           }
+          pivot_count(in, d, bb);
           append_cand<NT>(in, d, bb, ws, pos, acnt);
         }
         G::sync();
@@ -925,28 +944,13 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
   // smallest whose disc already holds >= floor samples bounds d_K, and every
   // candidate beyond it sorts after the pool.  Typical M = 256 windows shrink
   // from ~1.8 K to ~1.1 K candidates, halving the shared-memory sort.
-  if (NT > 32 && pos > 64 && dmax < 1e300) {
+  if (pivots && pos > 64) {
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ws.scr) + 16;
     if (G::rank() < 8) cnt[G::rank()] = 0;
     G::sync();
-    double pv[8];
-    unsigned long long acc[8];
 #pragma unroll
     for (int l = 0; l < 8; l++) {
-      pv[l] = r1 * (1.0 + 0.41421356237309515 * (double)(l + 1) * 0.125);
-      acc[l] = 0;
-    }
-    for (int i = G::rank(); i < pos; i += NT) {
-      const double d = ws.d[i];
-      const int32_t bb = ws.b[i];
-      const unsigned long long n =
-          (unsigned long long)min((int64_t)(T.bkt_off[bb + 1] - T.bkt_off[bb]), mfloor);
-#pragma unroll
-      for (int l = 0; l < 8; l++) acc[l] += d <= pv[l] ? n : 0ULL;
-    }
-#pragma unroll
-    for (int l = 0; l < 8; l++) {
-      unsigned long long v = acc[l];
+      unsigned long long v = pacc[l];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
       if ((G::rank() & 31) == 0 && v) atomicAdd(&cnt[l], v);

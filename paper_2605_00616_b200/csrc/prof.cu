@@ -1,5 +1,7 @@
 // prof.cu -- launch counter and CUDA-event kernel timing (emu_profile_* ABI).
+#include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
@@ -79,6 +81,22 @@ int emu_profile_read(const char* kernel, double* total_ms, int64_t* launches) {
   if (launches) *launches = a.n;
   a.ms = 0;
   a.n = 0;
+  return EMU_OK;
+}
+
+// Newline-separated names of every kernel with launches recorded since they
+// were last read (emu_profile_read), truncated to cap - 1 bytes.
+int emu_profile_names(char* buf, int64_t cap) {
+  if (!buf || cap < 1) return fail(EMU_ERR_INVALID, "buffer is NULL or empty");
+  std::string out;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& kv : *g_acc)
+      if (!kv.second.pending.empty() || kv.second.n) out += kv.first + "\n";
+  }
+  const size_t n = std::min<size_t>(out.size(), (size_t)cap - 1);
+  memcpy(buf, out.data(), n);
+  buf[n] = 0;
   return EMU_OK;
 }
 

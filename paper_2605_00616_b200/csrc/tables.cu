@@ -32,23 +32,31 @@ int cuda_fail(cudaError_t e, const char* what) {
   return EMU_ERR_CUDA;
 }
 
+// Every table array comes from the device's stream-ordered pool, kept
+// reserved (release threshold = max): repeated builds and table handles reuse
+// the memory instead of mapping and unmapping it (cudaMalloc / cudaFree made
+// the 100M-record build's time swing by 3x with what the previous build left).
+cudaError_t table_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static const bool pool_set = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return true;
+  }();
+  (void)pool_set;
+  return cudaMallocAsync(p, bytes > 0 ? bytes : 1, s);
+}
+
 void TableBuf::release() {
-  cudaFree(bkt_tt);
-  cudaFree(bkt_conc);
-  cudaFree(bkt_off);
-  cudaFree(samples);
-  cudaFree(row_tt);
-  cudaFree(row_start);
-  cudaFree(bsat);
-  cudaFree(ssat);
-  cudaFree(bmap);
-  cudaFree(wpre);
-  cudaFree(rowbase);
-  cudaFree(col_start);
-  cudaFree(col_tt);
-  cudaFree(col_b);
-  cudaFree(sq_t);
-  cudaFree(sq_c);
+  cudaDeviceSynchronize();  // kernels on any stream may still read the table
+  for (void* p : {(void*)bkt_tt, (void*)bkt_conc, (void*)bkt_off, (void*)samples, (void*)row_tt, (void*)row_start,
+                  (void*)bsat, (void*)ssat, (void*)bmap, (void*)wpre, (void*)rowbase, (void*)col_start, (void*)col_tt,
+                  (void*)col_b, (void*)sq_t, (void*)sq_c})
+    if (p) cudaFreeAsync(p, 0);
+  cudaStreamSynchronize(0);
   *this = TableBuf();
 }
 
@@ -100,8 +108,8 @@ int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, c
   const int64_t span_t = (int64_t)tb.tt_hi - tb.tt_lo, span_c = (int64_t)tb.c_hi - tb.c_lo;
   tb.lt = std::min<int64_t>(span_t + 1, kMaxSqTable);
   tb.lc = std::min<int64_t>(span_c + 1, kMaxSqTable);
-  EMU_CUDA(cudaMalloc((void**)&tb.sq_t, 8 * tb.lt));
-  EMU_CUDA(cudaMalloc((void**)&tb.sq_c, 8 * tb.lc));
+  EMU_CUDA(table_alloc((void**)&tb.sq_t, 8 * tb.lt, s));
+  EMU_CUDA(table_alloc((void**)&tb.sq_c, 8 * tb.lc, s));
   EMU_LAUNCH("index", s, k_sq_table<<<(unsigned)std::min<int64_t>(1024, (tb.lt + 255) / 256), 256, 0, s>>>(tb.sq_t, tb.lt, span_t));
   EMU_LAUNCH("index", s, k_sq_table<<<(unsigned)std::min<int64_t>(1024, (tb.lc + 255) / 256), 256, 0, s>>>(tb.sq_c, tb.lc, span_c));
   EMU_CUDA(cudaGetLastError());
@@ -154,17 +162,17 @@ int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, c
       cb[(size_t)k] = (int32_t)b;
     }
   }
-  EMU_CUDA(cudaMalloc((void**)&tb.col_start, 4 * (gnc + 1)));
-  EMU_CUDA(cudaMalloc((void**)&tb.col_tt, 4 * std::max<int64_t>(1, tb.nb)));
-  EMU_CUDA(cudaMalloc((void**)&tb.col_b, 4 * std::max<int64_t>(1, tb.nb)));
+  EMU_CUDA(table_alloc((void**)&tb.col_start, 4 * (gnc + 1), s));
+  EMU_CUDA(table_alloc((void**)&tb.col_tt, 4 * std::max<int64_t>(1, tb.nb), s));
+  EMU_CUDA(table_alloc((void**)&tb.col_b, 4 * std::max<int64_t>(1, tb.nb), s));
   EMU_CUDA(cudaMemcpyAsync(tb.col_start, cstart.data(), 4 * (gnc + 1), cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMemcpyAsync(tb.col_tt, ctt.data(), 4 * tb.nb, cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMemcpyAsync(tb.col_b, cb.data(), 4 * tb.nb, cudaMemcpyHostToDevice, s));
-  EMU_CUDA(cudaMalloc((void**)&tb.bsat, 4 * cells));
-  EMU_CUDA(cudaMalloc((void**)&tb.ssat, 4 * cells));
-  EMU_CUDA(cudaMalloc((void**)&tb.bmap, 4 * gnt * wpr));
-  EMU_CUDA(cudaMalloc((void**)&tb.wpre, 4 * gnt * wpr));
-  EMU_CUDA(cudaMalloc((void**)&tb.rowbase, 4 * (gnt + 1)));
+  EMU_CUDA(table_alloc((void**)&tb.bsat, 4 * cells, s));
+  EMU_CUDA(table_alloc((void**)&tb.ssat, 4 * cells, s));
+  EMU_CUDA(table_alloc((void**)&tb.bmap, 4 * gnt * wpr, s));
+  EMU_CUDA(table_alloc((void**)&tb.wpre, 4 * gnt * wpr, s));
+  EMU_CUDA(table_alloc((void**)&tb.rowbase, 4 * (gnt + 1), s));
   EMU_CUDA(cudaMemcpyAsync(tb.bsat, B.data(), 4 * cells, cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMemcpyAsync(tb.ssat, S.data(), 4 * cells, cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMemcpyAsync(tb.bmap, bm.data(), 4 * gnt * wpr, cudaMemcpyHostToDevice, s));
@@ -320,8 +328,8 @@ int build_search_index_dev(TableBuf& tb, cudaStream_t s) {
   const int64_t span_t = (int64_t)tb.tt_hi - tb.tt_lo, span_c = (int64_t)tb.c_hi - tb.c_lo;
   tb.lt = std::min<int64_t>(span_t + 1, kMaxSqTable);
   tb.lc = std::min<int64_t>(span_c + 1, kMaxSqTable);
-  EMU_CUDA(cudaMalloc((void**)&tb.sq_t, 8 * tb.lt));
-  EMU_CUDA(cudaMalloc((void**)&tb.sq_c, 8 * tb.lc));
+  EMU_CUDA(table_alloc((void**)&tb.sq_t, 8 * tb.lt, s));
+  EMU_CUDA(table_alloc((void**)&tb.sq_c, 8 * tb.lc, s));
   EMU_LAUNCH("index", s, k_sq_table<<<(unsigned)std::min<int64_t>(1024, (tb.lt + 255) / 256), 256, 0, s>>>(tb.sq_t, tb.lt, span_t));
   EMU_LAUNCH("index", s, k_sq_table<<<(unsigned)std::min<int64_t>(1024, (tb.lc + 255) / 256), 256, 0, s>>>(tb.sq_c, tb.lc, span_c));
   EMU_CUDA(cudaGetLastError());
@@ -333,14 +341,14 @@ int build_search_index_dev(TableBuf& tb, cudaStream_t s) {
   const int64_t st = gnc + 1, rows = gnt + 1, cells = rows * st, wpr = (gnc + 31) / 32;
   // column scan in chunks of rows: short per-thread chains, at most 512 chunks
   const int64_t chunk = std::max<int64_t>(16, (rows + 511) / 512), nch = (rows + chunk - 1) / chunk;
-  EMU_CUDA(cudaMalloc((void**)&tb.bsat, 4 * cells));
-  EMU_CUDA(cudaMalloc((void**)&tb.ssat, 4 * cells));
-  EMU_CUDA(cudaMalloc((void**)&tb.bmap, 4 * gnt * wpr));
-  EMU_CUDA(cudaMalloc((void**)&tb.wpre, 4 * gnt * wpr));
-  EMU_CUDA(cudaMalloc((void**)&tb.rowbase, 4 * (gnt + 1)));
-  EMU_CUDA(cudaMalloc((void**)&tb.col_start, 4 * (gnc + 1)));
-  EMU_CUDA(cudaMalloc((void**)&tb.col_tt, 4 * std::max<int64_t>(1, tb.nb)));
-  EMU_CUDA(cudaMalloc((void**)&tb.col_b, 4 * std::max<int64_t>(1, tb.nb)));
+  EMU_CUDA(table_alloc((void**)&tb.bsat, 4 * cells, s));
+  EMU_CUDA(table_alloc((void**)&tb.ssat, 4 * cells, s));
+  EMU_CUDA(table_alloc((void**)&tb.bmap, 4 * gnt * wpr, s));
+  EMU_CUDA(table_alloc((void**)&tb.wpre, 4 * gnt * wpr, s));
+  EMU_CUDA(table_alloc((void**)&tb.rowbase, 4 * (gnt + 1), s));
+  EMU_CUDA(table_alloc((void**)&tb.col_start, 4 * (gnc + 1), s));
+  EMU_CUDA(table_alloc((void**)&tb.col_tt, 4 * std::max<int64_t>(1, tb.nb), s));
+  EMU_CUDA(table_alloc((void**)&tb.col_b, 4 * std::max<int64_t>(1, tb.nb), s));
   int32_t* part = nullptr;
   EMU_CUDA(cudaMallocAsync((void**)&part, 8 * (size_t)nch * st, s));
   EMU_CUDA(cudaMemsetAsync(tb.bsat, 0, 4 * cells, s));
@@ -377,8 +385,7 @@ bool index_on_host() {
 template <typename T>
 static int dev_alloc(T** p, int64_t n) {
   *p = nullptr;
-  size_t bytes = sizeof(T) * (size_t)(n > 0 ? n : 1);
-  EMU_CUDA(cudaMalloc((void**)p, bytes));
+  EMU_CUDA(table_alloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), 0));
   return EMU_OK;
 }
 

@@ -30,6 +30,9 @@ struct TableBuf {
   DevTable view() const;
 };
 
+// Every TableBuf array is allocated here (stream-ordered pool) and freed by release().
+cudaError_t table_alloc(void** p, size_t bytes, cudaStream_t s);
+
 // Build the search index (summed-area tables + squared-delta tables) from
 // host copies of the bucket keys/offsets (construction time, not per query).
 int build_search_index(TableBuf& tb, const int32_t* h_tt, const int32_t* h_cc, const int64_t* h_off, cudaStream_t s);
