@@ -93,3 +93,22 @@ def test_c3_pools_match_reference(c3, c3_golden, floor):
     off, bkt, dist, prob, cdf, tid = orc.pools(g["key_tt"], g["key_conc"], g["key_phase"])
     assert np.array_equal(pool_digests(off, bkt, dist, prob, tid, soas), g[f"m{floor}_digest"])
     check_full_pools(off, bkt, dist, prob, tid, soas, g, f"m{floor}_")
+
+
+def test_c4_100m_build_matches_oracle():
+    """Config 4 at full size: the 100M-record canonical 3-table build (records
+    from the device generator G, the bench_configs c4 input) against the CPU
+    restatement of build_pack + save_pack's order, table by table (digest of
+    keys, offsets and samples)."""
+    from paper_2605_00616_b200.capture import records_device
+    from paper_2605_00616_b200.device import DeviceTables
+
+    dev = records_device(100_000_000, seed=100)
+    got = DeviceTables.build(*dev, canonical=True).to_host()
+    rec = [d.cpu().numpy() for d in dev]
+    del dev
+    torch.cuda.empty_cache()
+    want = O.build(*rec, canonical=True)
+    for g, w in zip(got, want):
+        assert len(g.tt) == len(w.tt) and len(g.samples) == len(w.samples) == int(w.off[-1])
+        assert soa_digest(g.tt, g.conc, g.off, g.samples) == soa_digest(w.tt, w.conc, w.off, w.samples)
