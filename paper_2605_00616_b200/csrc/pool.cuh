@@ -818,17 +818,20 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
   // radii of step 3b while the candidate's bucket is at hand.
   const bool pivots = NT > 32 && dmax < 1e300;
   double pv[8];
-  unsigned long long pacc[8];
+  unsigned pacc[8];
 #pragma unroll
   for (int l = 0; l < 8; l++) {
     pv[l] = r1 * (1.0 + 0.41421356237309515 * (double)(l + 1) * 0.125);
     pacc[l] = 0;
   }
+  // (each candidate counts at most min(floor, 2^20) samples: the per-thread and
+  // per-warp sums stay in 32 bits; a capped count can only make a pivot look
+  // short of the floor, never the reverse)
   auto pivot_count = [&](bool in, double d, int32_t bb) {
     if (!pivots || !in) return;
-    const unsigned long long cn = (unsigned long long)min((int64_t)(T.bkt_off[bb + 1] - T.bkt_off[bb]), mfloor);
+    const unsigned cn = (unsigned)min(min((int64_t)(T.bkt_off[bb + 1] - T.bkt_off[bb]), mfloor), (int64_t)1 << 20);
 #pragma unroll
-    for (int l = 0; l < 8; l++) pacc[l] += d <= pv[l] ? cn : 0ULL;
+    for (int l = 0; l < 8; l++) pacc[l] += d <= pv[l] ? cn : 0u;
   };
   int pos = 0;
   int* acnt = reinterpret_cast<int*>(ws.scr + 32);  // group tiers: append counter
@@ -950,10 +953,8 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
     G::sync();
 #pragma unroll
     for (int l = 0; l < 8; l++) {
-      unsigned long long v = pacc[l];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-      if ((G::rank() & 31) == 0 && v) atomicAdd(&cnt[l], v);
+      const unsigned v = __reduce_add_sync(kFull, pacc[l]);
+      if ((G::rank() & 31) == 0 && v) atomicAdd(&cnt[l], (unsigned long long)v);
     }
     G::sync();
     int l = 0;
@@ -961,8 +962,11 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
     const bool use = cnt[l] >= (unsigned long long)mfloor;
     const double piv = r1 * (1.0 + 0.41421356237309515 * (double)(l + 1) * 0.125);
     G::sync();
-    if (use) {
-      int out = 0;
+    if (use) {  // compact in place, appending with one shared atomic per warp (the sort imposes the order)
+      int* ocnt = reinterpret_cast<int*>(ws.scr + 32);
+      if (G::rank() == 0) *ocnt = 0;
+      G::sync();
+      const int lane = G::rank() & 31;
       for (int base = 0; base < pos; base += NT) {
         const int i = base + G::rank();
         double d = 0.0;
@@ -973,16 +977,20 @@ __device__ int64_t pool_search_sat(const DevTable& T, int32_t t, int32_t c, int6
           bb = ws.b[i];
           keep = d <= piv;
         }
-        long long kt;
-        const int ex = (int)G::excl_scan(keep ? 1 : 0, kt, ws.scr);
+        G::sync();  // this round is read before any of it is overwritten (writes stay below base + NT)
+        const unsigned m = __ballot_sync(kFull, keep);
+        int o = 0;
+        if (lane == 0 && m) o = atomicAdd(ocnt, __popc(m));
+        o = __shfl_sync(kFull, o, 0);
         if (keep) {
-          ws.d[out + ex] = d;
-          ws.b[out + ex] = bb;
+          const int q = o + __popc(m & ((1u << lane) - 1u));
+          ws.d[q] = d;
+          ws.b[q] = bb;
         }
-        out += (int)kt;
       }
       G::sync();
-      pos = out;
+      pos = *ocnt;
+      G::sync();
     }
   }
   EMU_PHASE(3);
