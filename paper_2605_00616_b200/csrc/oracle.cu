@@ -47,11 +47,15 @@ constexpr int kCtaSmem = kCtaCap * 12;
 constexpr int kCtaCache = 1024;  // cached counts/offsets per CTA workspace
 constexpr int kGrpThreads = 128;  // middle tier: one 4-warp group per key
 #ifndef EMU_GRP_CAP
-#define EMU_GRP_CAP 2048
+#define EMU_GRP_CAP 1024
 #endif
 #ifndef EMU_GRP_CACHE
-#define EMU_GRP_CACHE 1024
+#define EMU_GRP_CACHE 512
 #endif
+// Group workspace: 1024 candidates (12 KB) + 512 cached counts/offsets keep a
+// group CTA at ~18 KB of shared memory, so the 64-register limit (8 groups per
+// SM) binds instead of shared memory (6 per SM at 2048 / 1024: C3 M=256 45.4 ->
+// 37.9 ms); the rare larger windows go to the CTA tier.
 constexpr int kGrpCap = EMU_GRP_CAP;      // candidates per group workspace (bigger windows: CTA tier)
 constexpr int kGrpCache = EMU_GRP_CACHE;  // cached counts/offsets per group
 constexpr int kGrpSmem = kGrpCap * 12;
