@@ -443,9 +443,8 @@ def run_b200(args):
             _lib.profile_enable(True)
             for _ in range(reps):
                 fn()
-            out = {}
-            for name in names:
-                t, n = _lib.profile_read(name)
+            out = {name: {"ms_per_step": 0.0, "launches_per_step": 0.0} for name in names}
+            for name, (t, n) in _lib.profile_all().items():
                 out[name] = {"ms_per_step": t / reps, "launches_per_step": n / reps}
             _lib.profile_enable(False)
             return out

@@ -85,6 +85,9 @@ struct BatchCtl {
   int tile_total;  // tile tier: keys binned
   int fb_n;        // keys handed from the tile tier to the warp tier
   int fb_work;
+  int dense_n;     // cold path: keys from the bitmap, in (phase, conc, tt) order
+  int dense_n0;    // ... of which phase 0
+  int hash_n;      // cold path: keys outside the dense map (side list)
 };
 
 struct Keys {
@@ -358,6 +361,115 @@ __global__ void k_mark(MapView m, const int32_t* __restrict__ qt, const int32_t*
   }
 }
 
+// Cold batches (an empty cache): dedupe by a bitmap over the dense key domain
+// instead of claiming map entries.  Bit (phase, conc, tt) of every query is set
+// with a fire-and-forget atomic (one per distinct key per warp); a scan of the
+// bitmap then lists the batch's keys in (phase, conc, tt) order -- the tile
+// tier's neighbour order, so no binning pass is needed -- and clears it.  Keys
+// outside the dense map take k_mark's claim path into a side list.
+__device__ __forceinline__ int64_t bit_plane_stride(const MapView& m) {
+  return (((int64_t)m.dom_tt * m.dom_conc) + 31) & ~(int64_t)31;
+}
+__global__ void k_mark_bits(MapView m, const int32_t* __restrict__ qt, const int32_t* __restrict__ qc,
+                            const uint8_t* __restrict__ qp, int64_t Q, unsigned int* bits, int32_t* hk_tt,
+                            int32_t* hk_c, uint8_t* hk_p, int64_t* hk_e, BatchCtl* ctl) {
+  // k_mark's claim (an L2 hint load skips claimed entries; one CAS per distinct
+  // key per warp), but a winner only sets its key's bit: no append counter, no
+  // block barrier; the key list comes from the bitmap scan, in tile order
+  const int lane = threadIdx.x & 31;
+  const int64_t ps = bit_plane_stride(m);
+  for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < Q; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;  // warp-uniform trip count (match_any below)
+    const bool v = i < Q;
+    int ph = 0;
+    int32_t t = 0, c = 0;
+    if (v) {
+      ph = qp[i] ? 1 : 0;  // kept in L2: k_sample re-reads the keys next
+      t = qt[i];
+      c = qc[i];
+    }
+    const int64_t idx = v ? map_find<true>(m, ph, t, c) : -2;
+    const long long cur = idx >= 0 ? __ldcg(map_entry_ptr(m, idx)) : -1;  // a hint only (the CAS decides)
+    if (idx == -1) atomicOr(&ctl->flags, FLAG_HASH);
+    const bool cand = idx >= 0 && cur == kEntryEmpty;
+    if (!__any_sync(kFull, cand)) continue;
+    const unsigned peers =
+        __match_any_sync(kFull, cand ? (unsigned long long)idx : (0xffffffff00000000ULL | (unsigned)lane));
+    if (!cand || (__ffs(peers) - 1) != lane) continue;
+    if (atomicCAS((unsigned long long*)map_entry_ptr(m, idx), 0ULL, (unsigned long long)kEntryPending) != 0ULL)
+      continue;
+    if (idx < map_dense_size(m)) {
+      const uint64_t bit = (uint64_t)ph * ps + (uint64_t)(c - 1) * m.dom_tt + (uint64_t)(t - 1);
+      atomicOr(&bits[bit >> 5], 1u << (bit & 31));
+    } else {  // rare: keys outside the dense map
+      const int pos = atomicAdd(&ctl->hash_n, 1);
+      hk_tt[pos] = t;
+      hk_c[pos] = c;
+      hk_p[pos] = (uint8_t)ph;
+      hk_e[pos] = idx;
+    }
+  }
+}
+
+// Bitmap -> key list in bit order: per-block popcount totals, a scan of those,
+// then one word per thread emits its set bits (block scan for its offset) and
+// clears the word for the next batch.
+constexpr int kBitThreads = 256;
+__global__ void __launch_bounds__(kBitThreads) k_bits_count(const unsigned int* __restrict__ w, int64_t nwords,
+                                                           unsigned int* blk_tot) {
+  __shared__ unsigned int sm[33];
+  const int64_t i = (int64_t)blockIdx.x * kBitThreads + threadIdx.x;
+  unsigned int tot;
+  block_excl_scan<unsigned int>(i < nwords ? (unsigned)__popc(w[i]) : 0u, tot, sm);
+  if (threadIdx.x == 0) blk_tot[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(kBitThreads) k_bits_emit(unsigned int* __restrict__ w, int64_t nwords,
+                                                          int64_t plane_words, const unsigned int* __restrict__ blk_off,
+                                                          MapView m, int32_t* nk_tt, int32_t* nk_c, uint8_t* nk_p,
+                                                          int64_t* nk_e, int* n0) {
+  __shared__ unsigned int sm[33];
+  const int64_t i = (int64_t)blockIdx.x * kBitThreads + threadIdx.x;
+  unsigned int word = i < nwords ? w[i] : 0u;
+  unsigned int tot;
+  unsigned int ex = blk_off[blockIdx.x] + block_excl_scan<unsigned int>((unsigned)__popc(word), tot, sm);
+  if (i == plane_words) *n0 = (int)ex;
+  if (!word) return;
+  w[i] = 0u;
+  const int64_t ps = plane_words * 32;
+  while (word) {
+    const int b = __ffs(word) - 1;
+    word &= word - 1u;
+    const int64_t bit = i * 32 + b;
+    const int ph = bit >= ps ? 1 : 0;
+    const uint32_t r = (uint32_t)(bit - (int64_t)ph * ps);  // < dom_tt * dom_conc < 2^27: 32-bit division
+    const uint32_t c0 = r / (uint32_t)m.dom_tt, t0 = r - c0 * (uint32_t)m.dom_tt;
+    nk_tt[ex] = t0 + 1;
+    nk_c[ex] = c0 + 1;
+    nk_p[ex] = (uint8_t)ph;
+    nk_e[ex] = ((int64_t)ph * m.dom_tt + t0) * m.dom_conc + c0;  // map_find's dense index
+    ex++;
+  }
+}
+
+// After the bitmap scan: the side-list keys follow the dense ones (straight to
+// the warp tier; they are outside every tile) and new_count covers both.
+__global__ void k_append_hash(const int32_t* hk_tt, const int32_t* hk_c, const uint8_t* hk_p, const int64_t* hk_e,
+                              int32_t* nk_tt, int32_t* nk_c, uint8_t* nk_p, int64_t* nk_e, BatchCtl* ctl,
+                              int* fb_list) {
+  const int n = ctl->dense_n, nh = ctl->hash_n;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nh; k += gridDim.x * blockDim.x) {
+    nk_tt[n + k] = hk_tt[k];
+    nk_c[n + k] = hk_c[k];
+    nk_p[n + k] = hk_p[k];
+    nk_e[n + k] = hk_e[k];
+    fb_list[k] = n + k;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->new_count = n + nh;
+    ctl->fb_n = nh;
+  }
+}
+
 // Warp per new key: precomputed candidates -> register sort -> prefix ->
 // Shepard CDF; keys without a fast-path window run the full in-warp search,
 // and windows too large for a warp are escalated to k_pool_cta.
@@ -421,11 +533,16 @@ template <int MODE>
 __global__ void __launch_bounds__(kTileThreads, EMU_TILE_MINB)
     k_pool_tile(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk, TileIdx ti, const KeyWin* __restrict__ kw,
                 const long long* __restrict__ resv, const int* __restrict__ order, const int* __restrict__ off,
-                const int* __restrict__ total, int* work, int* fb_list, int* fb_n) {
+                const int* __restrict__ total, const int* __restrict__ dense_n0, int* work, int* fb_list,
+                int* fb_n) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   TileWarp& tw = reinterpret_cast<TileWarp*>(smem)[threadIdx.x >> 5];
-  const int n0 = ti.base[1] < ti.nb ? off[ti.base[1]] : *total;
+  // binned (order != nullptr): keys counting-sorted into tile bins by k_tile_bin;
+  // dense: the first *total keys come straight from the cold path's bitmap scan,
+  // already in (phase, conc, tt) order, not yet checked for tile eligibility
+  const bool dense = order == nullptr;
+  const int n0 = dense ? *dense_n0 : ti.base[1] < ti.nb ? off[ti.base[1]] : *total;
   const int p1 = (n0 + 31) & ~31;
   const int nslots = p1 + (*total - n0);
   const int nch = (nslots + 31) >> 5;
@@ -437,7 +554,8 @@ __global__ void __launch_bounds__(kTileThreads, EMU_TILE_MINB)
     const int pos = ch * 32 + lane;
     const int ph = ch * 32 >= p1 ? 1 : 0;  // a tile never straddles the planes
     const DevTable& T = ph ? P1 : P0;
-    const int w = (pos < nslots && (pos < n0 || pos >= p1)) ? order[pos] : -1;
+    int w = -1;
+    if (pos < nslots && (pos < n0 || pos >= p1)) w = dense ? (pos < n0 ? pos : n0 + (pos - p1)) : order[pos];
     EMU_DCHECK(w < (keys.count_dev ? *keys.count_dev : keys.count), "CHECK tile w=%d pos=%d n0=%d p1=%d nslots=%d\n", w,
                pos, n0, p1, nslots);
     KeyWin k;
@@ -447,6 +565,18 @@ __global__ void __launch_bounds__(kTileThreads, EMU_TILE_MINB)
       k = kw[w];
       t = keys.tt[w];
       c = keys.conc[w];
+    }
+    if (dense) {  // k_tile_bin's test: ineligible keys leave the tile -- to the warp tier, except big
+                  // windows (already on the group tier's list) and keys whose arena reservation failed
+                  // in prep (left pending for the host's flush-and-retry)
+      bool out = false, fb = false;
+      if (w >= 0) {
+        const bool pend = MODE == 0 && resv[w] == -2;
+        out = pend || tile_bin(T, ti, ph, t, c, k, cfg.floor) < 0;
+        fb = out && !pend && !(k.flags & kWinBig);
+      }
+      warp_push(fb_list, fb_n, fb, w);
+      if (out) w = -1;
     }
     const bool has = w >= 0 && k.i0 <= k.i1 && k.j0 <= k.j1;
     const int i0 = __reduce_min_sync(kFull, has ? k.i0 : 0x7fffffff), i1 = __reduce_max_sync(kFull, has ? k.i1 : -1);
@@ -1310,6 +1440,15 @@ struct emu_oracle_s {
   int* krank = nullptr;
   int* order = nullptr;
   int* fb_list = nullptr;
+  // cold-path dedupe bitmap over the dense key domain (self-clearing) and the
+  // side list of keys outside it
+  unsigned int* bits = nullptr;
+  int64_t bits_words = 0;
+  unsigned int* bits_part = nullptr;
+  int32_t* hk_tt = nullptr;
+  int32_t* hk_c = nullptr;
+  uint8_t* hk_p = nullptr;
+  int64_t* hk_e = nullptr;
   // CTA global scratch
   double* gd = nullptr;
   int32_t* gb = nullptr;
@@ -1534,7 +1673,15 @@ int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, doubl
 }
 
 void emu_oracle_destroy(emu_oracle_t o) {
-  if (o) cudaFree(o->miss);
+  if (o) {
+    cudaFree(o->miss);
+    cudaFree(o->bits);
+    cudaFree(o->bits_part);
+    cudaFree(o->hk_tt);
+    cudaFree(o->hk_c);
+    cudaFree(o->hk_p);
+    cudaFree(o->hk_e);
+  }
   if (!o) return;
   cudaFree(o->map.dense);
   cudaFree(o->map.hkeys);
@@ -1618,6 +1765,14 @@ static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
   cudaFree(o->krank);
   cudaFree(o->order);
   cudaFree(o->fb_list);
+  cudaFree(o->hk_tt);
+  cudaFree(o->hk_c);
+  cudaFree(o->hk_p);
+  cudaFree(o->hk_e);
+  o->hk_tt = nullptr;
+  o->hk_c = nullptr;
+  o->hk_p = nullptr;
+  o->hk_e = nullptr;
   o->kbin = o->krank = o->order = o->fb_list = nullptr;
   o->nk_tt = nullptr;
   o->nk_c = nullptr;
@@ -1632,7 +1787,9 @@ static int ensure_key_capacity(emu_oracle_t o, int64_t n_keys) {
   if ((rc = dalloc(&o->nk_tt, need)) || (rc = dalloc(&o->nk_c, need)) || (rc = dalloc(&o->nk_p, need)) ||
       (rc = dalloc(&o->nk_e, need)) || (rc = dalloc(&o->esc, need)) || (rc = dalloc(&o->esc2, need)) ||
       (rc = dalloc(&o->kw, need)) || (rc = dalloc(&o->resv, need)) || (rc = dalloc(&o->kbin, need)) ||
-      (rc = dalloc(&o->krank, need)) || (rc = dalloc(&o->order, need + 64)) || (rc = dalloc(&o->fb_list, need)))
+      (rc = dalloc(&o->krank, need)) || (rc = dalloc(&o->order, need + 64)) || (rc = dalloc(&o->fb_list, need)) ||
+      (rc = dalloc(&o->hk_tt, need)) || (rc = dalloc(&o->hk_c, need)) || (rc = dalloc(&o->hk_p, need)) ||
+      (rc = dalloc(&o->hk_e, need)))
     return rc;
   o->nk_cap = need;
   return EMU_OK;
@@ -1665,7 +1822,8 @@ struct OffOut {
 // tt) bins, warp per 32 keys, lane per key) -> warp tier for the keys the tile
 // tier handed over (or all keys) -> group tier -> CTA tier.
 template <int MODE>
-static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, cudaStream_t s, bool sync_check) {
+static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, cudaStream_t s, bool sync_check,
+                             bool dense_keys = false) {
   static const bool tile_debug = getenv("EMU_TILE_DEBUG") != nullptr;
   auto chk = [&](const char* what) -> int {
     EMU_CUDA(cudaGetLastError());
@@ -1689,7 +1847,13 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
   const int* list = o->fb_list;  // the warp tier's keys: from prep, or handed over by the tile tier
   const int* list_n = &o->ctl->fb_n;
   int* warp_work = &o->ctl->fb_work;
-  if (o->tile_on) {
+  if (o->tile_on && dense_keys) {  // cold path: keys already in tile order (build_missing_cold)
+    EMU_LAUNCH("pool_tile", s, k_pool_tile<MODE><<<kNumSMs * EMU_TILE_MINB, kTileThreads, kTileBytes, s>>>(
+                                   o->plane[0], o->plane[1], keys, o->cfg, sk, o->ti, o->kw, o->resv, nullptr,
+                                   nullptr, &o->ctl->dense_n, &o->ctl->dense_n0, &o->ctl->tile_work, o->fb_list,
+                                   &o->ctl->fb_n));
+    if ((rc = chk("pool_tile"))) return rc;
+  } else if (o->tile_on) {
     EMU_CUDA(cudaMemsetAsync(o->tile_cnt, 0, sizeof(int) * o->ti.nb, s));
     EMU_LAUNCH("tile_bin", s, k_tile_bin<MODE><<<kPrepGrid, 256, 0, s>>>(o->plane[0], o->plane[1], keys, o->cfg, o->ti,
                                                                           o->kw, o->resv, o->tile_cnt, o->kbin, o->krank,
@@ -1715,7 +1879,8 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
     }
     EMU_LAUNCH("pool_tile", s, k_pool_tile<MODE><<<kNumSMs * EMU_TILE_MINB, kTileThreads, kTileBytes, s>>>(
                                    o->plane[0], o->plane[1], keys, o->cfg, sk, o->ti, o->kw, o->resv, o->order,
-                                   o->tile_off, &o->ctl->tile_total, &o->ctl->tile_work, o->fb_list, &o->ctl->fb_n));
+                                   o->tile_off, &o->ctl->tile_total, nullptr, &o->ctl->tile_work, o->fb_list,
+                                   &o->ctl->fb_n));
     if ((rc = chk("pool_tile"))) return rc;
   }
   EMU_LAUNCH("pool_warp", s, k_pool_warp<MODE><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
@@ -1788,6 +1953,51 @@ static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, c
             c.new_count, c.tile_total, o->tile_on ? c.fb_n : c.new_count, c.esc_count, c.esc2_count);
   }
   return rc;
+}
+
+// Cold batch (the cache was just flushed): k_mark_bits -> bitmap scan (keys in
+// tile order) -> side-list keys appended -> the pool tiers with the tile tier
+// reading the keys in place (no k_tile_bin / scan / scatter).  Falls back to
+// build_missing without the tile tier.
+static int build_missing_cold(emu_oracle_t o, const int32_t* qt, const int32_t* qc, const uint8_t* qp, int64_t Q,
+                              cudaStream_t s) {
+  static const bool off = [] {
+    const char* v = getenv("EMU_COLD_BITMAP");
+    return v && v[0] == '0';
+  }();
+  if (!o->tile_on || off) return build_missing(o, qt, qc, qp, Q, s);
+  int rc = ensure_key_capacity(o, std::min<int64_t>(Q, map_entries(o)));
+  if (rc) return rc;
+  const int64_t ps = ((int64_t)o->map.dom_tt * o->map.dom_conc + 31) & ~(int64_t)31;
+  const int64_t words = 2 * ps / 32;
+  if (words != o->bits_words) {
+    cudaFree(o->bits);
+    cudaFree(o->bits_part);
+    o->bits = nullptr;
+    o->bits_part = nullptr;
+    o->bits_words = 0;
+    if ((rc = dalloc(&o->bits, words)) || (rc = dalloc(&o->bits_part, (words + kBitThreads - 1) / kBitThreads + 1)))
+      return rc;
+    EMU_CUDA(cudaMemsetAsync(o->bits, 0, 4 * words, s));
+    o->bits_words = words;
+  }
+  o->cold = false;
+  EMU_CUDA(reset_counters(o, s));
+  EMU_LAUNCH("mark", s, k_mark_bits<<<grid_for(Q, 256, kNumSMs * 8), 256, 0, s>>>(o->map, qt, qc, qp, Q, o->bits,
+                                                                                  o->hk_tt, o->hk_c, o->hk_p,
+                                                                                  o->hk_e, o->ctl));
+  const int64_t nblk = (words + kBitThreads - 1) / kBitThreads;
+  EMU_LAUNCH("bits", s, k_bits_count<<<(unsigned)nblk, kBitThreads, 0, s>>>(o->bits, words, o->bits_part));
+  EMU_LAUNCH("bits", s, k_scan_partials<unsigned int><<<1, 1024, 0, s>>>(
+                            o->bits_part, nblk, reinterpret_cast<unsigned int*>(&o->ctl->dense_n)));
+  EMU_LAUNCH("bits", s, k_bits_emit<<<(unsigned)nblk, kBitThreads, 0, s>>>(o->bits, words, ps / 32, o->bits_part,
+                                                                           o->map, o->nk_tt, o->nk_c, o->nk_p,
+                                                                           o->nk_e, &o->ctl->dense_n0));
+  EMU_LAUNCH("append_hash", s, k_append_hash<<<kNumSMs, 256, 0, s>>>(o->hk_tt, o->hk_c, o->hk_p, o->hk_e, o->nk_tt,
+                                                                     o->nk_c, o->nk_p, o->nk_e, o->ctl, o->fb_list));
+  EMU_CUDA(cudaGetLastError());
+  Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
+  return launch_pool_tiers<0>(o, keys, make_sink(o), s, false, true);
 }
 
 static int read_flags(emu_oracle_t o, cudaStream_t s, int* flags) {
@@ -1939,7 +2149,7 @@ static int draw_chunk(emu_oracle_t o, int rng_mode, const int32_t* qt, const int
     o->miss_cap = pow2_at_least(m);
   }
   if (head > 0) {
-    if ((rc = build_missing(o, qt, qc, qp, head, s))) return rc;
+    if ((rc = build_missing_cold(o, qt, qc, qp, head, s))) return rc;
     if ((rc = launch_sample(o, rng_mode, qt, qc, qp, head, us, ui, seed, ctr, lat, sidx, s))) return rc;
   }
   if (m <= 0) return EMU_OK;

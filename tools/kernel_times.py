@@ -33,8 +33,6 @@ for _ in range(sweeps):
 e1.record()
 torch.cuda.synchronize()
 out = {"step_ms": e0.elapsed_time(e1) / sweeps}
-for k in ("flush", "mark", "pool_prep", "tile_bin", "scan", "tile_scatter", "pool_tile", "pool_warp", "pool_grp",
-          "pool_cta", "sample", "sweep", "sample_list"):
-    ms, n = _lib.profile_read(k)
-    out[k] = round(ms / max(n, 1), 4)
+for k, (ms, n) in sorted(_lib.profile_all().items()):
+    out[k] = round(ms / sweeps, 4)
 print(os.environ.get("TAG", ""), out, flush=True)
