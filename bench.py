@@ -37,6 +37,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_QUERY = {"explicit": 41, "philox": 29}
+# library profiling name -> kernel (profiles/ncu_summary.json key) of the query-stream passes
+STREAM_KERNELS = {"mark": "k_mark_bits", "sample": "k_sample", "sweep": "k_sweep", "sample_list": "k_sample_list"}
 WORKLOAD = ("C2: 10M-query batched oracle sweep over a 1M-record Llama-3.1-8B-shaped profile table "
             "(synthetic generator G, M=32, p=2, eps=1e-9), cold pool cache per step")
 
@@ -461,7 +463,7 @@ def run_b200(args):
         line["roofline"] = {"bound": "hbm", "kernel": "k_mark + k_sample + k_sweep + k_sample_list (query stream)",
                             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                             "frac": achieved / peak,
-                            "traffic": sum((ncu_metric("k_" + k) or 0.0) for k in stream) or None,
+                            "traffic": sum((ncu_metric(STREAM_KERNELS[k]) or 0.0) for k in stream) or None,
                             "bytes_per_query": bpq,
                             "share_of_step": t_stream * 1e3 / max(step_ms, 1e-9),
                             "kernels_ms_per_step": {k: round(v["ms_per_step"], 4) for k, v in kern.items()},

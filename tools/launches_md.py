@@ -22,7 +22,7 @@ print("| kernel | launches | total us | us/launch |\n|---|---|---|---|")
 for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     print(f"| {k} | {n} | {t:.1f} | {t / n:.1f} |")
 sweep = {k: v for k, v in agg.items()
-         if any(s in k for s in ("k_mark", "k_pool", "k_tile", "k_sample", "k_fill_u64", "k_scan_i32", "k_sweep"))}
+         if any(s in k for s in ("k_mark", "k_bits", "k_append_hash", "k_pool", "k_tile", "k_sample", "k_fill_u64", "k_sweep"))}
 tot = sum(t for _, t in sweep.values()) or 1
 print("\nShare of the sweep kernels (serialised, cold-cache times):\n")
 for k, (n, t) in sorted(sweep.items(), key=lambda kv: -kv[1][1]):
