@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(kTileThreads, EMU_TILE_MINB)
           }
           if (start >= 0) {
             const PoolPtrs pp = pool_ptrs(sk.arena, start, K);
-            tile_finish<0>(T, t, c, K, cfg, tw, &pp, nullptr, nullptr, nullptr, nullptr);
+            tile_finish<0>(T, K, cfg, tw, &pp, nullptr, nullptr, nullptr, nullptr);
             *ep = make_entry(K, start);
           }
         }
@@ -633,8 +633,7 @@ __global__ void __launch_bounds__(kTileThreads, EMU_TILE_MINB)
         if (K > sk.kmax) {
           sk.x_K[w] = K + (int64_t)1000000;
         } else {
-          tile_finish<1>(T, t, c, K, cfg, tw, nullptr, sk.x_bkt + base, sk.x_dist + base, sk.x_prob + base,
-                         sk.x_cdf + base);
+          tile_finish<1>(T, K, cfg, tw, nullptr, sk.x_bkt + base, sk.x_dist + base, sk.x_prob + base, sk.x_cdf + base);
           sk.x_K[w] = K;
         }
       }

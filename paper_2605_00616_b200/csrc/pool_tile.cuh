@@ -43,22 +43,17 @@ constexpr int kTileRowShift = 4;  // ordering bins: 16 grid rows of one conc col
 constexpr int kTileMaxFloor = 32;
 constexpr int kTileRowPath = 512; // union boxes up to this many grid rows enumerate by rows
 #ifndef EMU_TILE_MINB
-#define EMU_TILE_MINB 9
+#define EMU_TILE_MINB 6
 #endif
 
-// Per warp 12 KB: the lane lists keep each exact distance rounded to FLOAT
-// (round-to-nearest is monotone, so a float order never contradicts the exact
-// one; float ties are settled by recomputing the exact doubles) and the finish
-// recomputes the K exact distances it needs.  Halving the list (was 8 B per
-// entry, 17.6 KB per warp) lets 18 warps share an SM instead of 12.
 struct TileWarp {
   int4 u[kTileU];             // union candidates in BUCKET order: (tt, conc, count, bucket)
-  float d[kTileL * 32];       // per-lane list: float(exact d) of entry e of lane l at [e * 32 + l] (union staging)
+  double d[kTileL * 32];      // per-lane list, entry e of lane l at [e * 32 + l] (staging for the union sort)
   uint8_t j[kTileL * 32];     // union index of that entry (= bucket order: ties in d break on it)
   uint8_t perm[kTileL * 32];  // sorted order: the e-th smallest entry of lane l is perm[e * 32 + l]
   uint8_t h[32 * 32];         // per lane: distance-bin counts (32 bins, <= kTileL each), then bin starts
 };
-static_assert(kTileL * 32 * 4 >= kTileU * 16, "the union staging area lives in TileWarp::d");
+static_assert(kTileL * 32 * 8 >= kTileU * 16, "the union staging area lives in TileWarp::d");
 constexpr int kTileBytes = (int)sizeof(TileWarp) * kTileWarps;
 
 // Ordering bins of the tile tier (per plane: gnc columns x ceil(gnt / 16) row blocks).
@@ -264,13 +259,6 @@ __device__ __forceinline__ int tile_enum_union(const DevTable& T, int32_t i0, in
   return tot;
 }
 
-// Exact distance (norm_dist's IEEE ops via the squared-delta tables) from the
-// key to union entry q.
-__device__ __forceinline__ double tile_dist(const DevTable& T, int32_t t, int32_t c, const int4& q, int64_t span_t,
-                                            int64_t span_c) {
-  return dist_tab(T, (int64_t)t - q.x, (int64_t)c - q.y, span_t, span_c);
-}
-
 // Lane l of a warp handles key w (or none: w < 0).  Returns K >= 1 with the
 // lane's pool: sorted entry e (< K) is list slot tw.perm[e * 32 + lane]; or a
 // negative reason for the warp tier (-2 list overflow, -3 prefix, -4 window test).
@@ -375,17 +363,15 @@ __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t
     const double da = dist_tab(T, t - qa.x, c - qa.y, span_t, span_c);
     const double db = dist_tab(T, t - qb.x, c - qb.y, span_t, span_c);
     if (da <= piv) {
-      const float fa = __double2float_rn(da);
-      tw.d[m2 * 32 + lane] = fa;
+      tw.d[m2 * 32 + lane] = da;
       tw.j[m2 * 32 + lane] = (uint8_t)ja;
-      h[min(31, (int)((double)fa * scale)) * 32] += 1;
+      h[min(31, (int)(da * scale)) * 32] += 1;
       m2++;
     }
     if (two && db <= piv) {
-      const float fb = __double2float_rn(db);
-      tw.d[m2 * 32 + lane] = fb;
+      tw.d[m2 * 32 + lane] = db;
       tw.j[m2 * 32 + lane] = (uint8_t)jb;
-      h[min(31, (int)((double)fb * scale)) * 32] += 1;
+      h[min(31, (int)(db * scale)) * 32] += 1;
       m2++;
     }
   }
@@ -405,26 +391,19 @@ __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t
     }
   }
   for (int e = 0; e < m; e++) {
-    const int bn = min(31, (int)((double)tw.d[e * 32 + lane] * scale));
+    const int bn = min(31, (int)(tw.d[e * 32 + lane] * scale));
     const int p = h[bn * 32];
     h[bn * 32] = (uint8_t)(p + 1);
     tw.perm[p * 32 + lane] = (uint8_t)e;
   }
   for (int p = 1; p < m; p++) {
     const int x = tw.perm[p * 32 + lane];
-    const float fx = tw.d[x * 32 + lane];
-    const int jx = tw.j[x * 32 + lane];
+    const double dx = tw.d[x * 32 + lane];
     int q = p;
     while (q > 0) {
       const int y = tw.perm[(q - 1) * 32 + lane];
-      const float fy = tw.d[y * 32 + lane];
-      bool before = fx < fy;
-      if (fx == fy) {  // float tie: the exact distances decide, then the union (bucket) order
-        const int jy = tw.j[y * 32 + lane];
-        const double dx = tile_dist(T, t, c, tw.u[jx], span_t, span_c), dy = tile_dist(T, t, c, tw.u[jy], span_t, span_c);
-        before = dx < dy || (dx == dy && jx < jy);
-      }
-      if (!before) break;
+      const double dy = tw.d[y * 32 + lane];
+      if (!(dx < dy || (dx == dy && tw.j[x * 32 + lane] < tw.j[y * 32 + lane]))) break;
       tw.perm[q * 32 + lane] = (uint8_t)y;
       q--;
     }
@@ -449,96 +428,62 @@ __device__ __forceinline__ int tile_search(const DevTable& T, int32_t t, int32_t
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   const double et = cov_t ? kInf : dist_tab(T, k.Wt + 1, 0, span_t, span_c);
   const double ec = cov_c ? kInf : dist_tab(T, 0, k.Wc + 1, span_t, span_c);
-  const double dK = tile_dist(T, t, c, tw.u[tw.j[tw.perm[(K - 1) * 32 + lane] * 32 + lane]], span_t, span_c);
-  return dK < fmin(et, ec) ? K : -4;
+  return tw.d[tw.perm[(K - 1) * 32 + lane] * 32 + lane] < fmin(et, ec) ? K : -4;
 }
 
 // Shepard weights -> probabilities -> cdf of the lane's pool, pool_finish's
-// operation order (oracle.py:124-127, :133), without a double per entry in
-// shared memory: the masses are recomputed from the exact distances in each of
-// three passes -- numpy's pairwise sum (K <= 32: the 8-accumulator leaf,
-// streamed), the sequential cumsum of the probabilities (for its last value),
-// and the same cumsum again, now writing cdf = acc / last.  Writes cache slots
-// (MODE 0) or explicit outputs (MODE 1).
+// operation order; writes cache slots (MODE 0) or explicit outputs (MODE 1).
 template <int MODE>
-__device__ __forceinline__ void tile_finish(const DevTable& T, int32_t t, int32_t c, int K, const Cfg& cfg,
-                                            TileWarp& tw, const PoolPtrs* pp, int32_t* o_bkt, double* o_dist,
-                                            double* o_prob, double* o_cdf) {
+__device__ __forceinline__ void tile_finish(const DevTable& T, int K, const Cfg& cfg, TileWarp& tw, const PoolPtrs* pp,
+                                            int32_t* o_bkt, double* o_dist, double* o_prob, double* o_cdf) {
   const int lane = threadIdx.x & 31;
-  const int64_t span_t = (int64_t)T.tt_hi - T.tt_lo, span_c = (int64_t)T.c_hi - T.c_lo;
-  auto entry = [&](int e) -> const int4& { return tw.u[tw.j[tw.perm[e * 32 + lane] * 32 + lane]]; };
-  auto mass = [&](int e, double* dist) -> double {
-    const int4& q = entry(e);
-    const double d = tile_dist(T, t, c, q, span_t, span_c);
-    if (dist) *dist = d;
+  double* a = tw.d + lane;              // slot s of this lane at a[s * 32]
+  const uint8_t* pm = tw.perm + lane;   // e-th smallest -> slot pm[e * 32]
+  for (int e = 0; e < K; e++) {
+    const int sl = pm[e * 32];
+    const double d = a[sl * 32];
+    const int4 q = tw.u[tw.j[sl * 32 + lane]];
+    if (MODE == 1) {
+      o_bkt[e] = q.w;
+      o_dist[e] = d;
+    }
     const double x = d > cfg.eps ? d : cfg.eps;
-    return __dmul_rn(__ddiv_rn(1.0, shepard_pow(x, cfg.p)), (double)q.z);
-  };
-  // pass 1: S = numpy's pairwise sum of the masses in sorted order
+    a[sl * 32] = __dmul_rn(__ddiv_rn(1.0, shepard_pow(x, cfg.p)), (double)q.z);  // mass
+  }
+  // numpy's pairwise sum (K <= floor <= 32: the 8-accumulator leaf), in sorted order
   double S;
   if (K < 8) {
     S = 0.0;
-    for (int e = 0; e < K; e++) {
-      double d;
-      const double mv = mass(e, &d);
-      if (MODE == 1) {
-        o_bkt[e] = entry(e).w;
-        o_dist[e] = d;
-      }
-      S = __dadd_rn(S, mv);
-    }
+    for (int e = 0; e < K; e++) S = __dadd_rn(S, a[pm[e * 32] * 32]);
   } else {
     double r[8];
-    const int body = K - (K % 8);
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      double d;
-      r[q] = mass(q, &d);
-      if (MODE == 1) {
-        o_bkt[q] = entry(q).w;
-        o_dist[q] = d;
-      }
-    }
-    for (int i = 8; i < body; i += 8) {
+    for (int q = 0; q < 8; q++) r[q] = a[pm[q * 32] * 32];
+    int i = 8;
+    for (; i < K - (K % 8); i += 8) {
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        double d;
-        r[q] = __dadd_rn(r[q], mass(i + q, &d));
-        if (MODE == 1) {
-          o_bkt[i + q] = entry(i + q).w;
-          o_dist[i + q] = d;
-        }
-      }
+      for (int q = 0; q < 8; q++) r[q] = __dadd_rn(r[q], a[pm[(i + q) * 32] * 32]);
     }
     S = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                   __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (int i = body; i < K; i++) {
-      double d;
-      S = __dadd_rn(S, mass(i, &d));
-      if (MODE == 1) {
-        o_bkt[i] = entry(i).w;
-        o_dist[i] = d;
-      }
-    }
+    for (; i < K; i++) S = __dadd_rn(S, a[pm[i * 32] * 32]);
   }
-  // pass 2: probabilities and their sequential cumsum (np.cumsum) -> last
   double acc = 0.0;
   for (int e = 0; e < K; e++) {
-    const double pr = __ddiv_rn(mass(e, nullptr), S);
+    const int sl = pm[e * 32];
+    const double pr = __ddiv_rn(a[sl * 32], S);
     if (MODE == 1) o_prob[e] = pr;
-    acc = e == 0 ? pr : __dadd_rn(acc, pr);
+    acc = e == 0 ? pr : __dadd_rn(acc, pr);  // np.cumsum: sequential
+    a[sl * 32] = acc;
   }
   const double last = acc;
-  // pass 3: the same cumsum again, cdf = acc / last
-  acc = 0.0;
   for (int e = 0; e < K; e++) {
-    const double pr = __ddiv_rn(mass(e, nullptr), S);
-    acc = e == 0 ? pr : __dadd_rn(acc, pr);
-    const double cdf = __ddiv_rn(acc, last);
+    const int sl = pm[e * 32];
+    const double cdf = __ddiv_rn(a[sl * 32], last);
     if (MODE == 1) {
       o_cdf[e] = cdf;
     } else {
-      const int4& q = entry(e);
+      const int4 q = tw.u[tw.j[sl * 32 + lane]];
       pool_put(*pp, e, cdf, make_int2((int32_t)T.bkt_off[q.w], q.z));
     }
   }
