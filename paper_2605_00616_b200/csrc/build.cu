@@ -50,25 +50,43 @@ struct RecIn {
   int64_t n;
 };
 
-__global__ void k_validate(RecIn r, unsigned long long* first_bad, int* maxv) {
+// Four records per thread per iteration (their loads issue together: the
+// check is a pure stream, latency-bound at one record per thread).
+__device__ __forceinline__ int record_check(const RecIn& r, int64_t i, int32_t t, int32_t c, double l) {
+  if (r.step && r.step[i] < 0) return 1;
+  if (t < 1) return 2;
+  if (c < 1) return 3;
+  if (r.ph[i] == 0 && t < c) return 4;
+  if (!(l > 0.0)) return 5;
+  return 0;
+}
+__global__ void __launch_bounds__(256, 6) k_validate(RecIn r, unsigned long long* first_bad, int* maxv) {
   int mt = 0, mc = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t t = r.tt[i], c = r.conc[i];
-    const double l = r.lat[i];
-    int code = 0;
-    if (r.step && r.step[i] < 0)
-      code = 1;
-    else if (t < 1)
-      code = 2;
-    else if (c < 1)
-      code = 3;
-    else if (r.ph[i] == 0 && t < c)
-      code = 4;
-    else if (!(l > 0.0))
-      code = 5;
-    if (code) atomicMin(first_bad, ((unsigned long long)i << 3) | (unsigned long long)code);
-    mt = max(mt, t);
-    mc = max(mc, c);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i0 < r.n; i0 += stride) {
+    int32_t t[4], c[4];
+    double l[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int64_t i = i0 + (int64_t)q * gridDim.x * blockDim.x;
+      t[q] = 1;
+      c[q] = 1;
+      l[q] = 1.0;
+      if (i < r.n) {
+        t[q] = r.tt[i];
+        c[q] = r.conc[i];
+        l[q] = r.lat[i];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int64_t i = i0 + (int64_t)q * gridDim.x * blockDim.x;
+      if (i >= r.n) continue;
+      const int code = record_check(r, i, t[q], c[q], l[q]);
+      if (code) atomicMin(first_bad, ((unsigned long long)i << 3) | (unsigned long long)code);
+      mt = max(mt, t[q]);
+      mc = max(mc, c[q]);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

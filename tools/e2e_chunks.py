@@ -1,5 +1,5 @@
 import os, sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2605_00616_b200 import LatencyOracle, OracleConfig
 from paper_2605_00616_b200.device import DeviceTables
