@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __r
 // d, flag 2 = inclusive prefix over tiles <= t (values < 2^30: n < 2^30).
 constexpr unsigned kLookAgg = 1u << 30, kLookPre = 2u << 30, kLookVal = (1u << 30) - 1u;
 template <typename H>
-__global__ void __launch_bounds__(kRThreads) k_onesweep(const H* __restrict__ a_hi, const uint64_t* __restrict__ a_lo,
+__global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__ a_hi, const uint64_t* __restrict__ a_lo,
                                                        H* __restrict__ b_hi, uint64_t* __restrict__ b_lo, int64_t n,
                                                        int shift, int key_is_hi, const unsigned int* __restrict__ gstart,
                                                        unsigned int* look, unsigned int* tile_ctr) {
