@@ -533,8 +533,24 @@ def run_b200(args):
         e2e_s = (time.perf_counter() - t0) / n_e2e
         e2e_s = all_reduce_max(e2e_s)
         h2d = Q * (4 + 4 + 1 + (12 if args.rng == "explicit" else 0))
+        # the e2e path's ceiling: pinned host -> device copy bandwidth, measured here
+        hb = torch.empty(h2d, dtype=torch.uint8).pin_memory()
+        db = torch.empty(h2d, dtype=torch.uint8, device="cuda")
+        db.copy_(hb, non_blocking=True)
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record()
+        for _ in range(3):
+            db.copy_(hb, non_blocking=True)
+        p1.record()
+        torch.cuda.synchronize()
+        h2d_ms = p0.elapsed_time(p1) / 3
+        del hb, db
         line["e2e"] = {"value": size * Q / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": Q * 8, "ms_per_step": e2e_s * 1e3,
+                       "pcie": {"h2d_GBps": h2d / h2d_ms / 1e6, "h2d_floor_ms": h2d_ms,
+                                "frac": h2d_ms / (e2e_s * 1e3),
+                                "note": "the step's input bytes alone over PCIe (pinned, one copy) vs the e2e step"},
                        "api": "LatencyOracle.sample_batch(numpy pinned, latencies out) -> emu_oracle_sample_host "
                               "(1M-query chunks, copy-in / build+draw / copy-out on three streams)"}
         # ---- p50 latency of one engine-step query (LatencyOracle.__call__), cached keys

@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(kSampleThreads, (QPT <= 1 ? 8 : QPT == 2 ? 6 :
 
 // One query's draw from its (built) map entry e: the inverse-CDF pick and the
 // Lemire index, exactly as k_sample; writes lat / sidx of query i.
-template <int RNG>
+template <int RNG, bool CG = false>
 __device__ __forceinline__ void draw_query(const Slot* __restrict__ arena, const double* __restrict__ s0,
                                            const double* __restrict__ s1, long long e, int ph, int64_t i,
                                            const uint64_t* __restrict__ usel, const uint32_t* __restrict__ uidx,
@@ -852,10 +852,10 @@ __device__ __forceinline__ void draw_query(const Slot* __restrict__ arena, const
     us = (uint64_t)px.x | ((uint64_t)px.y << 32);
     w0 = px.z;
   }
-  const PoolPick sl = pool_pick(arena, e, unit_k53(us));
+  const PoolPick sl = pool_pick<CG>(arena, e, unit_k53(us));
   const uint32_t k = draw_index<RNG>((uint32_t)sl.n, w0, px, ctr_base + (uint64_t)i, key);
   const int32_t sidx = sl.soff + (int32_t)k;
-  st_stream(out_lat + i, (ph ? s1 : s0)[sidx], hint);
+  st_stream(out_lat + i, ldp<CG>((ph ? s1 : s0) + sidx), hint);
   st_stream(out_sidx + i, sidx, hint);
 }
 
@@ -864,7 +864,7 @@ __device__ __forceinline__ void draw_query(const Slot* __restrict__ arena, const
 // appended to the miss list (and its key claimed and appended to the new-key
 // list, as k_mark does).  After the pool tiers, k_sample_list draws the misses
 // only, so each key / uniform is read from HBM once (41 B/query explicit).
-template <int RNG>
+template <int RNG, bool CG>
 __global__ void __launch_bounds__(kSampleThreads, 8) k_sweep(MapView m, const Slot* __restrict__ arena,
                                                              const double* __restrict__ s0,
                                                              const double* __restrict__ s1,
@@ -891,10 +891,10 @@ __global__ void __launch_bounds__(kSampleThreads, 8) k_sweep(MapView m, const Sl
       c = __ldcs(qc + i);
     }
     const int64_t idx = v ? map_find<true>(m, ph, t, c) : -2;
-    const long long e = idx >= 0 ? *map_entry_ptr(m, idx) : -1;
+    const long long e = idx >= 0 ? ldp<CG>(map_entry_ptr(m, idx)) : -1;
     if (idx == -1) atomicOr(&ctl->flags, FLAG_HASH);
     const bool hit = e > 0;
-    if (hit) draw_query<RNG>(arena, s0, s1, e, ph, i, usel, uidx, key, ctr_base, out_lat, out_sidx, true);
+    if (hit) draw_query<RNG, CG>(arena, s0, s1, e, ph, i, usel, uidx, key, ctr_base, out_lat, out_sidx, true);
     // claim empty entries: one CAS per distinct key per warp
     const bool cand = idx >= 0 && e == kEntryEmpty;
     bool won = false;
@@ -2158,14 +2158,27 @@ static int draw_chunk(emu_oracle_t o, int rng_mode, const int32_t* qt, const int
   EMU_CUDA(reset_counters(o, s));
   const int grid = grid_for(m, kSampleThreads, kNumSMs * 8);
   const uint64_t sd = seed;
-  if (rng_mode == EMU_RNG_EXPLICIT)
-    EMU_LAUNCH("sweep", s, k_sweep<EMU_RNG_EXPLICIT><<<grid, kSampleThreads, 0, s>>>(
-                               o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, m, us, ui, sd,
-                               ctr, lat, sidx, o->nk_tt, o->nk_c, o->nk_p, o->nk_e, o->miss, o->ctl));
-  else
-    EMU_LAUNCH("sweep", s, k_sweep<EMU_RNG_PHILOX><<<grid, kSampleThreads, 0, s>>>(
-                               o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, m, us, ui, sd,
-                               ctr, lat, sidx, o->nk_tt, o->nk_c, o->nk_p, o->nk_e, o->miss, o->ctl));
+  // EMU_SWEEP_CG=1: the sweep's gathers (entry, pool, sample) through L2 only (tuning knob)
+  static const bool cg = [] {
+    const char* v = getenv("EMU_SWEEP_CG");
+    return v && v[0] == '1';
+  }();
+#define EMU_SWEEP_LAUNCH(R, C)                                                                                     \
+  EMU_LAUNCH("sweep", s, (k_sweep<R, C><<<grid, kSampleThreads, 0, s>>>(                                          \
+                             o->map, o->arena, o->plane[0].samples, o->plane[1].samples, qt, qc, qp, m, us, ui, sd, \
+                             ctr, lat, sidx, o->nk_tt, o->nk_c, o->nk_p, o->nk_e, o->miss, o->ctl)))
+  if (rng_mode == EMU_RNG_EXPLICIT) {
+    if (cg)
+      EMU_SWEEP_LAUNCH(EMU_RNG_EXPLICIT, true);
+    else
+      EMU_SWEEP_LAUNCH(EMU_RNG_EXPLICIT, false);
+  } else {
+    if (cg)
+      EMU_SWEEP_LAUNCH(EMU_RNG_PHILOX, true);
+    else
+      EMU_SWEEP_LAUNCH(EMU_RNG_PHILOX, false);
+  }
+#undef EMU_SWEEP_LAUNCH
   EMU_CUDA(cudaGetLastError());
   int lgrid = kNumSMs * 4;
   if (may_sync) {  // flags .. miss_count in one copy
