@@ -248,7 +248,7 @@ __device__ __forceinline__ long long warp_alloc(unsigned long long* counter, lon
 template <int MODE>
 __global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Keys keys, Cfg cfg, Sink sk, KeyWin* kw,
                                                    long long* resv, int* esc_list, int* esc_count, int* wl,
-                                                   int* wl_n) {
+                                                   int* wl_n, int all_to_grp) {
   const int64_t n = keys.count_dev ? (int64_t)*keys.count_dev : keys.count;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
@@ -268,9 +268,9 @@ __global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Key
     if (!ready) k.flags = win ? ((k.flags & ~kWinReady) | kWinBig) : 0;
     long long r = -1;
     if (MODE == 0) {
-      const long long need = ready ? pool_total_slots(k.cap < cfg.floor ? k.cap : cfg.floor) : 0;
+      const long long need = ready && !all_to_grp ? pool_total_slots(k.cap < cfg.floor ? k.cap : cfg.floor) : 0;
       const long long st = warp_alloc(sk.arena_used, need);
-      if (ready) {
+      if (ready && !all_to_grp) {
         r = (st + need <= sk.arena_cap) ? st : -2;
         if (r == -2) atomicOr(sk.flags, FLAG_ARENA);
       }
@@ -282,8 +282,8 @@ __global__ void __launch_bounds__(256) k_pool_prep(DevTable P0, DevTable P1, Key
     // windows too big for a warp go straight onto the group tier's list; without
     // the tile tier the others form the warp tier's list (wl)
     const bool big = valid && (k.flags & kWinBig);
-    warp_push(esc_list, esc_count, big, (int)w);
-    if (wl) warp_push(wl, wl_n, valid && !big, (int)w);
+    warp_push(esc_list, esc_count, all_to_grp ? valid : big, (int)w);
+    if (wl && !all_to_grp) warp_push(wl, wl_n, valid && !big, (int)w);
   }
 }
 
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kGrpThreads, EMU_GRP_MINB) k_pool_grp(DevTable
     const int64_t ent = keys.entry ? keys.entry[w] : 0;
     const KeyWin k = kw[w];
     const bool ok = process_key<kGrpThreads, MODE>(T, w, keys.ph[w] ? 1 : 0, keys.tt[w], keys.conc[w], ent, cfg, ws,
-                                                   sk, (k.flags & kWinBig) ? &k : nullptr);
+                                                   sk, (k.flags & (kWinBig | kWinReady)) ? &k : nullptr);
     if (!ok && threadIdx.x == 0) esc2_list[atomicAdd(esc2_count, 1)] = w;
   }
 }
@@ -1424,6 +1424,8 @@ struct emu_oracle_s {
   int* esc2 = nullptr;
   int64_t chunk_cap = 0;
   bool cold = true;          // cache flushed since the last batch: the head of the next batch takes the mark path
+  bool sweep_ok = false;     // the last chunk met few new keys: warm chunks take the one-pass k_sweep
+  bool last_swept = false;   // the last chunk went through k_sweep (its miss count is in ctl_host)
   int* miss = nullptr;       // k_sweep miss list (query indices)
   int64_t miss_cap = 0;
   int64_t arena_max = 0;  // growth limit for the pool arena (slots)
@@ -1821,9 +1823,16 @@ struct OffOut {
 // arena reservation) -> tile tier (counting sort of the keys into (phase, conc,
 // tt) bins, warp per 32 keys, lane per key) -> warp tier for the keys the tile
 // tier handed over (or all keys) -> group tier -> CTA tier.
+// known_new >= 0: the host knows the number of new keys; a small batch
+// (<= kSmallBatch) skips the tile and warp tiers: every key goes to the group
+// tier, whose 4 warps per key finish one key sooner than a warp does -- with few
+// keys the tiers' latency, not their throughput, is the cost (config 5's
+// scenario batches each bring a few hundred to a few thousand new keys).
+constexpr int64_t kSmallBatch = 2048;
 template <int MODE>
 static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, cudaStream_t s, bool sync_check,
-                             bool dense_keys = false) {
+                             bool dense_keys = false, int64_t known_new = -1) {
+  const bool small = known_new >= 0 && known_new <= kSmallBatch && !getenv("EMU_NO_SMALL_BATCH");
   static const bool tile_debug = getenv("EMU_TILE_DEBUG") != nullptr;
   auto chk = [&](const char* what) -> int {
     EMU_CUDA(cudaGetLastError());
@@ -1842,12 +1851,14 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
   int rc;
   EMU_LAUNCH("pool_prep", s, k_pool_prep<MODE><<<kPrepGrid, 256, 0, s>>>(
                                  o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, o->esc,
-                                 &o->ctl->esc_count, o->tile_on ? nullptr : o->fb_list, &o->ctl->fb_n));
+                                 &o->ctl->esc_count, o->tile_on ? nullptr : o->fb_list, &o->ctl->fb_n, small ? 1 : 0));
   if ((rc = chk("pool_prep"))) return rc;
   const int* list = o->fb_list;  // the warp tier's keys: from prep, or handed over by the tile tier
   const int* list_n = &o->ctl->fb_n;
   int* warp_work = &o->ctl->fb_work;
-  if (o->tile_on && dense_keys) {  // cold path: keys already in tile order (build_missing_cold)
+  if (small) {
+    // tile and warp tiers skipped: prep put every key on the group tier's list
+  } else if (o->tile_on && dense_keys) {  // cold path: keys already in tile order (build_missing_cold)
     EMU_LAUNCH("pool_tile", s, k_pool_tile<MODE><<<kNumSMs * EMU_TILE_MINB, kTileThreads, kTileBytes, s>>>(
                                    o->plane[0], o->plane[1], keys, o->cfg, sk, o->ti, o->kw, o->resv, nullptr,
                                    nullptr, &o->ctl->dense_n, &o->ctl->dense_n0, &o->ctl->tile_work, o->fb_list,
@@ -1883,6 +1894,7 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
                                    &o->ctl->fb_n));
     if ((rc = chk("pool_tile"))) return rc;
   }
+  if (!small)
   EMU_LAUNCH("pool_warp", s, k_pool_warp<MODE><<<kWarpGrid, kWarpThreads, kWarpBytes * kWarpsPerCta, s>>>(
                                  o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, warp_work, o->esc,
                                  &o->ctl->esc_count, list, list_n));
@@ -1940,7 +1952,12 @@ static int build_missing(emu_oracle_t o, const int32_t* qt, const int32_t* qc, c
   }
   EMU_CUDA(cudaGetLastError());
   Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
-  rc = launch_pool_tiers<0>(o, keys, make_sink(o), s, false);
+  // one round trip for the new-key count: nothing to build skips the tiers, a
+  // few keys take the small-batch route
+  EMU_CUDA(cudaMemcpyAsync(o->ctl_host, o->ctl, offsetof(BatchCtl, miss_count) + sizeof(int), cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
+  const int64_t known = o->ctl_host->new_count;
+  rc = known == 0 ? EMU_OK : launch_pool_tiers<0>(o, keys, make_sink(o), s, false, false, known);
   static const bool tile_stats = [] {
     const char* v = getenv("EMU_TILE_STATS");
     return v && v[0] == '1';
@@ -2000,11 +2017,24 @@ static int build_missing_cold(emu_oracle_t o, const int32_t* qt, const int32_t* 
   return launch_pool_tiers<0>(o, keys, make_sink(o), s, false, true);
 }
 
+// Flags of the chunk (and, in ctl_host, its new-key / miss counts).
 static int read_flags(emu_oracle_t o, cudaStream_t s, int* flags) {
-  EMU_CUDA(cudaMemcpyAsync(o->flags_host, &o->ctl->flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaMemcpyAsync(o->ctl_host, o->ctl, offsetof(BatchCtl, miss_count) + sizeof(int), cudaMemcpyDeviceToHost,
+                           s));
   EMU_CUDA(cudaStreamSynchronize(s));
-  *flags = o->flags_host[0];
+  *flags = o->ctl_host->flags;
   return EMU_OK;
+}
+
+// Which path the next warm chunk takes.  k_sweep draws hits in its single pass
+// but sends every miss through a second, gathering pass (and a host round trip
+// to size it); a chunk that still meets many new keys -- what-if scenarios
+// exploring new batch shapes -- is cheaper as k_mark + tiers + k_sample.
+// (C5, 512 scenarios x 1M steps: 222 ms with k_sweep on every chunk.)
+static void update_path(emu_oracle_t o, bool swept, int64_t n) {
+  if (n <= 0) return;
+  const double frac = swept ? (double)o->ctl_host->miss_count / (double)n : (double)o->ctl_host->new_count / (double)n;
+  o->sweep_ok = frac < (swept ? 0.02 : 0.002);
 }
 
 // Handle a failed chunk: grow the hash on overflow; always flush the cache.
@@ -2135,9 +2165,18 @@ static int draw_chunk(emu_oracle_t o, int rng_mode, const int32_t* qt, const int
                       int64_t n, const uint64_t* us, const uint32_t* ui, uint64_t seed, uint64_t ctr, double* lat,
                       int32_t* sidx, cudaStream_t s, bool may_sync, int* flags_out = nullptr) {
   if (flags_out) *flags_out = -1;
+  // cold: the bitmap path for the head (all of it by default); warm with few new
+  // keys lately: k_sweep; otherwise the two-pass path (k_mark, tiers, k_sample)
+  const bool two_pass = !o->cold && !o->sweep_ok;
   const int64_t head = o->cold ? cold_head(n) : 0;
   const int64_t m = n - head;
   o->cold = false;
+  o->last_swept = false;
+  if (two_pass) {
+    int rc = build_missing(o, qt, qc, qp, n, s);
+    if (!rc) rc = launch_sample(o, rng_mode, qt, qc, qp, n, us, ui, seed, ctr, lat, sidx, s);
+    return rc;
+  }
   int rc;
   // scratch first: reallocating after the head pass is enqueued would stall on it
   if ((rc = ensure_key_capacity(o, std::min<int64_t>(n, map_entries(o))))) return rc;
@@ -2155,7 +2194,8 @@ static int draw_chunk(emu_oracle_t o, int rng_mode, const int32_t* qt, const int
   if (m <= 0) return EMU_OK;
   qt += head, qc += head, qp += head, lat += head, sidx += head, ctr += (uint64_t)head;
   if (us) us += head, ui += head;
-  EMU_CUDA(reset_counters(o, s));
+  if (head > 0) EMU_CUDA(reset_counters(o, s));  // (callers zero the whole block before a chunk)
+  o->last_swept = true;
   const int grid = grid_for(m, kSampleThreads, kNumSMs * 8);
   const uint64_t sd = seed;
   // EMU_SWEEP_CG=1: the sweep's gathers (entry, pool, sample) through L2 only (tuning knob)
@@ -2192,7 +2232,8 @@ static int draw_chunk(emu_oracle_t o, int rng_mode, const int32_t* qt, const int
     lgrid = grid_for(o->ctl_host->miss_count, kSampleThreads, kNumSMs * 4);
   }
   Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
-  if ((!may_sync || o->ctl_host->new_count > 0) && (rc = launch_pool_tiers<0>(o, keys, make_sink(o), s, false)))
+  if ((!may_sync || o->ctl_host->new_count > 0) &&
+      (rc = launch_pool_tiers<0>(o, keys, make_sink(o), s, false, false, may_sync ? o->ctl_host->new_count : -1)))
     return rc;
   if (rng_mode == EMU_RNG_EXPLICIT)
     EMU_LAUNCH("sample_list", s, k_sample_list<EMU_RNG_EXPLICIT><<<lgrid, kSampleThreads, 0, s>>>(
@@ -2233,6 +2274,7 @@ int emu_oracle_sample(emu_oracle_t o, const int32_t* q_tt, const int32_t* q_conc
     EMU_CUDA(cudaGetLastError());
     int flags = fk;
     if (fk < 0 && (rc = read_flags(o, s, &flags))) return rc;
+    update_path(o, o->last_swept, n);
     if (flags) {
       if (++attempts > 16) return fail(EMU_ERR_CUDA, "oracle could not fit a chunk after 16 retries");
       if (flags & FLAG_BADPOOL) return bad_pool_error(o, s);
