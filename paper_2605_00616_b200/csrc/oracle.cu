@@ -658,17 +658,21 @@ __global__ void __launch_bounds__(kGrpThreads, EMU_GRP_MINB) k_pool_grp(DevTable
   __shared__ int32_t ncache[2 * kGrpCache];
   PoolWS ws{(double*)smem, (int32_t*)(smem + kGrpCap * 8), kGrpCap, scr, dsh, rows, ncache, ncache + kGrpCache,
             kGrpCache};
-  const int n = *esc_count;
+  // esc_list == nullptr: every new key, in order (small batches, no k_pool_prep:
+  // the group's own 32-lane radius probe finds the window in two rounds)
+  const int n = esc_list ? *esc_count : (keys.count_dev ? *keys.count_dev : (int)keys.count);
   for (;;) {
     if (threadIdx.x == 0) s_w = atomicAdd(work, 1);
     __syncthreads();
     const int i = s_w;
     __syncthreads();
     if (i >= n) break;
-    const int w = esc_list[i];
+    const int w = esc_list ? esc_list[i] : i;
     const DevTable& T = keys.ph[w] ? P1 : P0;
     const int64_t ent = keys.entry ? keys.entry[w] : 0;
-    const KeyWin k = kw[w];
+    KeyWin k;
+    k.flags = 0;
+    if (kw) k = kw[w];
     const bool ok = process_key<kGrpThreads, MODE>(T, w, keys.ph[w] ? 1 : 0, keys.tt[w], keys.conc[w], ent, cfg, ws,
                                                    sk, (k.flags & (kWinBig | kWinReady)) ? &k : nullptr);
     if (!ok && threadIdx.x == 0) esc2_list[atomicAdd(esc2_count, 1)] = w;
@@ -1824,10 +1828,11 @@ struct OffOut {
 // tt) bins, warp per 32 keys, lane per key) -> warp tier for the keys the tile
 // tier handed over (or all keys) -> group tier -> CTA tier.
 // known_new >= 0: the host knows the number of new keys; a small batch
-// (<= kSmallBatch) skips the tile and warp tiers: every key goes to the group
-// tier, whose 4 warps per key finish one key sooner than a warp does -- with few
-// keys the tiers' latency, not their throughput, is the cost (config 5's
-// scenario batches each bring a few hundred to a few thousand new keys).
+// (<= kSmallBatch) skips k_pool_prep and the tile and warp tiers: every key goes
+// to the group tier, whose 4 warps per key (32-lane radius probe, then the
+// window) finish one key sooner than a thread + a warp do -- with few keys the
+// tiers' latency, not their throughput, is the cost (config 5's scenario
+// batches each bring a few hundred to a few thousand new keys).
 constexpr int64_t kSmallBatch = 2048;
 template <int MODE>
 static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, cudaStream_t s, bool sync_check,
@@ -1849,6 +1854,7 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
     return EMU_OK;
   };
   int rc;
+  if (!small)
   EMU_LAUNCH("pool_prep", s, k_pool_prep<MODE><<<kPrepGrid, 256, 0, s>>>(
                                  o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, o->esc,
                                  &o->ctl->esc_count, o->tile_on ? nullptr : o->fb_list, &o->ctl->fb_n, small ? 1 : 0));
@@ -1899,10 +1905,10 @@ static int launch_pool_tiers(emu_oracle_t o, const Keys& keys, const Sink& sk, c
                                  o->plane[0], o->plane[1], keys, o->cfg, sk, o->kw, o->resv, warp_work, o->esc,
                                  &o->ctl->esc_count, list, list_n));
   if ((rc = chk("pool_warp"))) return rc;
-  EMU_LAUNCH("pool_grp", s, k_pool_grp<MODE><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(o->plane[0], o->plane[1], keys,
-                                                                                     o->cfg, sk, o->kw, &o->ctl->esc_work,
-                                                                                     o->esc, &o->ctl->esc_count, o->esc2,
-                                                                                     &o->ctl->esc2_count));
+  EMU_LAUNCH("pool_grp", s, k_pool_grp<MODE><<<kGrpGrid, kGrpThreads, kGrpSmem, s>>>(
+                                o->plane[0], o->plane[1], keys, o->cfg, sk, small ? nullptr : o->kw,
+                                &o->ctl->esc_work, small ? nullptr : o->esc, &o->ctl->esc_count, o->esc2,
+                                &o->ctl->esc2_count));
   if ((rc = chk("pool_grp"))) return rc;
   EMU_LAUNCH("pool_cta", s, k_pool_cta<MODE><<<kCtaGrid, kCtaThreads, kCtaSmem, s>>>(o->plane[0], o->plane[1], keys,
                                                                                      o->cfg, sk, &o->ctl->esc2_work,
@@ -2032,6 +2038,14 @@ static int read_flags(emu_oracle_t o, cudaStream_t s, int* flags) {
 // exploring new batch shapes -- is cheaper as k_mark + tiers + k_sample.
 // (C5, 512 scenarios x 1M steps: 222 ms with k_sweep on every chunk.)
 static void update_path(emu_oracle_t o, bool swept, int64_t n) {
+  static const int mode = [] {  // EMU_SWEEP=0: never k_sweep, 1: always (tuning knob)
+    const char* v = getenv("EMU_SWEEP");
+    return v ? atoi(v) : -1;
+  }();
+  if (mode >= 0) {
+    o->sweep_ok = mode == 1;
+    return;
+  }
   if (n <= 0) return;
   const double frac = swept ? (double)o->ctl_host->miss_count / (double)n : (double)o->ctl_host->new_count / (double)n;
   o->sweep_ok = frac < (swept ? 0.02 : 0.002);
