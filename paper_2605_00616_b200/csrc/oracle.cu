@@ -2016,7 +2016,7 @@ static int build_missing_cold(emu_oracle_t o, const int32_t* qt, const int32_t* 
   EMU_LAUNCH("bits", s, k_bits_emit<<<(unsigned)nblk, kBitThreads, 0, s>>>(o->bits, words, ps / 32, o->bits_part,
                                                                            o->map, o->nk_tt, o->nk_c, o->nk_p,
                                                                            o->nk_e, &o->ctl->dense_n0));
-  EMU_LAUNCH("append_hash", s, k_append_hash<<<kNumSMs, 256, 0, s>>>(o->hk_tt, o->hk_c, o->hk_p, o->hk_e, o->nk_tt,
+  EMU_LAUNCH("append_hash", s, k_append_hash<<<1, 256, 0, s>>>(o->hk_tt, o->hk_c, o->hk_p, o->hk_e, o->nk_tt,
                                                                      o->nk_c, o->nk_p, o->nk_e, o->ctl, o->fb_list));
   EMU_CUDA(cudaGetLastError());
   Keys keys{o->nk_tt, o->nk_c, o->nk_p, o->nk_e, &o->ctl->new_count, 0};
