@@ -552,7 +552,7 @@ def run_b200(args):
                                 "frac": h2d_ms / (e2e_s * 1e3),
                                 "note": "the step's input bytes alone over PCIe (pinned, one copy) vs the e2e step"},
                        "api": "LatencyOracle.sample_batch(numpy pinned, latencies out) -> emu_oracle_sample_host "
-                              "(1M-query chunks, copy-in / build+draw / copy-out on three streams)"}
+                              "(2M-query chunks, copy-in / build+draw / copy-out on three streams)"}
         # ---- p50 latency of one engine-step query (LatencyOracle.__call__), cached keys
         if rank == 0:
             keys = list(zip(qt_h[:3000].tolist(), qc_h[:3000].tolist(), qp_h[:3000].tolist()))

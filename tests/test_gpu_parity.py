@@ -315,10 +315,10 @@ def test_full_scale_properties(c1_pack):
 
 @pytest.mark.parametrize("arena", [0, 1 << 20])
 def test_pipelined_host_path_matches_device_path(c1_pack, arena):
-    """emu_oracle_sample_host (1M-query chunks on three streams) returns exactly
+    """emu_oracle_sample_host (2M-query chunks on three streams) returns exactly
     what the device-resident call returns; a small arena makes a middle chunk
     overflow, which is redone by the serial flush-and-retry path."""
-    Q = 2_600_000
+    Q = 5_200_000  # three chunks
     qt, qc, qp = queries_llama(Q, 5)
     us, ui = explicit_uniforms(Q, 6)
     orc = LatencyOracle(c1_pack, OracleConfig(reliability_floor=32), arena_slots=arena)
@@ -331,7 +331,7 @@ def test_pipelined_host_path_matches_device_path(c1_pack, arena):
     assert np.array_equal(sidx_h, sidx_d.cpu().numpy())
     assert np.array_equal(lat_h, lat_d.cpu().numpy())
     assert np.array_equal(lat_l, lat_h)
-    k0 = 2_000_000  # inside the third chunk
+    k0 = 4_200_000  # inside the third chunk
     tabs = to_oracle_tables(c1_pack)
     lat_o, sidx_o = O.sample_batch(tabs, qt[k0:k0 + 20_000], qc[k0:k0 + 20_000], qp[k0:k0 + 20_000], 32,
                                    mode="explicit", u_sel=us[k0:k0 + 20_000], u_idx=ui[k0:k0 + 20_000], threads=8)
