@@ -321,6 +321,21 @@ __device__ __forceinline__ uint64_t unit_k53(uint64_t next64) { return next64 >>
 // u = k53 * 2^-53 (numpy's random()): returns the chosen bucket.
 // cdf[K-1] == 1.0 > u, so a hit always exists.  32-bit offset arithmetic
 // (K, start < 2^31 units).
+// 32-byte loads (LDG.E.256 on sm_100): a draw reads a pool's header and one
+// 8-cdf group with three instead of six 16-byte loads.  Pools start on 32-B
+// boundaries and their parts on even 16-B units, so every such load is aligned;
+// it may read up to 48 B past what the draw uses (still inside the pool, the
+// next pool, or the arena's slack units).
+template <bool CG>
+__device__ __forceinline__ double4 ld256(const double* p) {
+  double4 v;
+  if (CG)
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  else
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
 template <bool CG>
 __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ arena, int64_t start64, int64_t K64,
                                                    uint64_t k53) {
@@ -332,10 +347,9 @@ __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ aren
   int32_t g = 0;
   if (G > 1) {
     const double* sp = reinterpret_cast<const double*>(P);
-    if (G <= 5) {  // <= 4 splits: two 16-byte loads, count splits <= u
-      const double2 a = ldp<CG>(reinterpret_cast<const double2*>(sp));
-      const double2 b = G > 3 ? ldp<CG>(reinterpret_cast<const double2*>(sp) + 1) : make_double2(2.0, 2.0);
-      g = (a.x <= u) + (G > 2 && a.y <= u) + (b.x <= u) + (G > 4 && b.y <= u);
+    if (G <= 5) {  // <= 4 splits: one 32-byte load, count splits <= u
+      const double4 a = ld256<CG>(sp);
+      g = (a.x <= u) + (G > 2 && a.y <= u) + (G > 3 && a.z <= u) + (G > 4 && a.w <= u);
     } else {
       int32_t lo = 0, hi = G - 1;  // number of splits <= u
       while (lo < hi) {
@@ -348,15 +362,13 @@ __device__ __forceinline__ PoolPick pool_draw_slot(const Slot* __restrict__ aren
       g = lo;
     }
   }
-  const double2* C = reinterpret_cast<const double2*>(P + hs) + g * (kGroupSlots / 2);
+  const double* C = reinterpret_cast<const double*>(P + hs) + g * kGroupSlots;
   const int32_t n = min(kGroupSlots, K - g * kGroupSlots);
-  int32_t j = 0;
-#pragma unroll
-  for (int q = 0; q < kGroupSlots / 2; q++) {
-    if (2 * q < n) {
-      const double2 c = ldp<CG>(C + q);
-      j += (c.x <= u) + (2 * q + 1 < n && c.y <= u);
-    }
+  const double4 c0 = ld256<CG>(C);
+  int32_t j = (c0.x <= u) + (n > 1 && c0.y <= u) + (n > 2 && c0.z <= u) + (n > 3 && c0.w <= u);
+  if (n > 4) {
+    const double4 c1 = ld256<CG>(C + 4);
+    j += (c1.x <= u) + (n > 5 && c1.y <= u) + (n > 6 && c1.z <= u) + (n > 7 && c1.w <= u);
   }
   const int2 d = ldp<CG>(reinterpret_cast<const int2*>(P + hs + ((K + 1) >> 1)) + g * kGroupSlots + j);
   PoolPick pk;

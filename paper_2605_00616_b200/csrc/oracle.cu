@@ -66,6 +66,7 @@ constexpr int kGrpGrid = kNumSMs * EMU_GRP_MINB;
 constexpr int kCtaGrid = kNumSMs;
 constexpr int kSampleThreads = 256;
 constexpr int kQPT = 4;  // queries per thread, interleaved for memory-level parallelism
+constexpr int64_t kArenaSlack = 4;  // units past arena_cap: a draw's 32-B loads may read up to 48 B past a pool
 constexpr int64_t kHostChunk = 1 << 21;  // queries per pipelined chunk of emu_oracle_sample_host (2M: 5.04 ms e2e at C2 vs 5.73 at 1M, 6.93 at 512k)
 
 struct BatchCtl {
@@ -1614,12 +1615,17 @@ int emu_oracle_create(emu_tables_t t, int32_t floor, double shepard_power, doubl
   o->chunk_cap = 1LL << 24;
   o->gcap = pow2_at_least(max_nb);
   bool need_global = o->gcap > kCtaCap;
-  if ((rc = dalloc(&o->map.dense, 2 * dt * dc)) || (rc = alloc_hash(o, hcap)) || (rc = dalloc(&o->arena, o->arena_cap)) ||
+  if ((rc = dalloc(&o->map.dense, 2 * dt * dc)) || (rc = alloc_hash(o, hcap)) || (rc = dalloc(&o->arena, o->arena_cap + kArenaSlack)) ||
       (rc = dalloc(&o->arena_used, 1)) || (rc = dalloc(&o->ctl, 1)) || (rc = dalloc(&o->pcg, 6)) ||
 
       (need_global && ((rc = dalloc(&o->gd, kCtaGrid * o->gcap)) || (rc = dalloc(&o->gb, kCtaGrid * o->gcap))))) {
     emu_oracle_destroy(o);
     return rc;
+  }
+  // a draw's wide loads also read a pool's padding: keep the whole arena initialized
+  if (cudaMemset(o->arena, 0, sizeof(Slot) * (o->arena_cap + kArenaSlack)) != cudaSuccess) {
+    emu_oracle_destroy(o);
+    return cuda_fail(cudaGetLastError(), "arena memset");
   }
   {
     const char* tv = getenv("EMU_TILE");
@@ -2066,7 +2072,11 @@ static int64_t recover(emu_oracle_t o, int flags, int64_t chunk, cudaStream_t s,
     cudaFree(o->arena);
     o->arena = nullptr;
     o->arena_cap = std::min(o->arena_max, o->arena_cap * 4);
-    if ((*rc = dalloc(&o->arena, o->arena_cap))) return -1;
+    if ((*rc = dalloc(&o->arena, o->arena_cap + kArenaSlack))) return -1;
+    if (cudaMemsetAsync(o->arena, 0, sizeof(Slot) * (o->arena_cap + kArenaSlack), s) != cudaSuccess) {
+      *rc = cuda_fail(cudaGetLastError(), "arena memset");
+      return -1;
+    }
     if ((*rc = oracle_flush(o, s))) return -1;
     return chunk;
   }
