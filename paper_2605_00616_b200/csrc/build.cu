@@ -5,8 +5,12 @@
 // order (profile.py:281-282):
 //   1. k_validate   : StepTraceRecord.validate per record (profile.py:61-79);
 //                     smallest failing index wins (build_pack reports the first).
-//   2. k_make_keys  : hi = (tt-1) << cbits | (conc-1), lo = lat_bits << 1 | phase
-//                     (positive doubles order like their IEEE bit patterns).
+//   2. k_make_keys  : hi = phase << (top bit) | (tt-1) << cbits | (conc-1),
+//                     lo = lat_bits (positive doubles order like their IEEE
+//                     bit patterns); the phase rides in hi's top bit, which
+//                     no digit pass reads, so it costs no sort pass.  The
+//                     digit histograms of every pass come out of the same
+//                     read of the records.
 //   3. LSD radix sort, 8-bit digits, stable: per 4096-record tile, warp
 //      match_any ranking into shared memory in digit order, then coalesced
 //      digit runs out (k_radix_scatter); scratch from a stream-ordered pool:
@@ -99,12 +103,97 @@ __global__ void __launch_bounds__(256, 6) k_validate(RecIn r, unsigned long long
   }
 }
 
+// The phase bit of a key word (decode 0, mixed 1) and the bucket key under it.
 template <typename H>
-__global__ void k_make_keys(RecIn r, int cbits, H* __restrict__ hi, uint64_t* __restrict__ lo) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n; i += (int64_t)gridDim.x * blockDim.x) {
-    hi[i] = (H)(((uint64_t)(uint32_t)(r.tt[i] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[i] - 1));
-    lo[i] = ((uint64_t)__double_as_longlong(r.lat[i]) << 1) | (r.ph[i] ? 1ULL : 0ULL);
+__device__ __forceinline__ unsigned key_phase(H h) {
+  return (unsigned)(h >> (8 * sizeof(H) - 1));
+}
+template <typename H>
+__device__ __forceinline__ H key_bucket(H h) {
+  return h & (H)(~((H)1 << (8 * sizeof(H) - 1)));
+}
+
+struct PassSet {
+  int n;
+  int word[17];  // 0 = lo, 1 = hi (entry n is a sentinel)
+  int shift[17];
+};
+
+// One digit's histogram into a CTA's shared counters: a warp whose valid
+// digits all agree (the exponent digits of the latencies) adds once instead
+// of 32 same-address shared atomics.
+__device__ __forceinline__ void hist_add(unsigned int* sh, unsigned d, bool v) {
+  const unsigned vm = __ballot_sync(0xffffffffu, v);
+  if (!vm) return;
+  const int leader = __ffs(vm) - 1;
+  const unsigned d0 = __shfl_sync(0xffffffffu, d, leader);
+  if (__all_sync(0xffffffffu, !v || d == d0)) {
+    if ((int)(threadIdx.x & 31) == leader) atomicAdd(&sh[d0], (unsigned)__popc(vm));
+  } else if (v) {
+    atomicAdd(&sh[d], 1u);
   }
+}
+
+// Keys of every record, the bits in which any record differs from record 0
+// (diff[0] latency word, diff[1] bucket key: a digit position whose 8 bits
+// never differ is the same for all records and its pass is skipped), and the
+// histogram of the first pass's digit (hword/hshift: the lowest latency digit
+// in canonical mode, else the lowest key digit).  Each later pass's histogram
+// is counted by the pass before it (k_onesweep), so the records are read once
+// here instead of once per pass.
+template <typename H>
+__global__ void __launch_bounds__(256) k_make_keys(RecIn r, int cbits, H* __restrict__ hi, uint64_t* __restrict__ lo,
+                                                   int hword, int hshift, unsigned int* hist,
+                                                   unsigned long long* diff) {
+  __shared__ unsigned int sh[256];
+  sh[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t k0 = ((uint64_t)(uint32_t)(r.tt[0] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[0] - 1);
+  const uint64_t l0 = (uint64_t)__double_as_longlong(r.lat[0]);
+  uint64_t dk = 0, dl = 0;
+  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < r.n; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;  // warp-uniform trip count (votes in hist_add)
+    const bool v = i < r.n;
+    uint64_t h = 0, l = 0;
+    if (v) {
+      h = ((uint64_t)(uint32_t)(r.tt[i] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[i] - 1);
+      l = (uint64_t)__double_as_longlong(r.lat[i]);
+      hi[i] = (H)h | (r.ph[i] ? (H)1 << (8 * sizeof(H) - 1) : (H)0);
+      lo[i] = l;
+      dk |= h ^ k0;
+      dl |= l ^ l0;
+    }
+    hist_add(sh, (unsigned)(((hword ? h : l) >> hshift) & 255u), v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dk |= __shfl_xor_sync(0xffffffffu, dk, o);
+    dl |= __shfl_xor_sync(0xffffffffu, dl, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (dl) atomicOr(&diff[0], (unsigned long long)dl);
+    if (dk) atomicOr(&diff[1], (unsigned long long)dk);
+  }
+  __syncthreads();
+  if (sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+}
+
+// One digit's histogram over the key arrays (only when make_keys guessed the
+// first pass wrong: its lowest digit turned out to be the same everywhere).
+template <typename H>
+__global__ void __launch_bounds__(256) k_digit_hist1(const H* __restrict__ hi, const uint64_t* __restrict__ lo,
+                                                     int64_t n, int word, int shift, unsigned int* hist) {
+  __shared__ unsigned int sh[256];
+  sh[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;
+    const bool v = i < n;
+    const uint64_t w = v ? (word ? (uint64_t)key_bucket(hi[i]) : lo[i]) : 0;
+    hist_add(sh, (unsigned)((w >> shift) & 255u), v);
+  }
+  __syncthreads();
+  if (sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
 }
 
 // Record count of every (phase, bucket key) over the dense key domain
@@ -120,39 +209,14 @@ __global__ void k_dense_count(const H* __restrict__ hi, const uint64_t* __restri
   for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = b0 + threadIdx.x;  // warp-uniform trip count (match_any below)
     const bool v = i < n;
-    const unsigned key = v ? ((unsigned)(lo[i] & 1ULL) << kb) | (unsigned)hi[i] : 0xffffffffu - (unsigned)lane;
+    const unsigned key = v ? (key_phase(hi[i]) << kb) | (unsigned)key_bucket(hi[i]) : 0xffffffffu - (unsigned)lane;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     if (v && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&dcnt[key], (unsigned)__popc(peers));
   }
 }
 
-struct PassSet {
-  int n;
-  int word[16];  // 0 = lo, 1 = hi
-  int shift[16];
-};
-
-// Histograms of every candidate digit position in one read of the keys.
-template <typename H>
-__global__ void k_digit_hist(const H* __restrict__ hi, const uint64_t* __restrict__ lo, int64_t n, PassSet ps,
-                             unsigned int* hist) {
-  extern __shared__ unsigned int sh[];
-  for (int i = threadIdx.x; i < ps.n * 256; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t h = (uint64_t)hi[i], l = lo[i];
-    for (int p = 0; p < ps.n; p++) {
-      const uint64_t w = ps.word[p] ? h : l;
-      atomicAdd(&sh[p * 256 + (int)((w >> ps.shift[p]) & 255u)], 1u);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < ps.n * 256; i += blockDim.x)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
-
-__global__ void __launch_bounds__(kRThreads) k_radix_up(const uint64_t* __restrict__ key, int shift, int64_t n,
-                                                       int64_t nblk, unsigned int* counts) {
+__global__ void __launch_bounds__(kRThreads) k_radix_up(const uint64_t* __restrict__ key, uint64_t kmask, int shift,
+                                                       int64_t n, int64_t nblk, unsigned int* counts) {
   __shared__ unsigned int h[256];
   h[threadIdx.x] = 0;
   __syncthreads();
@@ -160,7 +224,7 @@ __global__ void __launch_bounds__(kRThreads) k_radix_up(const uint64_t* __restri
 #pragma unroll 4
   for (int k = 0; k < kRRounds; k++) {
     const int64_t i = base + (int64_t)k * kRThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[(key[i] >> shift) & 255u], 1u);
+    if (i < n) atomicAdd(&h[((key[i] & kmask) >> shift) & 255u], 1u);
   }
   __syncthreads();
   counts[(int64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
@@ -221,7 +285,7 @@ __global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __r
       h = a_hi[i];
       l = a_lo[i];
     }
-    const unsigned d = valid ? (unsigned)(((key_is_hi ? h : l) >> shift) & 255u) : 256u + (unsigned)lane;
+    const unsigned d = valid ? (unsigned)(((key_is_hi ? key_bucket(h) : l) >> shift) & 255u) : 256u + (unsigned)lane;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const unsigned rank = __popc(peers & lt_mask);
     if (valid && rank == 0) wh[w][d] = (unsigned short)__popc(peers);
@@ -246,7 +310,7 @@ __global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __r
   }
   for (int j = t; j < cnt_tile; j += kRThreads) {
     const uint64_t h = s_hi[j], l = s_lo[j];
-    const unsigned d = (unsigned)(((key_is_hi ? h : l) >> shift) & 255u);
+    const unsigned d = (unsigned)(((key_is_hi ? key_bucket(h) : l) >> shift) & 255u);
     const unsigned pos = gofs[d] + (unsigned)j - tstart[d];
     b_hi[pos] = h;
     b_lo[pos] = l;
@@ -254,7 +318,7 @@ __global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __r
 }
 
 // One LSD pass without an up-sweep ("onesweep"): every pass's global digit
-// starts come from the single all-digits histogram (k_digit_hist); a tile's
+// starts come from the single all-digits histogram (k_make_keys); a tile's
 // offset inside each digit bucket comes from a decoupled look-back over the
 // tiles before it.  Tiles take their index from an atomic counter in launch
 // order, so a tile only ever waits on tiles that are already running.
@@ -262,25 +326,33 @@ __global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __r
 // (12 B each way with 32-bit bucket keys) -- no separate counting pass.
 // look[t * 256 + d] = flag << 30 | value: flag 1 = tile t's own count of digit
 // d, flag 2 = inclusive prefix over tiles <= t (values < 2^30: n < 2^30).
+#ifndef EMU_LOOKBACK
+#define EMU_LOOKBACK 16
+#endif
 constexpr unsigned kLookAgg = 1u << 30, kLookPre = 2u << 30, kLookVal = (1u << 30) - 1u;
 template <typename H>
 __global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__ a_hi, const uint64_t* __restrict__ a_lo,
                                                        H* __restrict__ b_hi, uint64_t* __restrict__ b_lo, int64_t n,
-                                                       int shift, int key_is_hi, const unsigned int* __restrict__ gstart,
-                                                       unsigned int* look, unsigned int* tile_ctr) {
+                                                       int shift, int key_is_hi, const unsigned int* __restrict__ hcur,
+                                                       unsigned int* look, unsigned int* tile_ctr,
+                                                       unsigned int* __restrict__ hnext, int nshift, int nword) {
   constexpr int kWarpItems = kRTile / kRWarps;  // 512 consecutive records per warp
   extern __shared__ __align__(16) unsigned char osm[];
   uint64_t* s_lo = reinterpret_cast<uint64_t*>(osm);
   H* s_hi = reinterpret_cast<H*>(osm + (size_t)kRTile * 8);
   __shared__ unsigned short wcnt[kRWarps][256];  // per-warp digit counts, then each warp's offset in the digit
   __shared__ unsigned int tstart[256];
-  __shared__ unsigned int gofs[256];  // gstart[d] + this tile's exclusive prefix
+  __shared__ unsigned int gofs[256];  // the digit's global start + this tile's exclusive prefix
   __shared__ unsigned int wsum[kRWarps];
+  __shared__ unsigned int gsum[kRWarps];
+  __shared__ unsigned int nh[256];  // the next pass's digit counts of this tile
   __shared__ unsigned int s_tile;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (t == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  const unsigned hc = hcur[t];  // this pass's global count of digit t (counted by the pass before)
 #pragma unroll
   for (int q = 0; q < kRWarps; q++) wcnt[q][t] = 0;
+  nh[t] = 0;
   __syncthreads();
   const unsigned tile = s_tile;
   const int64_t base = (int64_t)tile * kRTile;
@@ -305,7 +377,7 @@ __global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__
 #pragma unroll
   for (int k = 0; k < kRRounds; k++) {
     const bool valid = w * kWarpItems + k * 32 + lane < cnt_tile;
-    const unsigned d = valid ? (unsigned)(((key_is_hi ? (uint64_t)h[k] : l[k]) >> shift) & 255u) : 256u + (unsigned)lane;
+    const unsigned d = valid ? (unsigned)(((key_is_hi ? (uint64_t)key_bucket(h[k]) : l[k]) >> shift) & 255u) : 256u + (unsigned)lane;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const unsigned r = __popc(peers & lt_mask);
     const unsigned before = valid ? wcnt[w][d] : 0u;
@@ -330,23 +402,34 @@ __global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__
     atomicExch(&look[t], kLookPre | c);
   else
     atomicExch(&look[(size_t)tile * 256 + t], kLookAgg | c);
-  unsigned x = c;  // exclusive scan of the 256 counts -> tile-local digit starts
+  unsigned x = c, g = hc;  // exclusive scans of the tile's and the global digit counts
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    const unsigned z = __shfl_up_sync(0xffffffffu, g, o);
+    if (lane >= o) {
+      x += y;
+      g += z;
+    }
   }
-  if (lane == 31) wsum[w] = x;
+  if (lane == 31) {
+    wsum[w] = x;
+    gsum[w] = g;
+  }
   __syncthreads();
-  unsigned wb = 0;
-  for (int q = 0; q < w; q++) wb += wsum[q];
+  unsigned wb = 0, gb = 0;
+  for (int q = 0; q < w; q++) {
+    wb += wsum[q];
+    gb += gsum[q];
+  }
   tstart[t] = wb + x - c;
+  const unsigned gstart = gb + g - hc;
   __syncthreads();
   // ---- stage the tile in digit order
 #pragma unroll
   for (int k = 0; k < kRRounds; k++) {
     if (w * kWarpItems + k * 32 + lane < cnt_tile) {
-      const unsigned d = (unsigned)(((key_is_hi ? (uint64_t)h[k] : l[k]) >> shift) & 255u);
+      const unsigned d = (unsigned)(((key_is_hi ? (uint64_t)key_bucket(h[k]) : l[k]) >> shift) & 255u);
       const unsigned lp = tstart[d] + wcnt[w][d] + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
       s_hi[lp] = h[k];
       s_lo[lp] = l[k];
@@ -357,7 +440,7 @@ __global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__
   // dependent chain is ~1/16 of the distance to the nearest inclusive prefix
   unsigned excl = 0;
   if (tile > 0) {
-    constexpr int kLB = 16;
+    constexpr int kLB = EMU_LOOKBACK;
     bool done = false;
     for (int64_t q0 = (int64_t)tile - 1; !done; q0 -= kLB) {
       unsigned v[kLB];
@@ -374,23 +457,29 @@ __global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__
     }
     atomicExch(&look[(size_t)tile * 256 + t], kLookPre | (excl + c));
   }
-  gofs[t] = gstart[t] + excl;
+  gofs[t] = gstart + excl;
   __syncthreads();
   // ---- write every digit's run of the tile out contiguously
   for (int j = t; j < cnt_tile; j += kRThreads) {
     const H hv = s_hi[j];
     const uint64_t lv = s_lo[j];
-    const unsigned d = (unsigned)(((key_is_hi ? (uint64_t)hv : lv) >> shift) & 255u);
+    const unsigned d = (unsigned)(((key_is_hi ? (uint64_t)key_bucket(hv) : lv) >> shift) & 255u);
     const unsigned pos = gofs[d] + (unsigned)j - tstart[d];
     b_hi[pos] = hv;
     b_lo[pos] = lv;
+    if (hnext) atomicAdd(&nh[((nword ? (uint64_t)key_bucket(hv) : lv) >> nshift) & 255u], 1u);
+  }
+  if (hnext) {  // the next pass's histogram, counted on the way out
+    __syncthreads();
+    if (nh[t]) atomicAdd(&hnext[t], nh[t]);
   }
 }
 
-// Stable partition by phase bit (lo & 1): decode (0) records first.
+// Stable partition by the phase bit (hi's top bit): decode (0) records first.
+template <typename H>
 struct PhaseIn {
-  const uint64_t* lo;
-  __device__ uint32_t operator()(int64_t i) const { return (lo[i] & 1ULL) ? 0u : 1u; }
+  const H* hi;
+  __device__ uint32_t operator()(int64_t i) const { return key_phase(hi[i]) ? 0u : 1u; }
 };
 template <typename H>
 struct PhaseOut {
@@ -401,7 +490,7 @@ struct PhaseOut {
   H* m_hi;
   uint64_t* m_lo;
   __device__ void operator()(int64_t i, uint32_t ex) const {
-    if (lo[i] & 1ULL) {
+    if (key_phase(hi[i])) {
       const int64_t j = i - (int64_t)ex;
       m_hi[j] = hi[i];
       m_lo[j] = lo[i];
@@ -416,7 +505,9 @@ struct PhaseOut {
 template <typename H>
 struct HeadIn {
   const H* hi;
-  __device__ uint32_t operator()(int64_t i) const { return (i == 0 || hi[i] != hi[i - 1]) ? 1u : 0u; }
+  __device__ uint32_t operator()(int64_t i) const {
+    return (i == 0 || key_bucket(hi[i]) != key_bucket(hi[i - 1])) ? 1u : 0u;
+  }
 };
 template <typename H>
 struct HeadOut {
@@ -428,13 +519,13 @@ struct HeadOut {
   int64_t* bkt_off;
   double* samples;
   __device__ void operator()(int64_t i, uint32_t ex) const {
-    const uint64_t h = (uint64_t)hi[i];
-    if (i == 0 || h != (uint64_t)hi[i - 1]) {
+    const uint64_t h = (uint64_t)key_bucket(hi[i]);
+    if (i == 0 || h != (uint64_t)key_bucket(hi[i - 1])) {
       bkt_tt[ex] = (int32_t)(h >> cbits) + 1;
       bkt_conc[ex] = (int32_t)(h & ((1ULL << cbits) - 1ULL)) + 1;
       bkt_off[ex] = i;
     }
-    samples[i] = __longlong_as_double((long long)(lo[i] >> 1));
+    samples[i] = __longlong_as_double((long long)lo[i]);
   }
 };
 
@@ -485,16 +576,17 @@ struct DenseOut {
 };
 // The samples of all three tables in one pass over the sorted records: the
 // combined table is the sorted run, the phase tables its stable partition.
+template <typename H>
 struct SampleOut {
+  const H* hi;
   const uint64_t* lo;
   double* comb;
   double* dec;
   double* mix;
   __device__ void operator()(int64_t i, uint32_t ex) const {
-    const uint64_t l = lo[i];
-    const double v = __longlong_as_double((long long)(l >> 1));
+    const double v = __longlong_as_double((long long)lo[i]);
     comb[i] = v;
-    if (l & 1ULL)
+    if (key_phase(hi[i]))
       mix[i - (int64_t)ex] = v;
     else
       dec[ex] = v;
@@ -663,7 +755,7 @@ static int segment_finish(TableBuf& tb, int64_t nb, int64_t m, unsigned int* par
 // records: one packed scan over the key domain per table (buckets, offsets),
 // one scan over the records for all samples, then rows / ranges / index.
 template <typename H>
-static int segment_dense(const uint64_t* lo, int64_t n, int cbits, int kb, const unsigned int* dcnt,
+static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, int kb, const unsigned int* dcnt,
                          uint64_t* part64, uint64_t* tot64, unsigned int* partial, unsigned int* total_dev,
                          int* mm_dev, cudaStream_t s, TableBuf* tab) {
   const int64_t D = 1LL << kb;
@@ -688,7 +780,7 @@ static int segment_dense(const uint64_t* lo, int64_t n, int cbits, int kb, const
     int64_t* off_end = tb.bkt_off + nb;
     EMU_LAUNCH("fill_end", s, k_set_i64<<<1, 1, 0, s>>>(off_end, m));
   }
-  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn{lo}, SampleOut{lo, tab[2].samples, tab[0].samples, tab[1].samples},
+  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn<H>{hi}, SampleOut<H>{hi, lo, tab[2].samples, tab[0].samples, tab[1].samples},
                                           n, partial, total_dev, s));
   for (int j = 0; j < 3; j++) {
     const int64_t nb = (int64_t)(tot[j] >> 32), m = (int64_t)(tot[j] & 0xffffffffULL);
@@ -729,7 +821,7 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   };
   H *hi0, *hi1;
   uint64_t *lo0, *lo1;
-  unsigned int *counts = nullptr, *hist = nullptr, *partial = nullptr, *gst = nullptr, *look = nullptr,
+  unsigned int *counts = nullptr, *hist = nullptr, *partial = nullptr, *look = nullptr,
                *tile_ctr = nullptr;
   const int64_t nblk = (n + kRTile - 1) / kRTile;
   // EMU_ONESWEEP=0 (64-bit keys only): the up-sweep + scan + scatter passes instead
@@ -738,8 +830,8 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   const int64_t ncount = onesweep ? 1 : 256 * nblk;
   const int64_t npart = std::max<int64_t>((ncount + kScanTile - 1) / kScanTile, (n + kScanTile - 1) / kScanTile) + 1;
   if ((rc = salloc(&hi0, n)) || (rc = salloc(&lo0, n)) || (rc = salloc(&hi1, n)) || (rc = salloc(&lo1, n)) ||
-      (rc = salloc(&counts, ncount)) || (rc = salloc(&hist, 16 * 256)) || (rc = salloc(&partial, npart)) ||
-      (rc = salloc(&gst, 16 * 256)) || (rc = salloc(&look, onesweep ? 256 * nblk : 1)) ||
+      (rc = salloc(&counts, ncount)) || (rc = salloc(&hist, 17 * 256 + 4)) || (rc = salloc(&partial, npart)) ||
+      (rc = salloc(&look, onesweep ? 256 * nblk : 1)) ||
       (rc = salloc(&tile_ctr, 16)))
     return rc;
   // key domains up to 2^24 per phase: dense counts -> segment_dense (no scans over the records)
@@ -753,32 +845,33 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
     if ((rc = salloc(&dcnt, 2 * D)) || (rc = salloc(&part64, 3 * np64)) || (rc = salloc(&tot64, 4))) return rc;
     EMU_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned int) * 2 * D, s));
   }
-  EMU_LAUNCH("make_keys", s, k_make_keys<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(r, cbits, hi0, lo0));
-  // which digit positions actually vary
+  // keys, the differing bits and the first digit's histogram; then the passes
+  // are the digit positions in which some record differs from record 0
+  const int hword0 = canonical ? 0 : 1;
+  EMU_CUDA(cudaMemsetAsync(hist, 0, 4 * 17 * 256 + 16, s));  // hist[17][256], then diff[2]
+  unsigned long long* diff = reinterpret_cast<unsigned long long*>(hist + 17 * 256);
+  EMU_LAUNCH("make_keys", s,
+             k_make_keys<H><<<grid_of(n, 256, kNumSMs * 8), 256, 0, s>>>(r, cbits, hi0, lo0, hword0, 0, hist, diff));
+  unsigned long long dh[2];
+  EMU_CUDA(cudaMemcpyAsync(dh, diff, 16, cudaMemcpyDeviceToHost, s));
+  EMU_CUDA(cudaStreamSynchronize(s));
   PassSet ps{};
   if (canonical)
-    for (int sft = 0; sft < 64; sft += 8) {
-      ps.word[ps.n] = 0;
+    for (int sft = 0; sft < 64; sft += 8)
+      if ((dh[0] >> sft) & 255u) {
+        ps.word[ps.n] = 0;
+        ps.shift[ps.n++] = sft;
+      }
+  for (int sft = 0; sft < tbits + cbits; sft += 8)
+    if ((dh[1] >> sft) & 255u) {
+      ps.word[ps.n] = 1;
       ps.shift[ps.n++] = sft;
     }
-  for (int sft = 0; sft < tbits + cbits; sft += 8) {
-    ps.word[ps.n] = 1;
-    ps.shift[ps.n++] = sft;
+  if (ps.n > 0 && (ps.word[0] != hword0 || ps.shift[0] != 0)) {  // the guessed first digit never varies
+    EMU_CUDA(cudaMemsetAsync(hist, 0, 4 * 256, s));
+    EMU_LAUNCH("digit_hist1", s, k_digit_hist1<H><<<grid_of(n, 256, kNumSMs * 8), 256, 0, s>>>(
+                                     hi0, lo0, n, ps.word[0], ps.shift[0], hist));
   }
-  EMU_CUDA(cudaMemsetAsync(hist, 0, 4 * 16 * 256, s));
-  EMU_LAUNCH("digit_hist", s,
-             k_digit_hist<H><<<grid_of(n, 256, kNumSMs * 4), 256, ps.n * 256 * 4, s>>>(hi0, lo0, n, ps, hist));
-  std::vector<unsigned int> hh(16 * 256), gs(16 * 256);
-  EMU_CUDA(cudaMemcpyAsync(hh.data(), hist, 4 * 16 * 256, cudaMemcpyDeviceToHost, s));
-  EMU_CUDA(cudaStreamSynchronize(s));
-  for (int p = 0; p < ps.n; p++) {  // global digit starts of every pass
-    unsigned acc = 0;
-    for (int d = 0; d < 256; d++) {
-      gs[p * 256 + d] = acc;
-      acc += hh[p * 256 + d];
-    }
-  }
-  EMU_CUDA(cudaMemcpyAsync(gst, gs.data(), 4 * 16 * 256, cudaMemcpyHostToDevice, s));
   EMU_CUDA(cudaMemsetAsync(tile_ctr, 0, 4 * 16, s));
   mark("keys+hist");
   // LSD passes
@@ -789,16 +882,15 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
     EMU_CUDA(cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem));
   }
   for (int p = 0; p < ps.n; p++) {
-    const unsigned int mx = *std::max_element(hh.begin() + p * 256, hh.begin() + (p + 1) * 256);
-    if ((int64_t)mx == n) continue;  // all records share this digit: pass is the identity
     if (onesweep) {
       EMU_CUDA(cudaMemsetAsync(look, 0, sizeof(unsigned int) * 256 * nblk, s));
       EMU_LAUNCH("onesweep", s, k_onesweep<H><<<(unsigned)nblk, kRThreads, osmem, s>>>(
-                                    hi0, lo0, hi1, lo1, n, ps.shift[p], ps.word[p], gst + p * 256, look, tile_ctr + p));
+                                    hi0, lo0, hi1, lo1, n, ps.shift[p], ps.word[p], hist + p * 256, look, tile_ctr + p,
+                                    p + 1 < ps.n ? hist + (p + 1) * 256 : nullptr, ps.shift[p + 1], ps.word[p + 1]));
     } else {
       if constexpr (std::is_same<H, uint64_t>::value) {
         const uint64_t* key = ps.word[p] ? hi0 : lo0;
-        EMU_LAUNCH("radix_up", s, k_radix_up<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.shift[p], n, nblk, counts));
+        EMU_LAUNCH("radix_up", s, k_radix_up<<<(unsigned)nblk, kRThreads, 0, s>>>(key, ps.word[p] ? ~(1ULL << 63) : ~0ULL, ps.shift[p], n, nblk, counts));
         EMU_CUDA(device_excl_scan<unsigned int>(
             [counts] __device__(int64_t i) { return counts[i]; },
             [counts] __device__(int64_t i, unsigned int ex) { counts[i] = ex; }, ncount, partial, total_dev, s));
@@ -815,19 +907,19 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   mark("radix sort");
   if (dense) {
     EMU_LAUNCH("dense_count", s, k_dense_count<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(hi0, lo0, n, kb, dcnt));
-    rc = segment_dense<H>(lo0, n, cbits, kb, dcnt, part64, tot64, partial, total_dev, small + 2, s, tab);
+    rc = segment_dense<H>(hi0, lo0, n, cbits, kb, dcnt, part64, tot64, partial, total_dev, small + 2, s, tab);
     mark("segment (dense)");
     return rc;
   }
   // combined table = sorted run; decode/mixed = stable partition by phase
   if ((rc = segment<H>(hi0, lo0, n, cbits, partial, total_dev, small + 2, s, tab[2]))) return rc;
   mark("segment combined");
-  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn{lo0}, [] __device__(int64_t, unsigned int) {}, n, partial,
+  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn<H>{hi0}, [] __device__(int64_t, unsigned int) {}, n, partial,
                                           total_dev, s));
   unsigned int n_dec = 0;
   EMU_CUDA(cudaMemcpyAsync(&n_dec, total_dev, 4, cudaMemcpyDeviceToHost, s));
   EMU_CUDA(cudaStreamSynchronize(s));
-  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn{lo0}, PhaseOut<H>{hi0, lo0, hi1, lo1, hi1 + n_dec, lo1 + n_dec}, n,
+  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn<H>{hi0}, PhaseOut<H>{hi0, lo0, hi1, lo1, hi1 + n_dec, lo1 + n_dec}, n,
                                           partial, total_dev, s));
   mark("phase partition");
   if ((rc = segment<H>(hi1, lo1, n_dec, cbits, partial, total_dev, small + 2, s, tab[0]))) return rc;
@@ -947,7 +1039,7 @@ extern "C" int emu_tables_build(const int32_t* tt, const int32_t* conc, const ui
     return EMU_OK;
   };
   const std::function<void(const char*)> mark_fn = mark;
-  if (tbits + cbits <= 32 && n < (1LL << 30))
+  if (tbits + cbits <= 31 && n < (1LL << 30))  // bit 31 carries the phase
     rc = sort_and_segment<uint32_t>(r, n, canonical != 0, cbits, tbits, s, t->tab, alloc_fn, total_dev, small, mark_fn);
   else
     rc = sort_and_segment<uint64_t>(r, n, canonical != 0, cbits, tbits, s, t->tab, alloc_fn, total_dev, small, mark_fn);

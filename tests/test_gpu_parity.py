@@ -120,6 +120,29 @@ def test_gpu_build_edge_cases():
                 assert soa_equal(got, w)
 
 
+@pytest.mark.gpu
+def test_gpu_build_constant_digits():
+    """Digit positions that never vary are skipped: float32-valued latencies
+    (low mantissa digits all zero -> the first pass is not the guessed one),
+    a single bucket key (no key passes), identical records (no pass at all)."""
+    rng = np.random.default_rng(11)
+    n = 50_000
+    conc = rng.integers(1, 300, n)
+    ph = rng.integers(0, 2, n)
+    tt = np.where(ph == 0, conc, conc + rng.integers(0, 4000, n))
+    cases = [
+        (tt, conc, ph, rng.random(n).astype(np.float32).astype(np.float64) + 1.0),
+        (np.full(n, 9), np.full(n, 4), np.zeros(n, np.int64), rng.random(n) + 1e-3),
+        (np.full(n, 9), np.full(n, 4), np.ones(n, np.int64), np.full(n, 0.25)),
+        (tt, conc, ph, np.full(n, 0.125)),
+    ]
+    for args in cases:
+        for canonical in (True, False):
+            pack = build_pack_arrays(*args, 4, canonical=canonical)
+            for got, w in zip(pack.soas(), O.build(*args, canonical=canonical)):
+                assert soa_equal(got, w)
+
+
 @pytest.mark.parametrize("bad,index,msg", [
     (dict(lat=0.0), 1, "latency_s must be > 0, got 0.0"),
     (dict(lat=-1.0), 1, "latency_s must be > 0, got -1.0"),

@@ -3,7 +3,7 @@
 usage: ncu -i rep --page source --csv --print-source cuda,sass -k regex:K > x.csv
        python tools/ncu_lines.py x.csv [top]
 """
-import csv, sys
+import csv, os, sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
@@ -36,5 +36,6 @@ for r in rows:
 ti = sum(v[0] for v in agg.values()) or 1
 ts = sum(v[1] for v in agg.values()) or 1
 print(f"total warp inst {ti:.4g}, stall samples {ts:.4g}")
-for (f, l), (i, s, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+col = 1 if os.environ.get("SORT") == "stall" else 0
+for (f, l), (i, s, src) in sorted(agg.items(), key=lambda kv: -kv[1][col])[:top]:
     print(f"{100 * i / ti:6.2f}% inst {100 * s / ts:6.2f}% stall  {f}:{l}  {src}")
