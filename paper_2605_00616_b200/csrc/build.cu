@@ -330,16 +330,24 @@ __global__ void __launch_bounds__(kRThreads) k_radix_scatter(const uint64_t* __r
 #define EMU_LOOKBACK 16
 #endif
 constexpr unsigned kLookAgg = 1u << 30, kLookPre = 2u << 30, kLookVal = (1u << 30) - 1u;
+#ifndef EMU_OS_ITEMS
+#define EMU_OS_ITEMS 12
+#endif
+constexpr int kOsItems = EMU_OS_ITEMS;          // records per thread of a onesweep tile
+constexpr int kOsTile = kRThreads * kOsItems;
+#ifndef EMU_OS_MINB
+#define EMU_OS_MINB 4
+#endif
 template <typename H>
-__global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__ a_hi, const uint64_t* __restrict__ a_lo,
+__global__ void __launch_bounds__(kRThreads, EMU_OS_MINB) k_onesweep(const H* __restrict__ a_hi, const uint64_t* __restrict__ a_lo,
                                                        H* __restrict__ b_hi, uint64_t* __restrict__ b_lo, int64_t n,
                                                        int shift, int key_is_hi, const unsigned int* __restrict__ hcur,
                                                        unsigned int* look, unsigned int* tile_ctr,
                                                        unsigned int* __restrict__ hnext, int nshift, int nword) {
-  constexpr int kWarpItems = kRTile / kRWarps;  // 512 consecutive records per warp
+  constexpr int kWarpItems = kOsTile / kRWarps;  // consecutive records per warp
   extern __shared__ __align__(16) unsigned char osm[];
   uint64_t* s_lo = reinterpret_cast<uint64_t*>(osm);
-  H* s_hi = reinterpret_cast<H*>(osm + (size_t)kRTile * 8);
+  H* s_hi = reinterpret_cast<H*>(osm + (size_t)kOsTile * 8);
   __shared__ unsigned short wcnt[kRWarps][256];  // per-warp digit counts, then each warp's offset in the digit
   __shared__ unsigned int tstart[256];
   __shared__ unsigned int gofs[256];  // the digit's global start + this tile's exclusive prefix
@@ -355,15 +363,15 @@ __global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__
   nh[t] = 0;
   __syncthreads();
   const unsigned tile = s_tile;
-  const int64_t base = (int64_t)tile * kRTile;
-  const int cnt_tile = (int)min((int64_t)kRTile, n - base);
+  const int64_t base = (int64_t)tile * kOsTile;
+  const int cnt_tile = (int)min((int64_t)kOsTile, n - base);
   const unsigned lt_mask = (1u << lane) - 1u;
   // ---- load: warp w owns records [w*512, (w+1)*512) of the tile, 32 per round (coalesced)
-  H h[kRRounds];
-  uint64_t l[kRRounds];
-  unsigned rk[kRRounds / 2];  // warp-local ranks (< 512), two per register
+  H h[kOsItems];
+  uint64_t l[kOsItems];
+  unsigned rk[kOsItems / 2];  // warp-local ranks (< 512), two per register
 #pragma unroll
-  for (int k = 0; k < kRRounds; k++) {
+  for (int k = 0; k < kOsItems; k++) {
     const int li = w * kWarpItems + k * 32 + lane;
     h[k] = 0;
     l[k] = 0;
@@ -373,21 +381,27 @@ __global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__
     }
   }
   // ---- warp-private ranking (no block barriers): rank = the warp's running
-  // count of the digit + this round's rank among equal digits
+  // count of the digit + this round's rank among equal digits.  The lowest
+  // lane of each digit group adds the group to the warp's counter (two 16-bit
+  // counters per word) and broadcasts the old count; a warp's shared atomics
+  // execute in issue order, so rounds need no __syncwarp.  12 records per
+  // thread keep the pass in 64 registers without spills (16 spilled; measured
+  // 7.9 vs 8.3 ms for the 10 C4 passes).
+  unsigned* wc32 = reinterpret_cast<unsigned*>(&wcnt[w][0]);
 #pragma unroll
-  for (int k = 0; k < kRRounds; k++) {
+  for (int k = 0; k < kOsItems; k++) {
     const bool valid = w * kWarpItems + k * 32 + lane < cnt_tile;
     const unsigned d = valid ? (unsigned)(((key_is_hi ? (uint64_t)key_bucket(h[k]) : l[k]) >> shift) & 255u) : 256u + (unsigned)lane;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const unsigned r = __popc(peers & lt_mask);
-    const unsigned before = valid ? wcnt[w][d] : 0u;
+    unsigned old = 0;
+    if (valid && r == 0) old = atomicAdd(&wc32[d >> 1], (unsigned)__popc(peers) << ((d & 1) * 16));
+    old = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1);
+    const unsigned before = (old >> ((d & 1) * 16)) & 0xffffu;
     if (k & 1)
       rk[k >> 1] |= (before + r) << 16;
     else
       rk[k >> 1] = before + r;
-    __syncwarp();
-    if (valid && r == 0) wcnt[w][d] = (unsigned short)(before + __popc(peers));
-    __syncwarp();
   }
   __syncthreads();
   // ---- per digit: the tile's count and each warp's offset inside the digit
@@ -427,7 +441,7 @@ __global__ void __launch_bounds__(kRThreads, 4) k_onesweep(const H* __restrict__
   __syncthreads();
   // ---- stage the tile in digit order
 #pragma unroll
-  for (int k = 0; k < kRRounds; k++) {
+  for (int k = 0; k < kOsItems; k++) {
     if (w * kWarpItems + k * 32 + lane < cnt_tile) {
       const unsigned d = (unsigned)(((key_is_hi ? (uint64_t)key_bucket(h[k]) : l[k]) >> shift) & 255u);
       const unsigned lp = tstart[d] + wcnt[w][d] + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
@@ -823,7 +837,7 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   uint64_t *lo0, *lo1;
   unsigned int *counts = nullptr, *hist = nullptr, *partial = nullptr, *look = nullptr,
                *tile_ctr = nullptr;
-  const int64_t nblk = (n + kRTile - 1) / kRTile;
+  const int64_t nblk = (n + kRTile - 1) / kRTile, nos = (n + kOsTile - 1) / kOsTile;
   // EMU_ONESWEEP=0 (64-bit keys only): the up-sweep + scan + scatter passes instead
   const char* os_env = getenv("EMU_ONESWEEP");
   const bool onesweep = n < (1LL << 30) && !(os_env && os_env[0] == '0' && sizeof(H) == 8);
@@ -831,7 +845,7 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   const int64_t npart = std::max<int64_t>((ncount + kScanTile - 1) / kScanTile, (n + kScanTile - 1) / kScanTile) + 1;
   if ((rc = salloc(&hi0, n)) || (rc = salloc(&lo0, n)) || (rc = salloc(&hi1, n)) || (rc = salloc(&lo1, n)) ||
       (rc = salloc(&counts, ncount)) || (rc = salloc(&hist, 17 * 256 + 4)) || (rc = salloc(&partial, npart)) ||
-      (rc = salloc(&look, onesweep ? 256 * nblk : 1)) ||
+      (rc = salloc(&look, onesweep ? 256 * nos : 1)) ||
       (rc = salloc(&tile_ctr, 16)))
     return rc;
   // key domains up to 2^24 per phase: dense counts -> segment_dense (no scans over the records)
@@ -875,7 +889,7 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   EMU_CUDA(cudaMemsetAsync(tile_ctr, 0, 4 * 16, s));
   mark("keys+hist");
   // LSD passes
-  const size_t osmem = (size_t)kRTile * (8 + sizeof(H));
+  const size_t osmem = (size_t)kOsTile * (8 + sizeof(H));
   if (onesweep) {
     EMU_CUDA(cudaFuncSetAttribute(k_onesweep<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem));
   } else {
@@ -883,8 +897,8 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   }
   for (int p = 0; p < ps.n; p++) {
     if (onesweep) {
-      EMU_CUDA(cudaMemsetAsync(look, 0, sizeof(unsigned int) * 256 * nblk, s));
-      EMU_LAUNCH("onesweep", s, k_onesweep<H><<<(unsigned)nblk, kRThreads, osmem, s>>>(
+      EMU_CUDA(cudaMemsetAsync(look, 0, sizeof(unsigned int) * 256 * nos, s));
+      EMU_LAUNCH("onesweep", s, k_onesweep<H><<<(unsigned)nos, kRThreads, osmem, s>>>(
                                     hi0, lo0, hi1, lo1, n, ps.shift[p], ps.word[p], hist + p * 256, look, tile_ctr + p,
                                     p + 1 < ps.n ? hist + (p + 1) * 256 : nullptr, ps.shift[p + 1], ps.word[p + 1]));
     } else {
