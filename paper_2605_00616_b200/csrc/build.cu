@@ -142,13 +142,14 @@ __device__ __forceinline__ void hist_add(unsigned int* sh, unsigned d, bool v) {
 // is counted by the pass before it (k_onesweep), so the records are read once
 // here instead of once per pass.
 template <typename H>
-__global__ void __launch_bounds__(256) k_make_keys(RecIn r, int cbits, H* __restrict__ hi, uint64_t* __restrict__ lo,
-                                                   int hword, int hshift, unsigned int* hist,
+__global__ void __launch_bounds__(256) k_make_keys(RecIn r, int cbits, int lsb, H* __restrict__ hi,
+                                                   uint64_t* __restrict__ lo, int hword, int hshift, unsigned int* hist,
                                                    unsigned long long* diff) {
   __shared__ unsigned int sh[256];
   sh[threadIdx.x] = 0;
   __syncthreads();
-  const uint64_t k0 = ((uint64_t)(uint32_t)(r.tt[0] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[0] - 1);
+  const uint64_t k0 = (((uint64_t)(uint32_t)(r.tt[0] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[0] - 1))
+                      << lsb | (lsb && r.ph[0] ? 1ULL : 0ULL);
   const uint64_t l0 = (uint64_t)__double_as_longlong(r.lat[0]);
   uint64_t dk = 0, dl = 0;
   for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < r.n; b0 += (int64_t)gridDim.x * blockDim.x) {
@@ -158,7 +159,12 @@ __global__ void __launch_bounds__(256) k_make_keys(RecIn r, int cbits, H* __rest
     if (v) {
       h = ((uint64_t)(uint32_t)(r.tt[i] - 1) << cbits) | (uint64_t)(uint32_t)(r.conc[i] - 1);
       l = (uint64_t)__double_as_longlong(r.lat[i]);
-      hi[i] = (H)h | (r.ph[i] ? (H)1 << (8 * sizeof(H) - 1) : (H)0);
+      if (lsb) {  // canonical dense builds: the phase sorts just below the bucket key
+        h = h << 1 | (r.ph[i] ? 1ULL : 0ULL);
+        hi[i] = (H)h;
+      } else {
+        hi[i] = (H)h | (r.ph[i] ? (H)1 << (8 * sizeof(H) - 1) : (H)0);
+      }
       lo[i] = l;
       dk |= h ^ k0;
       dl |= l ^ l0;
@@ -203,13 +209,15 @@ __global__ void __launch_bounds__(256) k_digit_hist1(const H* __restrict__ hi, c
 // buckets and offsets then come from scans over the domain (segment_dense)
 // instead of scans over the records.
 template <typename H>
-__global__ void k_dense_count(const H* __restrict__ hi, const uint64_t* __restrict__ lo, int64_t n, int kb,
+__global__ void k_dense_count(const H* __restrict__ hi, const uint64_t* __restrict__ lo, int64_t n, int kb, int lsb,
                               unsigned int* __restrict__ dcnt) {
   const int lane = threadIdx.x & 31;
   for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = b0 + threadIdx.x;  // warp-uniform trip count (match_any below)
     const bool v = i < n;
-    const unsigned key = v ? (key_phase(hi[i]) << kb) | (unsigned)key_bucket(hi[i]) : 0xffffffffu - (unsigned)lane;
+    const unsigned key = !v    ? 0xffffffffu - (unsigned)lane
+                         : lsb ? ((unsigned)(hi[i] & 1u) << kb) | (unsigned)(hi[i] >> 1)
+                               : (key_phase(hi[i]) << kb) | (unsigned)key_bucket(hi[i]);
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     if (v && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&dcnt[key], (unsigned)__popc(peers));
   }
@@ -580,8 +588,10 @@ struct DenseOut {
   int32_t* bkt_tt;
   int32_t* bkt_conc;
   int64_t* bkt_off;
+  unsigned int* koff;  // the key's first sample in this table (lsb builds), else null
   __device__ void operator()(int64_t k, uint64_t ex) const {
     if (!in.cnt(k)) return;
+    if (koff) koff[k] = (unsigned int)(ex & 0xffffffffULL);
     const int64_t b = (int64_t)(ex >> 32);
     bkt_tt[b] = (int32_t)(k >> cbits) + 1;
     bkt_conc[b] = (int32_t)(k & ((1LL << cbits) - 1)) + 1;
@@ -606,6 +616,50 @@ struct SampleOut {
       dec[ex] = v;
   }
 };
+
+// Samples of all three tables from a run sorted by (bucket key, phase,
+// latency) -- canonical dense builds: a key's decode records then its mixed
+// records, each ascending.  The phase tables take their sub-runs as they are;
+// the combined bucket is the merge of the two (a record's place = its rank in
+// its own sub-run + the count of the other sub-run's values below it, ties
+// going to decode first -- equal values, so the order among them is moot).
+__device__ __forceinline__ int64_t count_below(const uint64_t* __restrict__ a, int64_t m, uint64_t v, bool inclusive) {
+  int64_t lo = 0, hi = m;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const uint64_t x = a[mid];
+    if (x < v || (inclusive && x == v))
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+template <typename H>
+__global__ void __launch_bounds__(256) k_samples(const H* __restrict__ hi, const uint64_t* __restrict__ lo, int64_t n,
+                                                 int kb, const unsigned int* __restrict__ dcnt,
+                                                 const unsigned int* __restrict__ koff, double* __restrict__ dec,
+                                                 double* __restrict__ mix, double* __restrict__ comb) {
+  const int64_t K = 1LL << kb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = (uint64_t)hi[i], bits = lo[i];
+    const int64_t k = (int64_t)(h >> 1);
+    const int64_t s0 = koff[2 * K + k];  // the key's combined bucket = its run in the sorted records
+    const int64_t na = dcnt[k], nb = dcnt[K + k];
+    const double v = __longlong_as_double((long long)bits);
+    int64_t pos;
+    if (!(h & 1u)) {
+      const int64_t r = i - s0;
+      dec[koff[k] + r] = v;
+      pos = s0 + r + (nb ? count_below(lo + s0 + na, nb, bits, false) : 0);
+    } else {
+      const int64_t r = i - s0 - na;
+      mix[koff[K + k] + r] = v;
+      pos = s0 + r + (na ? count_below(lo + s0, na, bits, true) : 0);
+    }
+    comb[pos] = v;
+  }
+}
 
 __global__ void k_conc_range(const int32_t* c, int64_t n, int* mm) {
   int lo = 0x7fffffff, hi = 0;
@@ -771,7 +825,7 @@ static int segment_finish(TableBuf& tb, int64_t nb, int64_t m, unsigned int* par
 template <typename H>
 static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, int kb, const unsigned int* dcnt,
                          uint64_t* part64, uint64_t* tot64, unsigned int* partial, unsigned int* total_dev,
-                         int* mm_dev, cudaStream_t s, TableBuf* tab) {
+                         int* mm_dev, cudaStream_t s, TableBuf* tab, unsigned int* koff) {
   const int64_t D = 1LL << kb;
   const int64_t np = (D + kScanTile - 1) / kScanTile + 1;
   int rc;
@@ -789,13 +843,19 @@ static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, 
         (rc = palloc(s, &tb.bkt_off, nb + 1)) || (rc = palloc(s, &tb.samples, m)))
       return rc;
     EMU_CUDA(device_excl_scan<uint64_t>(DenseIn{dcnt, dcnt + D, j},
-                                        DenseOut{DenseIn{dcnt, dcnt + D, j}, cbits, tb.bkt_tt, tb.bkt_conc, tb.bkt_off},
+                                        DenseOut{DenseIn{dcnt, dcnt + D, j}, cbits, tb.bkt_tt, tb.bkt_conc, tb.bkt_off,
+                                                 koff ? koff + j * D : nullptr},
                                         D, part64 + j * np, tot64 + j, s));
     int64_t* off_end = tb.bkt_off + nb;
     EMU_LAUNCH("fill_end", s, k_set_i64<<<1, 1, 0, s>>>(off_end, m));
   }
-  EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn<H>{hi}, SampleOut<H>{hi, lo, tab[2].samples, tab[0].samples, tab[1].samples},
-                                          n, partial, total_dev, s));
+  if (koff)  // run sorted by (key, phase, latency): direct placement, no scan over the records
+    EMU_LAUNCH("samples", s, k_samples<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(
+                                 hi, lo, n, kb, dcnt, koff, tab[0].samples, tab[1].samples, tab[2].samples));
+  else
+    EMU_CUDA(device_excl_scan<unsigned int>(PhaseIn<H>{hi},
+                                            SampleOut<H>{hi, lo, tab[2].samples, tab[0].samples, tab[1].samples}, n,
+                                            partial, total_dev, s));
   for (int j = 0; j < 3; j++) {
     const int64_t nb = (int64_t)(tot[j] >> 32), m = (int64_t)(tot[j] & 0xffffffffULL);
     if (nb == 0) {  // empty table (e.g. no mixed records): the shapes segment() gives it
@@ -853,10 +913,14 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   const bool dense = kb <= 24 && getenv("EMU_DENSE_SEGMENT") == nullptr;
   const int64_t D = dense ? (1LL << kb) : 0;
   const int64_t np64 = (D + kScanTile - 1) / kScanTile + 1;
-  unsigned int* dcnt = nullptr;
+  unsigned int *dcnt = nullptr, *koff = nullptr;
   uint64_t *part64 = nullptr, *tot64 = nullptr;
+  // canonical dense builds sort the phase as the lowest key bit (decode before
+  // mixed inside a key) and place every sample directly (k_samples)
+  const int lsb = canonical && dense && getenv("EMU_PHASE_SCAN") == nullptr ? 1 : 0;
   if (dense) {
     if ((rc = salloc(&dcnt, 2 * D)) || (rc = salloc(&part64, 3 * np64)) || (rc = salloc(&tot64, 4))) return rc;
+    if (lsb && (rc = salloc(&koff, 3 * D))) return rc;
     EMU_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned int) * 2 * D, s));
   }
   // keys, the differing bits and the first digit's histogram; then the passes
@@ -865,7 +929,7 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   EMU_CUDA(cudaMemsetAsync(hist, 0, 4 * 17 * 256 + 16, s));  // hist[17][256], then diff[2]
   unsigned long long* diff = reinterpret_cast<unsigned long long*>(hist + 17 * 256);
   EMU_LAUNCH("make_keys", s,
-             k_make_keys<H><<<grid_of(n, 256, kNumSMs * 8), 256, 0, s>>>(r, cbits, hi0, lo0, hword0, 0, hist, diff));
+             k_make_keys<H><<<grid_of(n, 256, kNumSMs * 8), 256, 0, s>>>(r, cbits, lsb, hi0, lo0, hword0, 0, hist, diff));
   unsigned long long dh[2];
   EMU_CUDA(cudaMemcpyAsync(dh, diff, 16, cudaMemcpyDeviceToHost, s));
   EMU_CUDA(cudaStreamSynchronize(s));
@@ -876,7 +940,7 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
         ps.word[ps.n] = 0;
         ps.shift[ps.n++] = sft;
       }
-  for (int sft = 0; sft < tbits + cbits; sft += 8)
+  for (int sft = 0; sft < tbits + cbits + lsb; sft += 8)
     if ((dh[1] >> sft) & 255u) {
       ps.word[ps.n] = 1;
       ps.shift[ps.n++] = sft;
@@ -920,8 +984,8 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   EMU_CUDA(cudaGetLastError());
   mark("radix sort");
   if (dense) {
-    EMU_LAUNCH("dense_count", s, k_dense_count<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(hi0, lo0, n, kb, dcnt));
-    rc = segment_dense<H>(hi0, lo0, n, cbits, kb, dcnt, part64, tot64, partial, total_dev, small + 2, s, tab);
+    EMU_LAUNCH("dense_count", s, k_dense_count<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(hi0, lo0, n, kb, lsb, dcnt));
+    rc = segment_dense<H>(hi0, lo0, n, cbits, kb, dcnt, part64, tot64, partial, total_dev, small + 2, s, tab, koff);
     mark("segment (dense)");
     return rc;
   }
