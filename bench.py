@@ -463,7 +463,9 @@ def run_b200(args):
         line["roofline"] = {"bound": "hbm", "kernel": "k_mark + k_sample + k_sweep + k_sample_list (query stream)",
                             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                             "frac": achieved / peak,
-                            "traffic": sum((ncu_metric(STREAM_KERNELS[k]) or 0.0) for k in stream) or None,
+                            # ncu DRAM bytes per launch x launches per step, for the kernels this step ran
+                            "traffic": sum((ncu_metric(STREAM_KERNELS[k]) or 0.0) * kern[k]["launches_per_step"]
+                                           for k in stream) or None,
                             "bytes_per_query": bpq,
                             "share_of_step": t_stream * 1e3 / max(step_ms, 1e-9),
                             "kernels_ms_per_step": {k: round(v["ms_per_step"], 4) for k, v in kern.items()},
