@@ -120,6 +120,26 @@ def test_gpu_build_edge_cases():
                 assert soa_equal(got, w)
 
 
+def test_gpu_build_shared_keys_merge():
+    """Canonical builds place each sample directly: a key's decode and mixed
+    sub-runs are copied into the phase tables and merged into the combined
+    bucket by rank.  Keys holding thousands of records of BOTH phases, with
+    heavily tied latencies (ties across phases take either order: equal values)."""
+    rng = np.random.default_rng(21)
+    n = 400_000
+    keys = rng.integers(0, 60, n)
+    conc = 1 + keys % 12
+    tt = conc + keys // 12          # tt >= conc: valid for both phases
+    ph = rng.integers(0, 2, n)
+    lat = np.round(rng.random(n) * 64) / 64 + 0.001   # 65 distinct values: ties everywhere
+    distinct = rng.random(n) < 0.3
+    lat[distinct] = rng.random(int(distinct.sum())) + 0.001   # and 30 % distinct values among them
+    for canonical in (True, False):
+        pack = build_pack_arrays(tt, conc, ph, lat, 4, canonical=canonical)
+        for got, w in zip(pack.soas(), O.build(tt, conc, ph, lat, canonical=canonical)):
+            assert soa_equal(got, w)
+
+
 @pytest.mark.gpu
 def test_gpu_build_constant_digits():
     """Digit positions that never vary are skipped: float32-valued latencies
