@@ -661,6 +661,209 @@ __global__ void __launch_bounds__(256) k_samples(const H* __restrict__ hi, const
   }
 }
 
+// ---- key-first canonical builds: the records are sorted by (bucket key,
+// phase) only (3 passes instead of 10); each (key, phase) sub-run is then
+// sorted by latency on its own.  Sub-runs of <= 256 records: one warp, rank by
+// counting in shared memory; <= 4096: one CTA, bitonic sort in shared memory;
+// larger (the hot decode keys): split into ~256-record bins by the value's
+// place between the sub-run's min and max (monotone, so bins are ordered),
+// scattered into place, and each bin sorted like a small sub-run.  A bin over
+// 4096 records (heavy ties / clustered values) sets a flag and the build falls
+// back to the full LSD passes.
+struct SegItem {
+  int64_t start;  // first record of the run in the sorted-by-key order
+  int32_t count;
+  int32_t src1;   // 1: the run already sits in the output array (a bin), 0: read it from the key-sorted array
+};
+constexpr int kSegSmall = 256, kSegMedium = 4096, kSegBin = 256;
+struct SegCtl {
+  int n_small, n_medium, n_large, oversize;
+  int next_small, next_medium;
+  int pad[2];
+};
+
+__global__ void k_seg_classify(const unsigned int* __restrict__ dcnt, const unsigned int* __restrict__ comb_off,
+                               int64_t K, const uint64_t* __restrict__ lo_in, uint64_t* __restrict__ lo_out,
+                               SegItem* small, SegItem* medium, SegItem* large, SegCtl* ctl) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < 2 * K; j += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned c = dcnt[j];
+    if (!c) continue;
+    const int64_t k = j < K ? j : j - K;
+    const int64_t st = (int64_t)comb_off[k] + (j < K ? 0 : (int64_t)dcnt[k]);
+    if (c == 1) {
+      lo_out[st] = lo_in[st];
+      continue;
+    }
+    const SegItem it{st, (int32_t)c, 0};
+    if (c <= (unsigned)kSegSmall)
+      small[atomicAdd(&ctl->n_small, 1)] = it;
+    else if (c <= (unsigned)kSegMedium)
+      medium[atomicAdd(&ctl->n_medium, 1)] = it;
+    else
+      large[atomicAdd(&ctl->n_large, 1)] = it;
+  }
+}
+
+// Per large sub-run: min and max of the latency bits (positive doubles order
+// like their bit patterns) and its number of bins.
+__global__ void __launch_bounds__(256) k_seg_minmax(const SegItem* __restrict__ large, const SegCtl* __restrict__ ctl,
+                                                    const uint64_t* __restrict__ lo, uint64_t* mn, uint64_t* mx) {
+  __shared__ uint64_t smn[8], smx[8];
+  for (int it = blockIdx.x; it < ctl->n_large; it += gridDim.x) {
+    const SegItem g = large[it];
+    uint64_t a = ~0ULL, b = 0;
+    for (int64_t i = threadIdx.x; i < g.count; i += blockDim.x) {
+      const uint64_t v = lo[g.start + i];
+      a = v < a ? v : a;
+      b = v > b ? v : b;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x = __shfl_xor_sync(0xffffffffu, a, o), y = __shfl_xor_sync(0xffffffffu, b, o);
+      a = x < a ? x : a;
+      b = y > b ? y : b;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      smn[threadIdx.x >> 5] = a;
+      smx[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; w++) {
+        a = smn[w] < a ? smn[w] : a;
+        b = smx[w] > b ? smx[w] : b;
+      }
+      a = smn[0] < a ? smn[0] : a;
+      b = smx[0] > b ? smx[0] : b;
+      mn[it] = a;
+      mx[it] = b;
+    }
+    __syncthreads();
+  }
+}
+
+// Bin bases of the large sub-runs (one CTA: a handful of items).
+__global__ void k_seg_binbase(const SegItem* __restrict__ large, const SegCtl* __restrict__ ctl,
+                              int64_t* __restrict__ bbase, int64_t* total) {
+  if (threadIdx.x != 0) return;
+  int64_t acc = 0;
+  for (int it = 0; it < ctl->n_large; it++) {
+    bbase[it] = acc;
+    acc += (large[it].count + kSegBin - 1) / kSegBin;
+  }
+  *total = acc;
+}
+
+__device__ __forceinline__ int64_t seg_bin_of(uint64_t v, uint64_t a, uint64_t b, int64_t nb) {
+  if (b == a) return 0;
+  const double x = (__longlong_as_double((long long)v) - __longlong_as_double((long long)a)) /
+                   (__longlong_as_double((long long)b) - __longlong_as_double((long long)a)) * (double)nb;
+  if (!(x >= 0.0)) return v == b ? nb - 1 : 0;  // an infinite maximum: inf - inf
+  const int64_t k = x < (double)nb ? (int64_t)x : nb - 1;  // monotone non-decreasing in v
+  return k;
+}
+
+// pass 0: count records per bin; pass 1: scatter them into place (bin order).
+template <int PASS>
+__global__ void __launch_bounds__(256) k_seg_bins(const SegItem* __restrict__ large, const SegCtl* __restrict__ ctl,
+                                                  const uint64_t* __restrict__ mn, const uint64_t* __restrict__ mx,
+                                                  const int64_t* __restrict__ bbase, const uint64_t* __restrict__ lo,
+                                                  unsigned int* bcnt, const unsigned int* __restrict__ boff,
+                                                  uint64_t* __restrict__ out) {
+  for (int it = blockIdx.y; it < ctl->n_large; it += gridDim.y) {
+    const SegItem g = large[it];
+    const uint64_t a = mn[it], b = mx[it];
+    const int64_t nb = (g.count + kSegBin - 1) / kSegBin, base = bbase[it];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.count; i += (int64_t)gridDim.x * blockDim.x) {
+      const uint64_t v = lo[g.start + i];
+      const int64_t bin = base + seg_bin_of(v, a, b, nb);
+      if (PASS == 0) {
+        atomicAdd(&bcnt[bin], 1u);
+      } else {
+        const unsigned r = atomicAdd(&bcnt[bin], 1u);
+        out[g.start + (int64_t)(boff[bin] - boff[base]) + r] = v;
+      }
+    }
+  }
+}
+
+// The bins of every large sub-run as sort items (their records already sit in
+// the output array, in place).
+__global__ void k_seg_binitems(const SegItem* __restrict__ large, const SegCtl* __restrict__ ctl_in,
+                               const int64_t* __restrict__ bbase, const unsigned int* __restrict__ bcnt,
+                               const unsigned int* __restrict__ boff, SegItem* small, SegItem* medium, SegCtl* ctl) {
+  for (int it = blockIdx.y; it < ctl_in->n_large; it += gridDim.y) {
+    const SegItem g = large[it];
+    const int64_t nb = (g.count + kSegBin - 1) / kSegBin, base = bbase[it];
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nb; q += (int64_t)gridDim.x * blockDim.x) {
+      const unsigned c = bcnt[base + q];
+      if (c <= 1) continue;
+      const SegItem b{g.start + (int64_t)(boff[base + q] - boff[base]), (int32_t)c, 1};
+      if (c <= (unsigned)kSegSmall)
+        small[atomicAdd(&ctl->n_small, 1)] = b;
+      else if (c <= (unsigned)kSegMedium)
+        medium[atomicAdd(&ctl->n_medium, 1)] = b;
+      else
+        atomicExch(&ctl->oversize, 1);
+    }
+  }
+}
+
+// One warp per run of <= 256 records: rank by counting (ties by position).
+__global__ void __launch_bounds__(256) k_seg_sort_small(const SegItem* __restrict__ items, SegCtl* ctl,
+                                                        const uint64_t* __restrict__ lo_in, uint64_t* lo_out) {
+  __shared__ uint64_t sm[8][kSegSmall];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n_items = ctl->n_small;
+  for (int it = blockIdx.x * 8 + w; it < n_items; it += gridDim.x * 8) {
+    const SegItem g = items[it];
+    const uint64_t* src = g.src1 ? lo_out : lo_in;
+    for (int e = lane; e < g.count; e += 32) sm[w][e] = src[g.start + e];
+    __syncwarp();
+    for (int e = lane; e < g.count; e += 32) {
+      const uint64_t v = sm[w][e];
+      int r = 0;
+      for (int x = 0; x < g.count; x++) {
+        const uint64_t u = sm[w][x];
+        r += (u < v || (u == v && x < e)) ? 1 : 0;
+      }
+      lo_out[g.start + r] = v;
+    }
+    __syncwarp();
+  }
+}
+
+// One CTA per run of <= 4096 records: bitonic sort in shared memory.
+__global__ void __launch_bounds__(256) k_seg_sort_medium(const SegItem* __restrict__ items, SegCtl* ctl,
+                                                         const uint64_t* __restrict__ lo_in, uint64_t* lo_out) {
+  extern __shared__ uint64_t sv[];  // [kSegMedium]
+  const int n_items = ctl->n_medium;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const SegItem g = items[it];
+    const uint64_t* src = g.src1 ? lo_out : lo_in;
+    int P = 1;
+    while (P < g.count) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sv[i] = i < g.count ? src[g.start + i] : ~0ULL;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          const int l = i ^ j;
+          if (l > i) {
+            const uint64_t a = sv[i], b = sv[l];
+            if ((a > b) == ((i & k) == 0)) {
+              sv[i] = b;
+              sv[l] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < g.count; i += blockDim.x) lo_out[g.start + i] = sv[i];
+    __syncthreads();
+  }
+}
+
 __global__ void k_conc_range(const int32_t* c, int64_t n, int* mm) {
   int lo = 0x7fffffff, hi = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -819,13 +1022,27 @@ static int segment_finish(TableBuf& tb, int64_t nb, int64_t m, unsigned int* par
   return build_search_index(tb, htt.data(), hcc.data(), hoff.data(), s);
 }
 
+// Scratch of the key-first latency sort (all null: the run is fully sorted).
+struct SegScratch {
+  uint64_t* lo_out = nullptr;  // the sorted latencies (k_samples reads them)
+  SegItem *small = nullptr, *medium = nullptr, *large = nullptr;
+  SegCtl* ctl = nullptr;
+  uint64_t *mn = nullptr, *mx = nullptr;
+  int64_t* bbase = nullptr;  // [cap_large + 1]: the last entry is the bin total
+  unsigned int *bcnt = nullptr, *boff = nullptr;
+  int64_t nbins_cap = 0;
+};
+constexpr int kSegFallback = 1000;  // a latency bin too big to sort in shared memory: redo with the full passes
+
 // The three tables from the dense per-(phase, key) counts and the sorted
 // records: one packed scan over the key domain per table (buckets, offsets),
-// one scan over the records for all samples, then rows / ranges / index.
+// then every sample placed directly (canonical) or one scan over the records
+// (capture order), then rows / ranges / index.
+
 template <typename H>
 static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, int kb, const unsigned int* dcnt,
                          uint64_t* part64, uint64_t* tot64, unsigned int* partial, unsigned int* total_dev,
-                         int* mm_dev, cudaStream_t s, TableBuf* tab, unsigned int* koff) {
+                         int* mm_dev, cudaStream_t s, TableBuf* tab, unsigned int* koff, const SegScratch& sg) {
   const int64_t D = 1LL << kb;
   const int64_t np = (D + kScanTile - 1) / kScanTile + 1;
   int rc;
@@ -848,6 +1065,43 @@ static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, 
                                         D, part64 + j * np, tot64 + j, s));
     int64_t* off_end = tb.bkt_off + nb;
     EMU_LAUNCH("fill_end", s, k_set_i64<<<1, 1, 0, s>>>(off_end, m));
+  }
+  if (sg.lo_out) {  // key-first: sort every (key, phase) sub-run by latency into sg.lo_out
+    EMU_CUDA(cudaMemsetAsync(sg.ctl, 0, sizeof(SegCtl), s));
+    EMU_LAUNCH("seg_classify", s, k_seg_classify<<<grid_of(2 * D, 256, kNumSMs * 16), 256, 0, s>>>(
+                                      dcnt, koff + 2 * D, D, lo, sg.lo_out, sg.small, sg.medium, sg.large, sg.ctl));
+    SegCtl hc;
+    EMU_CUDA(cudaMemcpyAsync(&hc, sg.ctl, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    EMU_CUDA(cudaStreamSynchronize(s));
+    if (hc.n_large > 0) {
+      const unsigned gy = (unsigned)std::min(hc.n_large, 65535);
+      EMU_LAUNCH("seg_minmax", s, k_seg_minmax<<<std::min(hc.n_large, kNumSMs * 8), 256, 0, s>>>(
+                                      sg.large, sg.ctl, lo, sg.mn, sg.mx));
+      EMU_LAUNCH("seg_binbase", s, k_seg_binbase<<<1, 32, 0, s>>>(sg.large, sg.ctl, sg.bbase, sg.bbase + hc.n_large));
+      EMU_CUDA(cudaMemsetAsync(sg.bcnt, 0, sizeof(unsigned int) * sg.nbins_cap, s));
+      const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (int64_t)kNumSMs * 16 / gy + 1));
+      EMU_LAUNCH("seg_bins", s, k_seg_bins<0><<<dim3(gx, gy), 256, 0, s>>>(sg.large, sg.ctl, sg.mn, sg.mx, sg.bbase,
+                                                                            lo, sg.bcnt, sg.boff, sg.lo_out));
+      const unsigned int* bc = sg.bcnt;
+      unsigned int* bo = sg.boff;
+      EMU_CUDA(device_excl_scan<unsigned int>([bc] __device__(int64_t i) { return bc[i]; },
+                                              [bo] __device__(int64_t i, unsigned int ex) { bo[i] = ex; },
+                                              sg.nbins_cap, partial, total_dev, s));
+      EMU_CUDA(cudaMemsetAsync(sg.bcnt, 0, sizeof(unsigned int) * sg.nbins_cap, s));
+      EMU_LAUNCH("seg_bins", s, k_seg_bins<1><<<dim3(gx, gy), 256, 0, s>>>(sg.large, sg.ctl, sg.mn, sg.mx, sg.bbase,
+                                                                            lo, sg.bcnt, sg.boff, sg.lo_out));
+      EMU_LAUNCH("seg_binitems", s, k_seg_binitems<<<dim3(16, gy), 256, 0, s>>>(sg.large, sg.ctl, sg.bbase, sg.bcnt,
+                                                                                 sg.boff, sg.small, sg.medium, sg.ctl));
+    }
+    EMU_LAUNCH("seg_sort_small", s, k_seg_sort_small<<<kNumSMs * 8, 256, 0, s>>>(sg.small, sg.ctl, lo, sg.lo_out));
+    EMU_CUDA(cudaFuncSetAttribute(k_seg_sort_medium, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kSegMedium * sizeof(uint64_t))));
+    EMU_LAUNCH("seg_sort_medium", s, k_seg_sort_medium<<<kNumSMs * 4, 256, kSegMedium * sizeof(uint64_t), s>>>(
+                                         sg.medium, sg.ctl, lo, sg.lo_out));
+    EMU_CUDA(cudaMemcpyAsync(&hc, sg.ctl, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    EMU_CUDA(cudaStreamSynchronize(s));
+    if (hc.oversize) return kSegFallback;
+    lo = sg.lo_out;
   }
   if (koff)  // run sorted by (key, phase, latency): direct placement, no scan over the records
     EMU_LAUNCH("samples", s, k_samples<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(
@@ -888,7 +1142,7 @@ namespace emu {
 template <typename H>
 static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits, int tbits, cudaStream_t s,
                             TableBuf* tab, const std::function<int(void**, size_t)>& alloc, unsigned int* total_dev,
-                            int* small, const std::function<void(const char*)>& mark) {
+                            int* small, const std::function<void(const char*)>& mark, bool allow_kf = true) {
   int rc;
   auto salloc = [&](auto** p, int64_t count) -> int {
     return alloc(reinterpret_cast<void**>(p), sizeof(**p) * (size_t)(count > 0 ? count : 1));
@@ -918,14 +1172,32 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   // canonical dense builds sort the phase as the lowest key bit (decode before
   // mixed inside a key) and place every sample directly (k_samples)
   const int lsb = canonical && dense && getenv("EMU_PHASE_SCAN") == nullptr ? 1 : 0;
+  // key-first (canonical dense builds): sort by (key, phase) only, then each
+  // sub-run by latency in shared memory (EMU_BUILD_KF=1; default: all passes)
+  static const bool kf_env = [] {
+    const char* e = getenv("EMU_BUILD_KF");
+    return e && e[0] == '1';
+  }();
+  const bool kf = lsb && allow_kf && kf_env;
+  SegScratch sg;
   if (dense) {
     if ((rc = salloc(&dcnt, 2 * D)) || (rc = salloc(&part64, 3 * np64)) || (rc = salloc(&tot64, 4))) return rc;
     if (lsb && (rc = salloc(&koff, 3 * D))) return rc;
     EMU_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned int) * 2 * D, s));
   }
+  if (kf) {
+    const int64_t runs = std::min<int64_t>(2 * D, n), cap_large = n / kSegMedium + 1;
+    sg.nbins_cap = n / kSegBin + cap_large + 1;
+    if ((rc = salloc(&sg.lo_out, n)) || (rc = salloc(&sg.small, runs + sg.nbins_cap)) ||
+        (rc = salloc(&sg.medium, runs + sg.nbins_cap)) || (rc = salloc(&sg.large, cap_large)) ||
+        (rc = salloc(&sg.ctl, 1)) || (rc = salloc(&sg.mn, cap_large)) || (rc = salloc(&sg.mx, cap_large)) ||
+        (rc = salloc(&sg.bbase, cap_large + 1)) || (rc = salloc(&sg.bcnt, sg.nbins_cap)) ||
+        (rc = salloc(&sg.boff, sg.nbins_cap)))
+      return rc;
+  }
   // keys, the differing bits and the first digit's histogram; then the passes
   // are the digit positions in which some record differs from record 0
-  const int hword0 = canonical ? 0 : 1;
+  const int hword0 = canonical && !kf ? 0 : 1;
   EMU_CUDA(cudaMemsetAsync(hist, 0, 4 * 17 * 256 + 16, s));  // hist[17][256], then diff[2]
   unsigned long long* diff = reinterpret_cast<unsigned long long*>(hist + 17 * 256);
   EMU_LAUNCH("make_keys", s,
@@ -934,7 +1206,7 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   EMU_CUDA(cudaMemcpyAsync(dh, diff, 16, cudaMemcpyDeviceToHost, s));
   EMU_CUDA(cudaStreamSynchronize(s));
   PassSet ps{};
-  if (canonical)
+  if (canonical && !kf)
     for (int sft = 0; sft < 64; sft += 8)
       if ((dh[0] >> sft) & 255u) {
         ps.word[ps.n] = 0;
@@ -985,8 +1257,13 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   mark("radix sort");
   if (dense) {
     EMU_LAUNCH("dense_count", s, k_dense_count<H><<<grid_of(n, 256, kNumSMs * 16), 256, 0, s>>>(hi0, lo0, n, kb, lsb, dcnt));
-    rc = segment_dense<H>(hi0, lo0, n, cbits, kb, dcnt, part64, tot64, partial, total_dev, small + 2, s, tab, koff);
+    rc = segment_dense<H>(hi0, lo0, n, cbits, kb, dcnt, part64, tot64, partial, total_dev, small + 2, s, tab, koff,
+                          sg);
     mark("segment (dense)");
+    if (rc == kSegFallback) {  // a latency bin over 4096 records: the full LSD passes instead
+      for (int j = 0; j < 3; j++) tab[j].release();
+      return sort_and_segment<H>(r, n, canonical, cbits, tbits, s, tab, alloc, total_dev, small, mark, false);
+    }
     return rc;
   }
   // combined table = sorted run; decode/mixed = stable partition by phase

@@ -140,6 +140,25 @@ def test_gpu_build_shared_keys_merge():
             assert soa_equal(got, w)
 
 
+@pytest.mark.parametrize("tied", [0.0, 0.4])
+def test_gpu_build_large_subruns(tied):
+    """Canonical builds sort by (key, phase) first, then each sub-run by
+    latency: sub-runs over 4096 records are split into bins by value.  A tied
+    value holding 40 % of a sub-run makes a bin too big for shared memory and
+    the build falls back to the full radix passes -- same tables either way."""
+    rng = np.random.default_rng(31)
+    n = 300_000
+    keys = rng.integers(0, 6, n)
+    conc = 1 + keys
+    tt = conc + 3
+    ph = rng.integers(0, 2, n)
+    lat = np.exp(rng.normal(-4.0, 0.3, n))
+    lat[rng.random(n) < tied] = 0.02
+    pack = build_pack_arrays(tt, conc, ph, lat, 4, canonical=True)
+    for got, w in zip(pack.soas(), O.build(tt, conc, ph, lat, canonical=True)):
+        assert soa_equal(got, w)
+
+
 @pytest.mark.gpu
 def test_gpu_build_constant_digits():
     """Digit positions that never vary are skipped: float32-valued latencies
