@@ -661,21 +661,29 @@ __global__ void __launch_bounds__(256) k_samples(const H* __restrict__ hi, const
   }
 }
 
-// ---- key-first canonical builds: the records are sorted by (bucket key,
-// phase) only (3 passes instead of 10); each (key, phase) sub-run is then
-// sorted by latency on its own.  Sub-runs of <= 256 records: one warp, rank by
-// counting in shared memory; <= 4096: one CTA, bitonic sort in shared memory;
-// larger (the hot decode keys): split into ~256-record bins by the value's
-// place between the sub-run's min and max (monotone, so bins are ordered),
-// scattered into place, and each bin sorted like a small sub-run.  A bin over
-// 4096 records (heavy ties / clustered values) sets a flag and the build falls
-// back to the full LSD passes.
+// ---- key-first canonical builds (EMU_BUILD_KF=1; not the default): the
+// records are sorted by (bucket key, phase) only (3 passes instead of 10);
+// each (key, phase) sub-run is then sorted by latency on its own.  Runs of
+// <= 256 records: one warp, bitonic sort held in registers; <= 4096: one CTA,
+// bitonic sort in shared memory; larger (the hot decode keys): split into
+// bins of ~128 records (at most 8192 bins) by the value's place between the
+// sub-run's min and max (monotone, so bins are ordered), scattered into place,
+// and each bin sorted like a run.  A bin over 4096 records (heavy ties,
+// clustered values) sets a flag and the build falls back to the full passes.
+// Measured on C4: 14.3 ms against 10.7 for the full passes -- the 3 key passes
+// take 2.1 ms, but the CTA bitonic sorts of the 257-4096-record bins (5.5 ms)
+// and the two binning passes (2.8 ms) cost more than the 7 latency passes.
 struct SegItem {
   int64_t start;  // first record of the run in the sorted-by-key order
   int32_t count;
   int32_t src1;   // 1: the run already sits in the output array (a bin), 0: read it from the key-sorted array
 };
-constexpr int kSegSmall = 256, kSegMedium = 4096, kSegBin = 256;
+constexpr int kSegSmall = 256, kSegMedium = 4096, kSegBin = 128, kSegSmemBins = 8192;
+// bins of a large sub-run: ~kSegBin records each, at most kSegSmemBins (shared-memory counters)
+__host__ __device__ __forceinline__ int64_t seg_nbins(int64_t c) {
+  const int64_t nb = (c + kSegBin - 1) / kSegBin;
+  return nb < kSegSmemBins ? nb : kSegSmemBins;
+}
 struct SegCtl {
   int n_small, n_medium, n_large, oversize;
   int next_small, next_medium;
@@ -705,40 +713,28 @@ __global__ void k_seg_classify(const unsigned int* __restrict__ dcnt, const unsi
 }
 
 // Per large sub-run: min and max of the latency bits (positive doubles order
-// like their bit patterns) and its number of bins.
+// like their bit patterns); blockIdx.y = sub-run, blockIdx.x = chunk of it.
 __global__ void __launch_bounds__(256) k_seg_minmax(const SegItem* __restrict__ large, const SegCtl* __restrict__ ctl,
-                                                    const uint64_t* __restrict__ lo, uint64_t* mn, uint64_t* mx) {
-  __shared__ uint64_t smn[8], smx[8];
-  for (int it = blockIdx.x; it < ctl->n_large; it += gridDim.x) {
+                                                    const uint64_t* __restrict__ lo, unsigned long long* mn,
+                                                    unsigned long long* mx) {
+  for (int it = blockIdx.y; it < ctl->n_large; it += gridDim.y) {
     const SegItem g = large[it];
-    uint64_t a = ~0ULL, b = 0;
-    for (int64_t i = threadIdx.x; i < g.count; i += blockDim.x) {
-      const uint64_t v = lo[g.start + i];
+    unsigned long long a = ~0ULL, b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.count; i += (int64_t)gridDim.x * blockDim.x) {
+      const unsigned long long v = lo[g.start + i];
       a = v < a ? v : a;
       b = v > b ? v : b;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t x = __shfl_xor_sync(0xffffffffu, a, o), y = __shfl_xor_sync(0xffffffffu, b, o);
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, a, o), y = __shfl_xor_sync(0xffffffffu, b, o);
       a = x < a ? x : a;
       b = y > b ? y : b;
     }
     if ((threadIdx.x & 31) == 0) {
-      smn[threadIdx.x >> 5] = a;
-      smx[threadIdx.x >> 5] = b;
+      atomicMin(&mn[it], a);
+      atomicMax(&mx[it], b);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < 8; w++) {
-        a = smn[w] < a ? smn[w] : a;
-        b = smx[w] > b ? smx[w] : b;
-      }
-      a = smn[0] < a ? smn[0] : a;
-      b = smx[0] > b ? smx[0] : b;
-      mn[it] = a;
-      mx[it] = b;
-    }
-    __syncthreads();
   }
 }
 
@@ -749,7 +745,7 @@ __global__ void k_seg_binbase(const SegItem* __restrict__ large, const SegCtl* _
   int64_t acc = 0;
   for (int it = 0; it < ctl->n_large; it++) {
     bbase[it] = acc;
-    acc += (large[it].count + kSegBin - 1) / kSegBin;
+    acc += seg_nbins(large[it].count);
   }
   *total = acc;
 }
@@ -764,25 +760,47 @@ __device__ __forceinline__ int64_t seg_bin_of(uint64_t v, uint64_t a, uint64_t b
 }
 
 // pass 0: count records per bin; pass 1: scatter them into place (bin order).
+// blockIdx.y = sub-run, blockIdx.x = a contiguous chunk of it.  Sub-runs of
+// count in shared memory and touch the global counters once per (CTA, bin);
+// the chunk is read twice in pass 1 (count, then place: the second read hits L2).
 template <int PASS>
 __global__ void __launch_bounds__(256) k_seg_bins(const SegItem* __restrict__ large, const SegCtl* __restrict__ ctl,
-                                                  const uint64_t* __restrict__ mn, const uint64_t* __restrict__ mx,
+                                                  const unsigned long long* __restrict__ mn,
+                                                  const unsigned long long* __restrict__ mx,
                                                   const int64_t* __restrict__ bbase, const uint64_t* __restrict__ lo,
                                                   unsigned int* bcnt, const unsigned int* __restrict__ boff,
                                                   uint64_t* __restrict__ out) {
+  extern __shared__ unsigned int sh[];  // [kSegSmemBins] counts, then [kSegSmemBins] bases
   for (int it = blockIdx.y; it < ctl->n_large; it += gridDim.y) {
     const SegItem g = large[it];
     const uint64_t a = mn[it], b = mx[it];
-    const int64_t nb = (g.count + kSegBin - 1) / kSegBin, base = bbase[it];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.count; i += (int64_t)gridDim.x * blockDim.x) {
-      const uint64_t v = lo[g.start + i];
-      const int64_t bin = base + seg_bin_of(v, a, b, nb);
+    const int64_t nb = seg_nbins(g.count), base = bbase[it];
+    const int64_t per = (g.count + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = min((int64_t)g.count, (int64_t)blockIdx.x * per), c1 = min((int64_t)g.count, c0 + per);
+    unsigned int* cnt = sh;
+    unsigned int* bas = sh + kSegSmemBins;
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) cnt[q] = 0;
+    __syncthreads();
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x)
+      atomicAdd(&cnt[seg_bin_of(lo[g.start + i], a, b, nb)], 1u);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+      const unsigned c = cnt[q];
       if (PASS == 0) {
-        atomicAdd(&bcnt[bin], 1u);
+        if (c) atomicAdd(&bcnt[base + q], c);
       } else {
-        const unsigned r = atomicAdd(&bcnt[bin], 1u);
-        out[g.start + (int64_t)(boff[bin] - boff[base]) + r] = v;
+        bas[q] = c ? atomicAdd(&bcnt[base + q], c) + (boff[base + q] - boff[base]) : 0u;
+        cnt[q] = 0;
       }
+    }
+    __syncthreads();
+    if (PASS == 1) {
+      for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+        const uint64_t v = lo[g.start + i];
+        const int q = (int)seg_bin_of(v, a, b, nb);
+        out[g.start + (int64_t)bas[q] + atomicAdd(&cnt[q], 1u)] = v;
+      }
+      __syncthreads();
     }
   }
 }
@@ -794,7 +812,7 @@ __global__ void k_seg_binitems(const SegItem* __restrict__ large, const SegCtl* 
                                const unsigned int* __restrict__ boff, SegItem* small, SegItem* medium, SegCtl* ctl) {
   for (int it = blockIdx.y; it < ctl_in->n_large; it += gridDim.y) {
     const SegItem g = large[it];
-    const int64_t nb = (g.count + kSegBin - 1) / kSegBin, base = bbase[it];
+    const int64_t nb = seg_nbins(g.count), base = bbase[it];
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nb; q += (int64_t)gridDim.x * blockDim.x) {
       const unsigned c = bcnt[base + q];
       if (c <= 1) continue;
@@ -809,27 +827,72 @@ __global__ void k_seg_binitems(const SegItem* __restrict__ large, const SegCtl* 
   }
 }
 
-// One warp per run of <= 256 records: rank by counting (ties by position).
-__global__ void __launch_bounds__(256) k_seg_sort_small(const SegItem* __restrict__ items, SegCtl* ctl,
-                                                        const uint64_t* __restrict__ lo_in, uint64_t* lo_out) {
-  __shared__ uint64_t sm[8][kSegSmall];
+// One warp per run of <= kSegSmall records: bitonic sort held in registers
+// (E consecutive elements per lane; partners in other lanes via shuffles,
+// inside a lane via register swaps -- no shared memory, no syncs).
+template <int E>
+__device__ __forceinline__ void warp_bitonic_run(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                                 int64_t start, int n, int lane) {
+  uint64_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int i = lane * E + e;
+    v[e] = i < n ? src[start + i] : ~0ULL;
+  }
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lm = j / E;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], lm);
+          const bool up = ((lane * E + e) & k) == 0;
+          const bool keep_min = lower == up;
+          v[e] = keep_min ? (o < v[e] ? o : v[e]) : (o > v[e] ? o : v[e]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          const int q = e ^ j;
+          if (q > e) {
+            const bool up = ((lane * E + e) & k) == 0;
+            const uint64_t a = v[e], b = v[q];
+            const bool sw = (a > b) == up;
+            v[e] = sw ? b : a;
+            v[q] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int i = lane * E + e;
+    if (i < n) dst[start + i] = v[e];
+  }
+}
+
+constexpr int kSegSmallWarps = 4;
+__global__ void __launch_bounds__(32 * kSegSmallWarps) k_seg_sort_small(const SegItem* __restrict__ items, SegCtl* ctl,
+                                                                       const uint64_t* __restrict__ lo_in,
+                                                                       uint64_t* lo_out) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int n_items = ctl->n_small;
-  for (int it = blockIdx.x * 8 + w; it < n_items; it += gridDim.x * 8) {
+  for (int it = blockIdx.x * kSegSmallWarps + w; it < n_items; it += gridDim.x * kSegSmallWarps) {
     const SegItem g = items[it];
     const uint64_t* src = g.src1 ? lo_out : lo_in;
-    for (int e = lane; e < g.count; e += 32) sm[w][e] = src[g.start + e];
-    __syncwarp();
-    for (int e = lane; e < g.count; e += 32) {
-      const uint64_t v = sm[w][e];
-      int r = 0;
-      for (int x = 0; x < g.count; x++) {
-        const uint64_t u = sm[w][x];
-        r += (u < v || (u == v && x < e)) ? 1 : 0;
-      }
-      lo_out[g.start + r] = v;
-    }
-    __syncwarp();
+    // in place (src == dst) is safe: every lane holds its elements before any store
+    if (g.count <= 32)
+      warp_bitonic_run<1>(src, lo_out, g.start, g.count, lane);
+    else if (g.count <= 64)
+      warp_bitonic_run<2>(src, lo_out, g.start, g.count, lane);
+    else if (g.count <= 128)
+      warp_bitonic_run<4>(src, lo_out, g.start, g.count, lane);
+    else
+      warp_bitonic_run<8>(src, lo_out, g.start, g.count, lane);
   }
 }
 
@@ -1075,12 +1138,19 @@ static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, 
     EMU_CUDA(cudaStreamSynchronize(s));
     if (hc.n_large > 0) {
       const unsigned gy = (unsigned)std::min(hc.n_large, 65535);
-      EMU_LAUNCH("seg_minmax", s, k_seg_minmax<<<std::min(hc.n_large, kNumSMs * 8), 256, 0, s>>>(
-                                      sg.large, sg.ctl, lo, sg.mn, sg.mx));
+      EMU_CUDA(cudaMemsetAsync(sg.mn, 0xff, sizeof(uint64_t) * hc.n_large, s));
+      EMU_CUDA(cudaMemsetAsync(sg.mx, 0, sizeof(uint64_t) * hc.n_large, s));
+      const unsigned gm = (unsigned)std::max<int64_t>(1, std::min<int64_t>(256, (int64_t)kNumSMs * 16 / gy + 1));
+      EMU_LAUNCH("seg_minmax", s, k_seg_minmax<<<dim3(gm, gy), 256, 0, s>>>(
+                                      sg.large, sg.ctl, lo, (unsigned long long*)sg.mn, (unsigned long long*)sg.mx));
       EMU_LAUNCH("seg_binbase", s, k_seg_binbase<<<1, 32, 0, s>>>(sg.large, sg.ctl, sg.bbase, sg.bbase + hc.n_large));
       EMU_CUDA(cudaMemsetAsync(sg.bcnt, 0, sizeof(unsigned int) * sg.nbins_cap, s));
-      const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (int64_t)kNumSMs * 16 / gy + 1));
-      EMU_LAUNCH("seg_bins", s, k_seg_bins<0><<<dim3(gx, gy), 256, 0, s>>>(sg.large, sg.ctl, sg.mn, sg.mx, sg.bbase,
+      const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(256, (int64_t)kNumSMs * 8 / gy + 1));
+      const size_t bsm = 2 * kSegSmemBins * sizeof(unsigned int);
+      EMU_CUDA(cudaFuncSetAttribute(k_seg_bins<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      EMU_CUDA(cudaFuncSetAttribute(k_seg_bins<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      EMU_LAUNCH("seg_bins", s, k_seg_bins<0><<<dim3(gx, gy), 256, bsm, s>>>(sg.large, sg.ctl, (unsigned long long*)sg.mn,
+                                                                            (unsigned long long*)sg.mx, sg.bbase,
                                                                             lo, sg.bcnt, sg.boff, sg.lo_out));
       const unsigned int* bc = sg.bcnt;
       unsigned int* bo = sg.boff;
@@ -1088,12 +1158,14 @@ static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, 
                                               [bo] __device__(int64_t i, unsigned int ex) { bo[i] = ex; },
                                               sg.nbins_cap, partial, total_dev, s));
       EMU_CUDA(cudaMemsetAsync(sg.bcnt, 0, sizeof(unsigned int) * sg.nbins_cap, s));
-      EMU_LAUNCH("seg_bins", s, k_seg_bins<1><<<dim3(gx, gy), 256, 0, s>>>(sg.large, sg.ctl, sg.mn, sg.mx, sg.bbase,
+      EMU_LAUNCH("seg_bins", s, k_seg_bins<1><<<dim3(gx, gy), 256, bsm, s>>>(sg.large, sg.ctl, (unsigned long long*)sg.mn,
+                                                                            (unsigned long long*)sg.mx, sg.bbase,
                                                                             lo, sg.bcnt, sg.boff, sg.lo_out));
       EMU_LAUNCH("seg_binitems", s, k_seg_binitems<<<dim3(16, gy), 256, 0, s>>>(sg.large, sg.ctl, sg.bbase, sg.bcnt,
                                                                                  sg.boff, sg.small, sg.medium, sg.ctl));
     }
-    EMU_LAUNCH("seg_sort_small", s, k_seg_sort_small<<<kNumSMs * 8, 256, 0, s>>>(sg.small, sg.ctl, lo, sg.lo_out));
+    EMU_LAUNCH("seg_sort_small", s, k_seg_sort_small<<<kNumSMs * 12, 32 * kSegSmallWarps, 0, s>>>(sg.small, sg.ctl, lo,
+                                                                                           sg.lo_out));
     EMU_CUDA(cudaFuncSetAttribute(k_seg_sort_medium, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kSegMedium * sizeof(uint64_t))));
     EMU_LAUNCH("seg_sort_medium", s, k_seg_sort_medium<<<kNumSMs * 4, 256, kSegMedium * sizeof(uint64_t), s>>>(

@@ -140,6 +140,20 @@ def test_gpu_build_shared_keys_merge():
             assert soa_equal(got, w)
 
 
+def test_gpu_build_key_first_mode():
+    """The key-first canonical build (EMU_BUILD_KF=1, read once per process):
+    every build test of this file again in a child process with it on."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    env = dict(os.environ, EMU_BUILD_KF="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "build and not key_first"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("tied", [0.0, 0.4])
 def test_gpu_build_large_subruns(tied):
     """Canonical builds sort by (key, phase) first, then each sub-run by
