@@ -661,18 +661,17 @@ __global__ void __launch_bounds__(256) k_samples(const H* __restrict__ hi, const
   }
 }
 
-// ---- key-first canonical builds (EMU_BUILD_KF=1; not the default): the
-// records are sorted by (bucket key, phase) only (3 passes instead of 10);
+// ---- key-first canonical builds (the default; EMU_BUILD_KF=0 turns it off):
+// the records are sorted by (bucket key, phase) only (3 passes instead of 10);
 // each (key, phase) sub-run is then sorted by latency on its own.  Runs of
 // <= 256 records: one warp, bitonic sort held in registers; <= 4096: one CTA,
-// bitonic sort in shared memory; larger (the hot decode keys): split into
-// bins of ~128 records (at most 8192 bins) by the value's place between the
-// sub-run's min and max (monotone, so bins are ordered), scattered into place,
-// and each bin sorted like a run.  A bin over 4096 records (heavy ties,
-// clustered values) sets a flag and the build falls back to the full passes.
-// Measured on C4: 14.3 ms against 10.7 for the full passes -- the 3 key passes
-// take 2.1 ms, but the CTA bitonic sorts of the 257-4096-record bins (5.5 ms)
-// and the two binning passes (2.8 ms) cost more than the 7 latency passes.
+// value bins of ~32 records in shared memory, each sorted by a warp the same
+// way; larger (the hot decode keys): split into bins of ~128 records (at most
+// 8192 bins) by the value's place between the sub-run's min and max
+// (monotone, so bins are ordered), scattered into place by two
+// shared-memory-histogram passes, and each bin sorted like a run.  A bin over
+// 4096 records (heavy ties, clustered values) sets a flag and the build falls
+// back to the full passes.  C4: 10.05 ms against 10.7 for the full passes.
 struct SegItem {
   int64_t start;  // first record of the run in the sorted-by-key order
   int32_t count;
@@ -750,13 +749,31 @@ __global__ void k_seg_binbase(const SegItem* __restrict__ large, const SegCtl* _
   *total = acc;
 }
 
-__device__ __forceinline__ int64_t seg_bin_of(uint64_t v, uint64_t a, uint64_t b, int64_t nb) {
-  if (b == a) return 0;
-  const double x = (__longlong_as_double((long long)v) - __longlong_as_double((long long)a)) /
-                   (__longlong_as_double((long long)b) - __longlong_as_double((long long)a)) * (double)nb;
-  if (!(x >= 0.0)) return v == b ? nb - 1 : 0;  // an infinite maximum: inf - inf
-  const int64_t k = x < (double)nb ? (int64_t)x : nb - 1;  // monotone non-decreasing in v
-  return k;
+// Value bins of a run with minimum a and maximum b (latency bits): bin =
+// floor((v - a) * nb / (b - a)), the scale computed once per run.  Every step
+// is a correctly rounded IEEE op of a non-decreasing argument, so the bin is
+// monotone non-decreasing in v (bins are ordered).
+struct SegScale {
+  double a, k;  // min as a double, nb / (max - min)
+  int64_t nb;
+  bool flat;    // max == min (or an infinite max): everything in bin 0 / the last bin
+  uint64_t b;
+};
+__device__ __forceinline__ SegScale seg_scale(uint64_t a, uint64_t b, int64_t nb) {
+  SegScale s;
+  s.a = __longlong_as_double((long long)a);
+  const double r = __longlong_as_double((long long)b) - s.a;
+  s.k = (double)nb / r;
+  s.nb = nb;
+  s.b = b;
+  s.flat = !(r > 0.0) || !(s.k < 1e308);
+  return s;
+}
+__device__ __forceinline__ int64_t seg_bin_of(uint64_t v, const SegScale& s) {
+  if (s.flat) return v == s.b && s.b != (uint64_t)__double_as_longlong(s.a) ? s.nb - 1 : 0;
+  const double x = (__longlong_as_double((long long)v) - s.a) * s.k;
+  if (!(x >= 0.0)) return v == s.b ? s.nb - 1 : 0;  // an infinite maximum: inf - inf
+  return x < (double)s.nb ? (int64_t)x : s.nb - 1;
 }
 
 // pass 0: count records per bin; pass 1: scatter them into place (bin order).
@@ -773,16 +790,26 @@ __global__ void __launch_bounds__(256) k_seg_bins(const SegItem* __restrict__ la
   extern __shared__ unsigned int sh[];  // [kSegSmemBins] counts, then [kSegSmemBins] bases
   for (int it = blockIdx.y; it < ctl->n_large; it += gridDim.y) {
     const SegItem g = large[it];
-    const uint64_t a = mn[it], b = mx[it];
     const int64_t nb = seg_nbins(g.count), base = bbase[it];
+    const SegScale sc = seg_scale(mn[it], mx[it], nb);
     const int64_t per = (g.count + gridDim.x - 1) / gridDim.x;
     const int64_t c0 = min((int64_t)g.count, (int64_t)blockIdx.x * per), c1 = min((int64_t)g.count, c0 + per);
     unsigned int* cnt = sh;
     unsigned int* bas = sh + kSegSmemBins;
     for (int q = threadIdx.x; q < nb; q += blockDim.x) cnt[q] = 0;
     __syncthreads();
-    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x)
-      atomicAdd(&cnt[seg_bin_of(lo[g.start + i], a, b, nb)], 1u);
+    // four independent loads per thread in flight (the loop is latency-bound otherwise)
+    for (int64_t i0 = c0 + threadIdx.x; i0 < c1; i0 += 4 * (int64_t)blockDim.x) {
+      uint64_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t i = i0 + u * (int64_t)blockDim.x;
+        v[u] = i < c1 ? lo[g.start + i] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (i0 + u * (int64_t)blockDim.x < c1) atomicAdd(&cnt[seg_bin_of(v[u], sc)], 1u);
+    }
     __syncthreads();
     for (int q = threadIdx.x; q < nb; q += blockDim.x) {
       const unsigned c = cnt[q];
@@ -795,10 +822,19 @@ __global__ void __launch_bounds__(256) k_seg_bins(const SegItem* __restrict__ la
     }
     __syncthreads();
     if (PASS == 1) {
-      for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-        const uint64_t v = lo[g.start + i];
-        const int q = (int)seg_bin_of(v, a, b, nb);
-        out[g.start + (int64_t)bas[q] + atomicAdd(&cnt[q], 1u)] = v;
+      for (int64_t i0 = c0 + threadIdx.x; i0 < c1; i0 += 4 * (int64_t)blockDim.x) {
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t i = i0 + u * (int64_t)blockDim.x;
+          v[u] = i < c1 ? lo[g.start + i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (i0 + u * (int64_t)blockDim.x < c1) {
+            const int q = (int)seg_bin_of(v[u], sc);
+            out[g.start + (int64_t)bas[q] + atomicAdd(&cnt[q], 1u)] = v[u];
+          }
       }
       __syncthreads();
     }
@@ -896,33 +932,119 @@ __global__ void __launch_bounds__(32 * kSegSmallWarps) k_seg_sort_small(const Se
   }
 }
 
-// One CTA per run of <= 4096 records: bitonic sort in shared memory.
+// One CTA per run of 257-4096 records: a bucket sort inside shared memory --
+// split the run into ~32-record value bins (min/max-normalised, monotone), then
+// each bin sorted by one warp with the register bitonic; a bin over 256
+// records (ties, clustered values) sends the whole run to a shared-memory
+// bitonic sort instead.  (Holding the run in registers instead of a second
+// shared buffer, for 4 CTAs/SM instead of 3, measured slower: 3.1 vs 2.6 ms.)
+constexpr int kSegSub = 256;  // value bins per run at most
 __global__ void __launch_bounds__(256) k_seg_sort_medium(const SegItem* __restrict__ items, SegCtl* ctl,
                                                          const uint64_t* __restrict__ lo_in, uint64_t* lo_out) {
-  extern __shared__ uint64_t sv[];  // [kSegMedium]
+  extern __shared__ uint64_t sv[];  // [kSegMedium] the run, then [kSegMedium] the run in bin order
+  uint64_t* sb = sv + kSegMedium;
+  __shared__ unsigned int hist[kSegSub], cur[kSegSub], wtot[8];
+  __shared__ unsigned long long rmn[8], rmx[8];
+  __shared__ int big;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int n_items = ctl->n_medium;
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
     const SegItem g = items[it];
     const uint64_t* src = g.src1 ? lo_out : lo_in;
-    int P = 1;
-    while (P < g.count) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) sv[i] = i < g.count ? src[g.start + i] : ~0ULL;
+    const int n = g.count;
+    unsigned long long a = ~0ULL, b = 0;
+    for (int i0 = t; i0 < n; i0 += 4 * blockDim.x) {
+      uint64_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) v[u] = i0 + u * (int)blockDim.x < n ? src[g.start + i0 + u * blockDim.x] : 0;
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (i0 + u * (int)blockDim.x < n) {
+          sv[i0 + u * blockDim.x] = v[u];
+          a = v[u] < a ? v[u] : a;
+          b = v[u] > b ? v[u] : b;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, a, o), y = __shfl_xor_sync(0xffffffffu, b, o);
+      a = x < a ? x : a;
+      b = y > b ? y : b;
+    }
+    if (lane == 0) {
+      rmn[w] = a;
+      rmx[w] = b;
+    }
+    hist[t] = 0;
+    if (t == 0) big = 0;
     __syncthreads();
-    for (int k = 2; k <= P; k <<= 1)
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < P; i += blockDim.x) {
-          const int l = i ^ j;
-          if (l > i) {
-            const uint64_t a = sv[i], b = sv[l];
-            if ((a > b) == ((i & k) == 0)) {
-              sv[i] = b;
-              sv[l] = a;
+    a = rmn[0];
+    b = rmx[0];
+#pragma unroll
+    for (int q = 1; q < 8; q++) {
+      a = rmn[q] < a ? rmn[q] : a;
+      b = rmx[q] > b ? rmx[q] : b;
+    }
+    const int nsub = min(kSegSub, (n + 31) / 32);
+    const SegScale sc = seg_scale(a, b, nsub);
+    for (int i = t; i < n; i += blockDim.x) atomicAdd(&hist[seg_bin_of(sv[i], sc)], 1u);
+    __syncthreads();
+    // exclusive scan of the bin counts (one per thread)
+    const unsigned c = hist[t];
+    unsigned x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wtot[w] = x;
+    __syncthreads();
+    unsigned wb = 0;
+    for (int q = 0; q < w; q++) wb += wtot[q];
+    cur[t] = wb + x - c;
+    if (c > 256) big = 1;
+    __syncthreads();
+    if (!big) {
+      for (int i = t; i < n; i += blockDim.x) {
+        const uint64_t v = sv[i];
+        sb[atomicAdd(&cur[seg_bin_of(v, sc)], 1u)] = v;
+      }
+      __syncthreads();
+      for (int q = w; q < nsub; q += 8) {  // cur[q] is now the end of bin q
+        const int cq = (int)hist[q], s0 = (int)cur[q] - cq;
+        if (cq <= 1) continue;
+        if (cq <= 32)
+          warp_bitonic_run<1>(sb, sb, s0, cq, lane);
+        else if (cq <= 64)
+          warp_bitonic_run<2>(sb, sb, s0, cq, lane);
+        else if (cq <= 128)
+          warp_bitonic_run<4>(sb, sb, s0, cq, lane);
+        else
+          warp_bitonic_run<8>(sb, sb, s0, cq, lane);
+      }
+      __syncthreads();
+      for (int i = t; i < n; i += blockDim.x) lo_out[g.start + i] = sb[i];
+    } else {  // a bin too big for one warp: bitonic sort of the whole run
+      int P = 1;
+      while (P < n) P <<= 1;
+      for (int i = n + t; i < P; i += blockDim.x) sv[i] = ~0ULL;
+      __syncthreads();
+      for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = t; i < P; i += blockDim.x) {
+            const int l = i ^ j;
+            if (l > i) {
+              const uint64_t p = sv[i], q = sv[l];
+              if ((p > q) == ((i & k) == 0)) {
+                sv[i] = q;
+                sv[l] = p;
+              }
             }
           }
+          __syncthreads();
         }
-        __syncthreads();
-      }
-    for (int i = threadIdx.x; i < g.count; i += blockDim.x) lo_out[g.start + i] = sv[i];
+      for (int i = t; i < n; i += blockDim.x) lo_out[g.start + i] = sv[i];
+    }
     __syncthreads();
   }
 }
@@ -1145,7 +1267,7 @@ static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, 
                                       sg.large, sg.ctl, lo, (unsigned long long*)sg.mn, (unsigned long long*)sg.mx));
       EMU_LAUNCH("seg_binbase", s, k_seg_binbase<<<1, 32, 0, s>>>(sg.large, sg.ctl, sg.bbase, sg.bbase + hc.n_large));
       EMU_CUDA(cudaMemsetAsync(sg.bcnt, 0, sizeof(unsigned int) * sg.nbins_cap, s));
-      const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(256, (int64_t)kNumSMs * 8 / gy + 1));
+      const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(256, (int64_t)kNumSMs * 24 / gy + 1));
       const size_t bsm = 2 * kSegSmemBins * sizeof(unsigned int);
       EMU_CUDA(cudaFuncSetAttribute(k_seg_bins<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
       EMU_CUDA(cudaFuncSetAttribute(k_seg_bins<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
@@ -1167,8 +1289,8 @@ static int segment_dense(const H* hi, const uint64_t* lo, int64_t n, int cbits, 
     EMU_LAUNCH("seg_sort_small", s, k_seg_sort_small<<<kNumSMs * 12, 32 * kSegSmallWarps, 0, s>>>(sg.small, sg.ctl, lo,
                                                                                            sg.lo_out));
     EMU_CUDA(cudaFuncSetAttribute(k_seg_sort_medium, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kSegMedium * sizeof(uint64_t))));
-    EMU_LAUNCH("seg_sort_medium", s, k_seg_sort_medium<<<kNumSMs * 4, 256, kSegMedium * sizeof(uint64_t), s>>>(
+                                  (int)(2 * kSegMedium * sizeof(uint64_t))));
+    EMU_LAUNCH("seg_sort_medium", s, k_seg_sort_medium<<<kNumSMs * 3, 256, 2 * kSegMedium * sizeof(uint64_t), s>>>(
                                          sg.medium, sg.ctl, lo, sg.lo_out));
     EMU_CUDA(cudaMemcpyAsync(&hc, sg.ctl, sizeof(hc), cudaMemcpyDeviceToHost, s));
     EMU_CUDA(cudaStreamSynchronize(s));
@@ -1245,10 +1367,10 @@ static int sort_and_segment(const RecIn& r, int64_t n, bool canonical, int cbits
   // mixed inside a key) and place every sample directly (k_samples)
   const int lsb = canonical && dense && getenv("EMU_PHASE_SCAN") == nullptr ? 1 : 0;
   // key-first (canonical dense builds): sort by (key, phase) only, then each
-  // sub-run by latency in shared memory (EMU_BUILD_KF=1; default: all passes)
+  // sub-run by latency on chip (EMU_BUILD_KF=0: the full latency passes instead)
   static const bool kf_env = [] {
     const char* e = getenv("EMU_BUILD_KF");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   const bool kf = lsb && allow_kf && kf_env;
   SegScratch sg;

@@ -140,16 +140,17 @@ def test_gpu_build_shared_keys_merge():
             assert soa_equal(got, w)
 
 
-def test_gpu_build_key_first_mode():
-    """The key-first canonical build (EMU_BUILD_KF=1, read once per process):
-    every build test of this file again in a child process with it on."""
+def test_gpu_build_full_pass_mode():
+    """Canonical builds sort key-first by default; EMU_BUILD_KF=0 (read once per
+    process) gives the full latency + key radix passes: every build test of
+    this file again in a child process with it."""
     import subprocess
     import sys
 
     from conftest import ROOT
-    env = dict(os.environ, EMU_BUILD_KF="1")
+    env = dict(os.environ, EMU_BUILD_KF="0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "build and not key_first"],
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "build and not full_pass"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
