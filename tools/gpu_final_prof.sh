@@ -5,7 +5,7 @@ TAG=${TAG:-r2f}
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-extras > gpurun_out/launches_bench_$TAG.log 2>&1; echo launches rc=$?
 SWEEPS=3 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_mark|k_bits|k_pool|k_sample" -s 9 -c 9 -o gpurun_out/prof_cold_$TAG python tools/profile_sweep.py > gpurun_out/ncu_cold_$TAG.txt 2>&1; echo cold rc=$?
 EMU_SWEEP=1 SWEEPS=1 WARM=3 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_sweep" -s 2 -c 1 -o gpurun_out/prof_warm_$TAG python tools/profile_sweep.py > gpurun_out/ncu_warm_$TAG.txt 2>&1; echo warm rc=$?
-BUILDS=2 timeout 900 ncu --set full --clock-control none -k regex:"k_onesweep|k_dense_count|k_validate|k_make_keys|k_digit_hist" -s 13 -c 13 -o gpurun_out/prof_c4_$TAG python tools/c4_build.py > gpurun_out/ncu_c4_$TAG.txt 2>&1; echo c4 rc=$?
+BUILDS=2 timeout 900 ncu --set full --clock-control none -k regex:"k_onesweep|k_dense_count|k_validate|k_make_keys|k_digit_hist|k_seg_|k_samples" -s 15 -c 15 -o gpurun_out/prof_c4_$TAG python tools/c4_build.py > gpurun_out/ncu_c4_$TAG.txt 2>&1; echo c4 rc=$?
 Q=2000000 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pool_grp" -c 1 -o gpurun_out/prof_grp_$TAG python tools/c3_sweep.py > gpurun_out/ncu_grp_$TAG.txt 2>&1; echo grp rc=$?
 ls -la gpurun_out/*$TAG*
 # summaries on the box (the reports are too big to all come back)
