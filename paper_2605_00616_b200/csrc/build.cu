@@ -666,18 +666,25 @@ __global__ void __launch_bounds__(256) k_samples(const H* __restrict__ hi, const
 // each (key, phase) sub-run is then sorted by latency on its own.  Runs of
 // <= 256 records: one warp, bitonic sort held in registers; <= 4096: one CTA,
 // value bins of ~32 records in shared memory, each sorted by a warp the same
-// way; larger (the hot decode keys): split into bins of ~128 records (at most
-// 8192 bins) by the value's place between the sub-run's min and max
+// way; larger (the hot decode keys): split into bins of ~256 records (at most
+// 4096 bins) by the value's place between the sub-run's min and max
 // (monotone, so bins are ordered), scattered into place by two
 // shared-memory-histogram passes, and each bin sorted like a run.  A bin over
 // 4096 records (heavy ties, clustered values) sets a flag and the build falls
-// back to the full passes.  C4: 10.05 ms against 10.7 for the full passes.
+// back to the full passes.  C4: 9.7 ms against 10.7 for the full passes
+// (128-record bins: 10.05 ms; 512 and 1024 overflow and fall back).
 struct SegItem {
   int64_t start;  // first record of the run in the sorted-by-key order
   int32_t count;
   int32_t src1;   // 1: the run already sits in the output array (a bin), 0: read it from the key-sorted array
 };
-constexpr int kSegSmall = 256, kSegMedium = 4096, kSegBin = 128, kSegSmemBins = 8192;
+#ifndef EMU_SEG_BIN
+#define EMU_SEG_BIN 256
+#endif
+#ifndef EMU_SEG_MAXBINS
+#define EMU_SEG_MAXBINS 4096
+#endif
+constexpr int kSegSmall = 256, kSegMedium = 4096, kSegBin = EMU_SEG_BIN, kSegSmemBins = EMU_SEG_MAXBINS;
 // bins of a large sub-run: ~kSegBin records each, at most kSegSmemBins (shared-memory counters)
 __host__ __device__ __forceinline__ int64_t seg_nbins(int64_t c) {
   const int64_t nb = (c + kSegBin - 1) / kSegBin;
