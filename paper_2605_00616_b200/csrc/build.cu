@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(256) k_samples(const H* __restrict__ hi, const
 // (monotone, so bins are ordered), scattered into place by two
 // shared-memory-histogram passes, and each bin sorted like a run.  A bin over
 // 4096 records (heavy ties, clustered values) sets a flag and the build falls
-// back to the full passes.  C4: 9.7 ms against 10.7 for the full passes
+// back to the full passes.  C4: 9.6 ms against 10.7 for the full passes
 // (128-record bins: 10.05 ms; 512 and 1024 overflow and fall back).
 struct SegItem {
   int64_t start;  // first record of the run in the sorted-by-key order
@@ -940,12 +940,15 @@ __global__ void __launch_bounds__(32 * kSegSmallWarps) k_seg_sort_small(const Se
 }
 
 // One CTA per run of 257-4096 records: a bucket sort inside shared memory --
-// split the run into ~32-record value bins (min/max-normalised, monotone), then
+// split the run into ~24-record value bins (min/max-normalised, monotone), then
 // each bin sorted by one warp with the register bitonic; a bin over 256
 // records (ties, clustered values) sends the whole run to a shared-memory
 // bitonic sort instead.  (Holding the run in registers instead of a second
 // shared buffer, for 4 CTAs/SM instead of 3, measured slower: 3.1 vs 2.6 ms.)
-constexpr int kSegSub = 256;  // value bins per run at most
+#ifndef EMU_SEG_SUBT
+#define EMU_SEG_SUBT 24
+#endif
+constexpr int kSegSub = 256;  // value bins per run at most (~EMU_SEG_SUBT records each)
 __global__ void __launch_bounds__(256) k_seg_sort_medium(const SegItem* __restrict__ items, SegCtl* ctl,
                                                          const uint64_t* __restrict__ lo_in, uint64_t* lo_out) {
   extern __shared__ uint64_t sv[];  // [kSegMedium] the run, then [kSegMedium] the run in bin order
@@ -992,7 +995,7 @@ __global__ void __launch_bounds__(256) k_seg_sort_medium(const SegItem* __restri
       a = rmn[q] < a ? rmn[q] : a;
       b = rmx[q] > b ? rmx[q] : b;
     }
-    const int nsub = min(kSegSub, (n + 31) / 32);
+    const int nsub = min(kSegSub, (n + EMU_SEG_SUBT - 1) / EMU_SEG_SUBT);
     const SegScale sc = seg_scale(a, b, nsub);
     for (int i = t; i < n; i += blockDim.x) atomicAdd(&hist[seg_bin_of(sv[i], sc)], 1u);
     __syncthreads();
